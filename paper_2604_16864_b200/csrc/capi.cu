@@ -1,0 +1,483 @@
+// C-ABI entry points (include/hierasparse_b200.h): argument validation with the
+// reference's error taxonomy, pool sizing, TMA descriptor encoding, per-stream
+// workspaces and kernel launches.  No host synchronisation on the hot entry
+// points (hs_prune_compress, hs_decode*, hs_prefill).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+#include "../../include/hierasparse_b200.h"
+#include "kernels.h"
+
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launch_count{0};
+
+hs_status fail(hs_status code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define HS_CHECK_CONFIG(ok, ...) \
+    do {                         \
+        if (!(ok)) return fail(HS_ERR_CONFIG, __VA_ARGS__); \
+    } while (0)
+
+hs_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(HS_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------ TMA encode ---
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// A small always-valid device buffer backing descriptors of empty pools.
+void* dummy_buffer() {
+    static void* p = nullptr;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!p) {
+        if (cudaMalloc(&p, 1 << 16) != cudaSuccess) p = nullptr;
+        else cudaMemset(p, 0, 1 << 16);
+    }
+    return p;
+}
+
+// 2-D tile map over a row-major [outer][inner] 16-bit array.
+bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+              uint32_t box_outer, CUtensorMapSwizzle sw) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    if (ptr == nullptr || outer == 0) {
+        ptr = dummy_buffer();
+        outer = box_outer;
+        if (!ptr) return false;
+    }
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {inner * 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// ------------------------------------------------------------ workspaces ---
+struct Workspace {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+std::mutex g_ws_mu;
+std::map<std::tuple<int, cudaStream_t, int>, Workspace> g_ws;
+
+enum WsKind { kWsCompress = 0, kWsDecode = 1, kWsMisc = 2, kWsPrefill = 3 };
+
+// Per (device, stream, purpose) scratch; grows on demand and is zeroed on
+// (re)allocation (the decode arrival counters rely on that and self-reset).
+void* workspace(cudaStream_t s, size_t bytes, int kind, hs_status* st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace& w = g_ws[std::make_tuple(dev, s, kind)];
+    if (w.bytes < bytes) {
+        if (w.ptr) {
+            cudaStreamSynchronize(s);
+            cudaFree(w.ptr);
+        }
+        w.ptr = nullptr;
+        w.bytes = 0;
+        const size_t nb = bytes + (bytes >> 2) + 4096;
+        cudaError_t e = cudaMalloc(&w.ptr, nb);
+        if (e != cudaSuccess) {
+            *st = cuda_fail(e, "workspace allocation");
+            return nullptr;
+        }
+        w.bytes = nb;
+        e = cudaMemsetAsync(w.ptr, 0, nb, s);
+        if (e != cudaSuccess) {
+            *st = cuda_fail(e, "workspace clear");
+            return nullptr;
+        }
+    }
+    *st = HS_OK;
+    return w.ptr;
+}
+
+// -------------------------------------------------------------- geometry ---
+hs_status pool_counts(uint64_t rows, const hs_sparsity_config* cfg, double s, uint32_t* nb_out,
+                      uint32_t* dense, uint32_t* sparse, uint32_t* prefix_out, uint32_t* suffix_out,
+                      uint32_t* quota_out) {
+    HS_CHECK_CONFIG(cfg != nullptr, "SparsityConfig: null");
+    HS_CHECK_CONFIG(cfg->s_key >= 0.0 && cfg->s_key <= 1.0, "SparsityConfig: s_key outside [0, 1]");
+    HS_CHECK_CONFIG(cfg->s_value >= 0.0 && cfg->s_value <= 1.0, "SparsityConfig: s_value outside [0, 1]");
+    HS_CHECK_CONFIG(s >= 0.0 && s <= 1.0, "select_blocks: sparsity outside [0, 1]");
+    HS_CHECK_CONFIG(cfg->block_size > 0 && cfg->block_size % 4 == 0,
+                    "SparsityConfig: block_size must be a positive multiple of m_group");
+    HS_CHECK_CONFIG(rows % cfg->block_size == 0,
+                    "prune_cache: sequence length not divisible by block_size");
+    const uint64_t nb = rows / cfg->block_size;
+    // masks.hpp:93-98 rounding, pruner.hpp:130-131 clamping.
+    uint64_t p = (cfg->sink_tokens + cfg->block_size - 1) / cfg->block_size;
+    uint64_t q = (cfg->local_window + cfg->block_size - 1) / cfg->block_size;
+    if (p > nb) p = nb;
+    if (q > nb - p) q = nb - p;
+    const uint64_t prunable = nb - p - q;
+    const uint64_t quota = static_cast<uint64_t>(floor(s * static_cast<double>(prunable)));
+    HS_CHECK_CONFIG(nb - quota <= 32767, "compress: dense pool exceeds int16 index capacity");
+    HS_CHECK_CONFIG(quota <= 32767, "compress: sparse pool exceeds int16 index capacity");
+    if (nb_out) *nb_out = static_cast<uint32_t>(nb);
+    if (dense) *dense = static_cast<uint32_t>(nb - quota);
+    if (sparse) *sparse = static_cast<uint32_t>(quota);
+    if (prefix_out) *prefix_out = static_cast<uint32_t>(p);
+    if (suffix_out) *suffix_out = static_cast<uint32_t>(q);
+    if (quota_out) *quota_out = static_cast<uint32_t>(quota);
+    return HS_OK;
+}
+
+hs_status check_device_cache(const hs_device_cache* c, const char* what) {
+    HS_CHECK_CONFIG(c != nullptr, "%s: null cache", what);
+    HS_CHECK_CONFIG(c->dtype == HS_DTYPE_BF16 || c->dtype == HS_DTYPE_F16, "%s: unsupported dtype", what);
+    HS_CHECK_CONFIG(c->block_size == hs::kBlock, "%s: device kernels need block_size 64", what);
+    HS_CHECK_CONFIG(c->head_dim == hs::kHeadDim, "%s: device kernels need head_dim 128", what);
+    HS_CHECK_CONFIG(c->n_units >= 1, "%s: n_units must be positive", what);
+    HS_CHECK_CONFIG(c->dense_count + c->sparse_count == c->logical_blocks,
+                    "%s: pool counts do not cover the block map", what);
+    HS_CHECK_CONFIG(c->dense_count <= 32767 && c->sparse_count <= 32767,
+                    "%s: pool exceeds int16 index capacity", what);
+    HS_CHECK_CONFIG(c->logical_blocks == 0 || c->index_map != nullptr, "%s: null index map", what);
+    HS_CHECK_CONFIG(c->dense_count == 0 || c->dense_pool != nullptr, "%s: null dense pool", what);
+    HS_CHECK_CONFIG(c->sparse_count == 0 || (c->nnz_pool && c->meta_pool), "%s: null sparse pools", what);
+    return HS_OK;
+}
+
+hs_status check_pair(const hs_device_cache* k, const hs_device_cache* v) {
+    hs_status st;
+    if ((st = check_device_cache(k, "key cache"))) return st;
+    if ((st = check_device_cache(v, "value cache"))) return st;
+    HS_CHECK_CONFIG(k->axis == HS_AXIS_CHANNEL, "attention: key cache must be channel-grouped");
+    HS_CHECK_CONFIG(v->axis == HS_AXIS_SEQUENCE, "attention: value cache must be sequence-grouped");
+    HS_CHECK_CONFIG(k->logical_blocks == v->logical_blocks, "attention: key/value block counts differ");
+    HS_CHECK_CONFIG(k->block_size == v->block_size, "attention: key/value block sizes differ");
+    HS_CHECK_CONFIG(k->n_units == v->n_units, "attention: key/value unit counts differ");
+    HS_CHECK_CONFIG(k->dtype == v->dtype, "attention: key/value dtypes differ");
+    return HS_OK;
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// Split count: fill the machine (decode_ctas_per_sm CTAs per SM) with balanced ranges.
+int choose_splits(int n_units, int nb) {
+    const int slots = hs::decode_ctas_per_sm() * sm_count();
+    int best = 1;
+    double best_cost = 1e30;
+    for (int s = 1; s <= nb && s <= 256; ++s) {
+        const int ctas = n_units * s;
+        const int waves = (ctas + slots - 1) / slots;
+        const double per_cta = static_cast<double>(nb) / s;  // blocks per CTA
+        // wave-quantised time + per-CTA fixed overhead (~2 blocks) + combine cost
+        const double cost = waves * (per_cta + 2.0) + 0.02 * s;
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = s;
+        }
+    }
+    return best;
+}
+
+hs_status fill_decode_maps(hs::DecodeLaunch& L, const hs_device_cache* k, const hs_device_cache* v) {
+    const uint64_t U = k->n_units;
+    bool ok = true;
+    ok &= make_map(&L.tm_knnz, k->nnz_pool, 64, U * k->sparse_count * 64, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_map(&L.tm_kden, k->dense_pool, 128, U * k->dense_count * 64, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_map(&L.tm_vnnz, v->nnz_pool, 32, U * v->sparse_count * 128, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
+    ok &= make_map(&L.tm_vden, v->dense_pool, 64, U * v->dense_count * 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (!ok) return fail(HS_ERR_CUDA, "cuTensorMapEncodeTiled failed (driver entry point unavailable?)");
+    return HS_OK;
+}
+
+void count_launch(int n = 1) { g_launch_count.fetch_add(n); }
+
+}  // namespace
+
+extern "C" {
+
+HS_API const char* hs_last_error(void) { return g_err.c_str(); }
+HS_API int hs_version(void) { return 1; }
+HS_API uint64_t hs_kernel_launches(void) { return g_launch_count.load(); }
+
+HS_API hs_status hs_pool_counts(uint64_t rows, const hs_sparsity_config* cfg, double sparsity,
+                                uint32_t* logical_blocks, uint32_t* dense_count,
+                                uint32_t* sparse_count, uint32_t* prefix_blocks,
+                                uint32_t* suffix_blocks) {
+    return pool_counts(rows, cfg, sparsity, logical_blocks, dense_count, sparse_count, prefix_blocks,
+                       suffix_blocks, nullptr);
+}
+
+HS_API hs_status hs_cache_bytes(const hs_device_cache* c, uint64_t* index_bytes, uint64_t* dense_bytes,
+                                uint64_t* nnz_bytes, uint64_t* meta_bytes, uint64_t* slot_block_bytes) {
+    HS_CHECK_CONFIG(c != nullptr, "hs_cache_bytes: null cache");
+    const uint64_t U = c->n_units, be = static_cast<uint64_t>(c->block_size) * c->head_dim;
+    if (index_bytes) *index_bytes = U * c->logical_blocks * 2;
+    if (dense_bytes) *dense_bytes = U * c->dense_count * be * 2;
+    if (nnz_bytes) *nnz_bytes = U * c->sparse_count * be;
+    if (meta_bytes) *meta_bytes = U * c->sparse_count * be / 8;
+    if (slot_block_bytes) *slot_block_bytes = U * c->logical_blocks * 4;
+    return HS_OK;
+}
+
+HS_API hs_status hs_prune_compress(const void* src, uint64_t src_unit_stride, uint64_t rows,
+                                   const hs_sparsity_config* cfg, double sparsity,
+                                   hs_device_cache* out, double* losses, uint8_t* flags,
+                                   void* stream) {
+    HS_CHECK_CONFIG(out != nullptr && src != nullptr, "prune_cache: null argument");
+    uint32_t nb, dc, sc, pre, suf, quota;
+    hs_status st = pool_counts(rows, cfg, sparsity, &nb, &dc, &sc, &pre, &suf, &quota);
+    if (st) return st;
+    HS_CHECK_CONFIG(out->head_dim % 4 == 0, "prune_cache: head dimension not divisible by m_group");
+    HS_CHECK_CONFIG(cfg->block_size == hs::kBlock, "prune_cache: device kernels need block_size 64");
+    HS_CHECK_CONFIG(out->block_size == cfg->block_size, "prune_cache: cache block size mismatch");
+    HS_CHECK_CONFIG(out->logical_blocks == nb, "prune_cache: cache block count %u != %u", out->logical_blocks, nb);
+    HS_CHECK_CONFIG(out->dense_count == dc && out->sparse_count == sc,
+                    "prune_cache: pool counts (%u, %u) do not match the selection (%u, %u)",
+                    out->dense_count, out->sparse_count, dc, sc);
+    if ((st = check_device_cache(out, "prune_cache"))) return st;
+    HS_CHECK_CONFIG(out->n_units == 1 || src_unit_stride >= rows * out->head_dim,
+                    "prune_cache: unit stride too small");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool static_sel = quota == 0 || quota == nb - pre - suf;
+    hs::CompressLaunch L{};
+    L.bf16 = out->dtype == HS_DTYPE_BF16;
+    L.axis = out->axis;
+    L.n_units = out->n_units;
+    L.nb = nb;
+    L.dense_count = dc;
+    L.sparse_count = sc;
+    L.prefix = pre;
+    L.suffix = suf;
+    L.quota = quota;
+    L.static_selection = static_sel;
+    L.all_sparse = quota > 0;
+    L.src = src;
+    L.src_unit_stride = src_unit_stride;
+    L.flags_out = flags;
+    L.losses = losses;
+    L.index_map = out->index_map;
+    L.slot_block = out->slot_block;
+    L.dense_pool = out->dense_pool;
+    L.nnz_pool = out->nnz_pool;
+    L.meta_pool = out->meta_pool;
+    if (nb == 0) return HS_OK;
+    if (!static_sel) {
+        const size_t need_l = losses ? 0 : static_cast<size_t>(out->n_units) * nb * sizeof(double);
+        const size_t need = need_l + static_cast<size_t>(out->n_units) * nb + 256;
+        uint8_t* ws = static_cast<uint8_t*>(workspace(s, need, kWsCompress, &st));
+        if (st) return st;
+        if (!losses) L.losses = reinterpret_cast<double*>(ws);
+        L.flags_tmp = ws + need_l;
+    }
+    cudaError_t e = hs::launch_prune_compress(L, s);
+    count_launch(static_sel ? 2 : 4);
+    if (e != cudaSuccess) return cuda_fail(e, "prune_compress launch");
+    return HS_OK;
+}
+
+HS_API hs_status hs_compress_with_flags(const void* src, uint64_t src_unit_stride, uint64_t rows,
+                                        const uint8_t* flags, hs_device_cache* out, void* stream) {
+    HS_CHECK_CONFIG(out != nullptr && src != nullptr && flags != nullptr, "compress: null argument");
+    HS_CHECK_CONFIG(out->block_size == hs::kBlock, "compress: device kernels need block_size 64");
+    HS_CHECK_CONFIG(rows % out->block_size == 0, "compress: sequence length not divisible by block_size");
+    const uint32_t nb = static_cast<uint32_t>(rows / out->block_size);
+    HS_CHECK_CONFIG(out->logical_blocks == nb, "compress: block mask does not cover the sequence");
+    hs_status st = check_device_cache(out, "compress");
+    if (st) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // Validate the pool counts against the mask (host read; off the hot path).
+    std::vector<uint8_t> hf(static_cast<size_t>(out->n_units) * nb);
+    cudaError_t e = cudaMemcpyAsync(hf.data(), flags, hf.size(), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "compress: reading the block mask");
+    for (uint32_t u = 0; u < out->n_units; ++u) {
+        uint32_t d = 0;
+        for (uint32_t b = 0; b < nb; ++b) d += hf[static_cast<size_t>(u) * nb + b] != 0;
+        HS_CHECK_CONFIG(d == out->dense_count, "compress: unit %u has %u dense blocks, cache holds %u", u, d,
+                        out->dense_count);
+    }
+    hs::CompressLaunch L{};
+    L.bf16 = out->dtype == HS_DTYPE_BF16;
+    L.axis = out->axis;
+    L.n_units = out->n_units;
+    L.nb = nb;
+    L.dense_count = out->dense_count;
+    L.sparse_count = out->sparse_count;
+    L.src = src;
+    L.src_unit_stride = src_unit_stride;
+    L.flags_in = flags;
+    L.index_map = out->index_map;
+    L.slot_block = out->slot_block;
+    L.dense_pool = out->dense_pool;
+    L.nnz_pool = out->nnz_pool;
+    L.meta_pool = out->meta_pool;
+    if (nb == 0) return HS_OK;
+    e = hs::launch_prune_compress(L, s);
+    count_launch(2);
+    if (e != cudaSuccess) return cuda_fail(e, "compress launch");
+    return HS_OK;
+}
+
+HS_API hs_status hs_decompress(const hs_device_cache* c, void* dst, void* stream) {
+    hs_status st = check_device_cache(c, "decompress");
+    if (st) return st;
+    HS_CHECK_CONFIG(dst != nullptr, "decompress: null destination");
+    if (c->logical_blocks == 0) return HS_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int* bad = static_cast<int*>(workspace(s, 64, kWsMisc, &st));
+    if (st) return st;
+    cudaMemsetAsync(bad, 0, sizeof(int), s);
+    hs::DecompressLaunch L{c->axis, static_cast<int>(c->n_units), static_cast<int>(c->logical_blocks),
+                           static_cast<int>(c->dense_count), static_cast<int>(c->sparse_count),
+                           c->index_map, c->dense_pool, c->nnz_pool, c->meta_pool, dst, bad};
+    cudaError_t e = hs::launch_decompress(L, s);
+    count_launch();
+    if (e != cudaSuccess) return cuda_fail(e, "decompress launch");
+    int hbad = 0;
+    e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "decompress");
+    if (hbad == 1) return fail(HS_ERR_DATA, "decompress: index map holds a zero or dangling entry");
+    if (hbad == 2) return fail(HS_ERR_DATA, "unpack_metadata: corrupt metadata, codes not increasing");
+    return HS_OK;
+}
+
+static hs_status decode_common(const void* q, const hs_device_cache* k, const hs_device_cache* v,
+                               const void* k_tail, const void* v_tail, uint32_t tail, uint32_t gqa,
+                               float scale, uint32_t splits, uint32_t block_begin, uint32_t block_end,
+                               int include_tail, float* out, int out_mode, void* stream) {
+    hs_status st = check_pair(k, v);
+    if (st) return st;
+    HS_CHECK_CONFIG(q != nullptr && out != nullptr, "decode_attention: null argument");
+    HS_CHECK_CONFIG(gqa >= 1, "decode_attention: no query rows");
+    HS_CHECK_CONFIG(gqa <= 8, "decode_attention: device kernel supports up to 8 query rows per KV head");
+    HS_CHECK_CONFIG(tail == 0 || (k_tail && v_tail), "decode_attention: null dense tail");
+    HS_CHECK_CONFIG(static_cast<uint64_t>(k->logical_blocks) * k->block_size + tail > 0,
+                    "decode_attention: empty cache");
+    HS_CHECK_CONFIG(block_begin <= block_end && block_end <= k->logical_blocks,
+                    "attend_range: block range out of bounds");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    hs::DecodeLaunch L{};
+    L.bf16 = k->dtype == HS_DTYPE_BF16;
+    L.n_units = k->n_units;
+    L.nb = k->logical_blocks;
+    L.gqa = gqa;
+    L.tail = tail;
+    L.k_dense_count = k->dense_count;
+    L.k_sparse_count = k->sparse_count;
+    L.v_dense_count = v->dense_count;
+    L.v_sparse_count = v->sparse_count;
+    L.scale_log2 = scale * 1.4426950408889634f;
+    L.q = q;
+    L.k_index = k->index_map;
+    L.v_index = v->index_map;
+    L.k_meta = k->meta_pool;
+    L.v_meta = v->meta_pool;
+    L.k_tail = k_tail;
+    L.v_tail = v_tail;
+    L.block_begin = block_begin;
+    L.block_end = block_end;
+    L.include_tail = include_tail;
+    const int span = static_cast<int>(block_end - block_begin);
+    int ns = splits ? static_cast<int>(splits) : choose_splits(L.n_units, span);
+    if (ns > span) ns = span;  // attention.hpp:373-374 clamp
+    if (ns < 1) ns = 1;
+    L.nsplit = ns;
+    if ((st = fill_decode_maps(L, k, v))) return st;
+    const size_t part_bytes = static_cast<size_t>(L.n_units) * ns * gqa * (hs::kHeadDim + 2) * sizeof(float);
+    const size_t cnt_bytes = ((static_cast<size_t>(L.n_units) * sizeof(int) + 255) / 256) * 256;
+    uint8_t* ws = static_cast<uint8_t*>(workspace(s, cnt_bytes + part_bytes, kWsDecode, &st));
+    if (st) return st;
+    L.counters = reinterpret_cast<int*>(ws);
+    L.partial = reinterpret_cast<float*>(ws + cnt_bytes);
+    L.out = out;
+    L.out_mode = out_mode;
+    cudaError_t e = hs::launch_decode(L, s);
+    count_launch();
+    if (e != cudaSuccess) return cuda_fail(e, "decode launch");
+    return HS_OK;
+}
+
+HS_API hs_status hs_decode(const void* q, const hs_device_cache* k, const hs_device_cache* v,
+                           const void* k_tail, const void* v_tail, uint32_t tail, uint32_t gqa,
+                           float scale, uint32_t splits, float* out, void* stream) {
+    HS_CHECK_CONFIG(k != nullptr, "decode_attention: null key cache");
+    return decode_common(q, k, v, k_tail, v_tail, tail, gqa, scale, splits, 0, k->logical_blocks, 1, out, 0,
+                         stream);
+}
+
+HS_API hs_status hs_decode_partial(const void* q, const hs_device_cache* k, const hs_device_cache* v,
+                                   const void* k_tail, const void* v_tail, uint32_t tail, uint32_t gqa,
+                                   float scale, uint32_t block_begin, uint32_t block_end, int include_tail,
+                                   float* partial, void* stream) {
+    return decode_common(q, k, v, k_tail, v_tail, tail, gqa, scale, 0, block_begin, block_end, include_tail,
+                         partial, 1, stream);
+}
+
+HS_API hs_status hs_decode_combine(const float* partials, uint32_t n_parts, uint32_t n_units, uint32_t gqa,
+                                   uint32_t d, float* out, void* stream) {
+    HS_CHECK_CONFIG(partials && out, "decode_combine: null argument");
+    HS_CHECK_CONFIG(n_parts >= 1 && n_units >= 1 && gqa >= 1 && d >= 1, "decode_combine: empty shape");
+    cudaError_t e = hs::launch_combine(partials, n_parts, n_units, gqa, d, out, static_cast<cudaStream_t>(stream));
+    count_launch();
+    if (e != cudaSuccess) return cuda_fail(e, "combine launch");
+    return HS_OK;
+}
+
+HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_device_cache* k,
+                            const hs_device_cache* v, const void* k_tail, const void* v_tail, uint32_t tail,
+                            int causal, float scale, float* out, void* stream) {
+    (void)q; (void)n_q; (void)gqa; (void)k; (void)v; (void)k_tail; (void)v_tail; (void)tail;
+    (void)causal; (void)scale; (void)out; (void)stream;
+    return fail(HS_ERR_CONFIG, "prefill_attention: device kernel not built yet");
+}
+
+}  // extern "C"

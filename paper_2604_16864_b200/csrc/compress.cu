@@ -1,0 +1,471 @@
+// Hierarchical pruning + pooled 2:4 compression on B200 (HBM-bound integer /
+// byte work, no tensor cores).
+//
+// Reference contract (bit-exact): pruner.hpp:40-176 (element_mask, block_loss,
+// select_blocks, hierarchical_mask_for) and compressed_cache.hpp:133-267
+// (assemble_cache, fused_magnitude_compress).  Pipeline per cache kind:
+//
+//   static selection (quota 0 or all prunable, known on the host):
+//     assign_slots  -> pack<with losses>                    (source read once)
+//   loss-driven selection (0 < quota < prunable):
+//     classify (losses) -> rank (flags) -> assign_slots -> pack
+//
+// Layout: source [unit][rows][d] token-major 16-bit.  One CTA per 64x128 block
+// (16 KB): 16-byte vector loads, coalesced stores of the stored layouts.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hs {
+namespace {
+
+constexpr int kThreads = 256;
+
+// Top-2-of-4 by magnitude with the stable-sort tie rule (pruner.hpp:53-74):
+// element i is kept iff #{j: |x_j|>|x_i|} + #{j<i: |x_j|==|x_i|} < 2.
+// Returns the 4-bit keep mask.
+__device__ __forceinline__ uint32_t keep_mask4(uint32_t m0, uint32_t m1, uint32_t m2,
+                                               uint32_t m3) {
+    const uint32_t r0 = (m1 > m0) + (m2 > m0) + (m3 > m0);
+    const uint32_t r1 = (m0 >= m1) + (m2 > m1) + (m3 > m1);
+    const uint32_t r2 = (m0 >= m2) + (m1 >= m2) + (m3 > m2);
+    const uint32_t r3 = (m0 >= m3) + (m1 >= m3) + (m2 >= m3);
+    return (r0 < 2) | ((r1 < 2) << 1) | ((r2 < 2) << 2) | ((r3 < 2) << 3);
+}
+
+// Canonical 4-bit group code (nm_metadata.hpp:42-46, :81-83): first kept
+// position in the low 2 bits.  Also returns the two kept positions.
+__device__ __forceinline__ uint32_t group_code(uint32_t keep, uint32_t& p0, uint32_t& p1) {
+    p0 = __ffs(keep) - 1;
+    p1 = __ffs(keep & (keep - 1)) - 1;
+    return p0 | (p1 << 2);
+}
+
+// Exact-loss bookkeeping.  Every 16-bit float is M * 2^e with integer M below
+// 2^(mant+1); a double sum of such terms is exact in any order while the total
+// stays below 2^(53 + e_min), and then equals the reference's sequential double
+// sum bit for bit (pruner.hpp:85-87).  We track e_min/e_max of the nonzero
+// pruned terms and fall back to a sequential sum when the bound can fail.
+template <typename T>
+__device__ __forceinline__ int unit_exp(uint32_t mag) {
+    constexpr int mant = F16Traits<T>::kMantBits;
+    const int E = static_cast<int>(mag >> mant);
+    return (E ? E : 1) - F16Traits<T>::kExpBias - mant;
+}
+
+struct LossAcc {
+    double sum = 0.0;
+    int emin = 1 << 20;
+    int emax = -(1 << 20);
+};
+
+template <typename T>
+__device__ __forceinline__ void loss_add(LossAcc& a, uint16_t bits) {
+    const uint32_t mag = mag16(bits);
+    if (mag == 0) return;
+    const int e = unit_exp<T>(mag);
+    a.emin = min(a.emin, e);
+    a.emax = max(a.emax, e);
+    a.sum += fabs(static_cast<double>(F16Traits<T>::to_float(bits)));
+}
+
+// Reduce LossAcc across the CTA; thread 0 gets the totals.  Returns true on
+// thread 0 when the exactness bound holds.
+template <typename T>
+__device__ bool loss_reduce(LossAcc& a, double* s_sum, int* s_emin, int* s_emax) {
+    for (int o = 16; o > 0; o >>= 1) {
+        a.sum += __shfl_xor_sync(0xffffffffu, a.sum, o);
+        a.emin = min(a.emin, __shfl_xor_sync(0xffffffffu, a.emin, o));
+        a.emax = max(a.emax, __shfl_xor_sync(0xffffffffu, a.emax, o));
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_sum[w] = a.sum;
+        s_emin[w] = a.emin;
+        s_emax[w] = a.emax;
+    }
+    __syncthreads();
+    bool exact = false;
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        int lo = 1 << 20, hi = -(1 << 20);
+        for (int i = 0; i < kThreads / 32; ++i) {
+            s += s_sum[i];
+            lo = min(lo, s_emin[i]);
+            hi = max(hi, s_emax[i]);
+        }
+        a.sum = s;
+        // terms < 2^(mant+1) units each, at most B*d/2 = 2^12 terms.
+        constexpr int kMBits = F16Traits<T>::kMantBits + 1;
+        exact = (hi < lo) || (hi - lo) + kMBits + 12 <= 53;
+    }
+    return exact;
+}
+
+// g[p] for p in [0, 4) without local-memory indexing.
+__device__ __forceinline__ uint32_t pick4(uint16_t g0, uint16_t g1, uint16_t g2, uint16_t g3, uint32_t p) {
+    return p == 0 ? g0 : (p == 1 ? g1 : (p == 2 ? g2 : g3));
+}
+
+__device__ __forceinline__ const uint16_t* unit_src(const uint16_t* src, uint64_t stride, int u) {
+    return src + static_cast<uint64_t>(u) * stride;
+}
+
+// Sequential reference-order loss (pruner.hpp:85-87) for the rare blocks whose
+// exponent spread defeats the exact-sum bound.  Logical row-major order.
+template <typename T, int AXIS>
+__device__ double sequential_loss(const uint16_t* blk /*[64][128] logical*/) {
+    double loss = 0.0;
+    for (int r = 0; r < kBlock; ++r) {
+        for (int c = 0; c < kHeadDim; ++c) {
+            uint32_t m[4];
+            int pos;
+            if (AXIS == 0) {
+                const int g0 = c & ~3;
+                for (int i = 0; i < 4; ++i) m[i] = mag16(blk[r * kHeadDim + g0 + i]);
+                pos = c & 3;
+            } else {
+                const int r0 = r & ~3;
+                for (int i = 0; i < 4; ++i) m[i] = mag16(blk[(r0 + i) * kHeadDim + c]);
+                pos = r & 3;
+            }
+            const uint32_t keep = keep_mask4(m[0], m[1], m[2], m[3]);
+            if (!((keep >> pos) & 1u))
+                loss += fabs(static_cast<double>(F16Traits<T>::to_float(blk[r * kHeadDim + c])));
+        }
+    }
+    return loss;
+}
+
+// ---------------------------------------------------------------------------
+// Per-block work.  MODE: 0 = losses only (classify), 1 = pack, 2 = pack + losses.
+// ---------------------------------------------------------------------------
+struct PackArgs {
+    const uint16_t* src;
+    uint64_t src_stride;      // elements per unit
+    int nb;
+    int dense_count;
+    int sparse_count;
+    const int16_t* index_map; // [u][nb] (modes 1, 2)
+    uint16_t* dense_pool;
+    uint16_t* nnz_pool;
+    uint16_t* meta_pool;
+    double* losses;           // [u][nb] (modes 0, 2)
+};
+
+template <typename T, int AXIS, int MODE>
+__global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
+    const int b = blockIdx.x, u = blockIdx.y, t = threadIdx.x;
+    const uint16_t* blk = unit_src(a.src, a.src_stride, u) + static_cast<uint64_t>(b) * kBlock * kHeadDim;
+    __shared__ double s_sum[kThreads / 32];
+    __shared__ int s_emin[kThreads / 32], s_emax[kThreads / 32];
+
+    bool dense = false;
+    int slot = 0;
+    if (MODE != 0) {
+        const int e = a.index_map[static_cast<int64_t>(u) * a.nb + b];
+        dense = e > 0;
+        slot = (e > 0 ? e : -e) - 1;
+    }
+    constexpr bool kLoss = MODE != 1;
+    LossAcc acc;
+
+    if (AXIS == 0) {
+        // Key cache: groups of 4 channels along a token row, stored layout = logical.
+        const int c = t & 15;  // 16-byte chunk: channels 8c..8c+7 (groups 2c, 2c+1)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const int r = p * 16 + (t >> 4);
+            const uint4 v = *reinterpret_cast<const uint4*>(blk + r * kHeadDim + c * 8);
+            if (MODE != 0 && dense) {
+                uint16_t* dst = a.dense_pool + (static_cast<uint64_t>(u) * a.dense_count + slot) * (kBlock * kHeadDim);
+                *reinterpret_cast<uint4*>(dst + r * kHeadDim + c * 8) = v;
+            }
+            if (MODE == 1 && dense) continue;
+            const uint16_t x[8] = {
+                (uint16_t)(v.x & 0xFFFF), (uint16_t)(v.x >> 16), (uint16_t)(v.y & 0xFFFF), (uint16_t)(v.y >> 16),
+                (uint16_t)(v.z & 0xFFFF), (uint16_t)(v.z >> 16), (uint16_t)(v.w & 0xFFFF), (uint16_t)(v.w >> 16)};
+            uint32_t kept_vals[4];
+            uint32_t meta_byte = 0;
+#pragma unroll
+            for (int gi = 0; gi < 2; ++gi) {
+                const uint16_t* g = x + 4 * gi;
+                const uint32_t keep = keep_mask4(mag16(g[0]), mag16(g[1]), mag16(g[2]), mag16(g[3]));
+                uint32_t p0, p1;
+                meta_byte |= group_code(keep, p0, p1) << (4 * gi);
+                kept_vals[2 * gi] = pick4(g[0], g[1], g[2], g[3], p0);
+                kept_vals[2 * gi + 1] = pick4(g[0], g[1], g[2], g[3], p1);
+                if (kLoss) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (!((keep >> i) & 1u)) loss_add<T>(acc, g[i]);
+                }
+            }
+            if (MODE != 0 && !dense) {
+                const uint64_t sb = static_cast<uint64_t>(u) * a.sparse_count + slot;
+                uint16_t* nnz = a.nnz_pool + sb * (kBlock * kHeadDim / 2);
+                *reinterpret_cast<uint2*>(nnz + r * (kHeadDim / 2) + c * 4) =
+                    make_uint2(kept_vals[0] | (kept_vals[1] << 16), kept_vals[2] | (kept_vals[3] << 16));
+                uint8_t* meta = reinterpret_cast<uint8_t*>(a.meta_pool + sb * (kBlock * kHeadDim / 16));
+                meta[r * (kHeadDim / 8) + c] = static_cast<uint8_t>(meta_byte);
+            }
+        }
+    } else {
+        // Value cache: groups of 4 tokens down a channel; stored transposed [d][B].
+        __shared__ __align__(16) uint16_t tile[kBlock * kHeadDim];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int chunk = t + i * kThreads;  // 1024 chunks of 8 elements
+            reinterpret_cast<uint4*>(tile)[chunk] = reinterpret_cast<const uint4*>(blk)[chunk];
+        }
+        __syncthreads();
+        const int c = t & 127;  // channel
+        const int h = t >> 7;   // token half: groups 8h..8h+7
+        if (MODE != 0 && dense) {
+            uint16_t* dst = a.dense_pool + (static_cast<uint64_t>(u) * a.dense_count + slot) * (kBlock * kHeadDim) +
+                            c * kBlock + 32 * h;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t w[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = 32 * h + 8 * q + 2 * j;
+                    w[j] = tile[r * kHeadDim + c] | (static_cast<uint32_t>(tile[(r + 1) * kHeadDim + c]) << 16);
+                }
+                reinterpret_cast<uint4*>(dst)[q] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+        if (!(MODE == 1 && dense)) {
+            uint32_t vals[8];
+            uint32_t meta = 0;
+#pragma unroll
+            for (int gi = 0; gi < 8; ++gi) {
+                const int r0 = 32 * h + 4 * gi;
+                uint16_t g[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) g[i] = tile[(r0 + i) * kHeadDim + c];
+                const uint32_t keep = keep_mask4(mag16(g[0]), mag16(g[1]), mag16(g[2]), mag16(g[3]));
+                uint32_t p0, p1;
+                meta |= group_code(keep, p0, p1) << (4 * gi);
+                vals[gi] = pick4(g[0], g[1], g[2], g[3], p0) | (pick4(g[0], g[1], g[2], g[3], p1) << 16);
+                if (kLoss) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (!((keep >> i) & 1u)) loss_add<T>(acc, g[i]);
+                }
+            }
+            if (MODE != 0 && !dense) {
+                const uint64_t sb = static_cast<uint64_t>(u) * a.sparse_count + slot;
+                uint16_t* nnz = a.nnz_pool + sb * (kBlock * kHeadDim / 2) + c * (kBlock / 2) + 16 * h;
+                reinterpret_cast<uint4*>(nnz)[0] = make_uint4(vals[0], vals[1], vals[2], vals[3]);
+                reinterpret_cast<uint4*>(nnz)[1] = make_uint4(vals[4], vals[5], vals[6], vals[7]);
+                uint16_t* mp = a.meta_pool + sb * (kBlock * kHeadDim / 16) + c * (kBlock / 16) + 2 * h;
+                *reinterpret_cast<uint32_t*>(mp) = meta;
+            }
+        }
+    }
+
+    if (kLoss) {
+        const bool exact = loss_reduce<T>(acc, s_sum, s_emin, s_emax);
+        if (t == 0) {
+            double loss = acc.sum;
+            if (!exact) loss = sequential_loss<T, AXIS>(blk);
+            a.losses[static_cast<int64_t>(u) * a.nb + b] = loss;
+        }
+    }
+}
+
+// select_blocks (pruner.hpp:94-117) as a rank: block i (prunable) is sparse iff
+// #{j prunable: L_j < L_i or (L_j == L_i and j < i)} < quota.
+__global__ void __launch_bounds__(256) rank_kernel(const double* losses, int nb, int prefix,
+                                                   int suffix, int quota, uint8_t* flags) {
+    const int u = blockIdx.y;
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    const double* L = losses + static_cast<int64_t>(u) * nb;
+    __shared__ double tile[1024];
+    const int lo = prefix, hi = nb - suffix;
+    const double li = (i < nb) ? L[i] : 0.0;
+    int rank = 0;
+    for (int j0 = lo; j0 < hi; j0 += 1024) {
+        __syncthreads();
+        for (int j = threadIdx.x; j < 1024 && j0 + j < hi; j += 256) tile[j] = L[j0 + j];
+        __syncthreads();
+        const int n = min(1024, hi - j0);
+        for (int j = 0; j < n; ++j) {
+            const double lj = tile[j];
+            rank += (lj < li) || (lj == li && j0 + j < i);
+        }
+    }
+    if (i < nb) {
+        const bool prunable = i >= lo && i < hi;
+        flags[static_cast<int64_t>(u) * nb + i] = (prunable && rank < quota) ? 0 : 1;
+    }
+}
+
+// Slot assignment in block order (assemble_cache, compressed_cache.hpp:156-185):
+// index_map = +(dense rank + 1) or -(sparse rank + 1); slot_block inverts it.
+// flags_in == nullptr selects the static pattern (protected dense, prunable
+// sparse iff all_sparse).
+__global__ void __launch_bounds__(1024) assign_slots_kernel(const uint8_t* flags_in, int nb,
+                                                            int prefix, int suffix, int all_sparse,
+                                                            int dense_count, int16_t* index_map,
+                                                            int32_t* slot_block, uint8_t* flags_out) {
+    const int u = blockIdx.x, t = threadIdx.x;
+    const int per = (nb + 1023) / 1024;
+    const int b0 = min(nb, t * per), b1 = min(nb, b0 + per);
+    auto flag_of = [&](int b) -> int {
+        if (flags_in) return flags_in[static_cast<int64_t>(u) * nb + b] != 0;
+        const bool prot = b < prefix || b >= nb - suffix;
+        return prot || !all_sparse;
+    };
+    int nd = 0;
+    for (int b = b0; b < b1; ++b) nd += flag_of(b);
+    // block exclusive scan of nd
+    __shared__ int warp_sums[32];
+    int x = nd;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if ((t & 31) >= o) x += y;
+    }
+    if ((t & 31) == 31) warp_sums[t >> 5] = x;
+    __syncthreads();
+    if (t < 32) {
+        int w = warp_sums[t];
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (t >= o) w += y;
+        }
+        warp_sums[t] = w;
+    }
+    __syncthreads();
+    int dense_before = x - nd + ((t >> 5) ? warp_sums[(t >> 5) - 1] : 0);
+    int sparse_before = b0 - dense_before;
+    int16_t* im = index_map + static_cast<int64_t>(u) * nb;
+    int32_t* sb = slot_block ? slot_block + static_cast<int64_t>(u) * nb : nullptr;
+    for (int b = b0; b < b1; ++b) {
+        const int f = flag_of(b);
+        if (f) {
+            im[b] = static_cast<int16_t>(dense_before + 1);
+            if (sb) sb[dense_before] = b;
+            ++dense_before;
+        } else {
+            im[b] = static_cast<int16_t>(-(sparse_before + 1));
+            if (sb) sb[dense_count + sparse_before] = b;
+            ++sparse_before;
+        }
+        if (flags_out) flags_out[static_cast<int64_t>(u) * nb + b] = static_cast<uint8_t>(f);
+    }
+}
+
+// decompress (compressed_cache.hpp:271-298): pools -> logical [rows][d].
+template <int AXIS>
+__global__ void __launch_bounds__(kThreads) decompress_kernel(const int16_t* index_map, int nb,
+                                                              int dense_count, int sparse_count,
+                                                              const uint16_t* dense_pool,
+                                                              const uint16_t* nnz_pool,
+                                                              const uint16_t* meta_pool,
+                                                              uint16_t* dst, int* bad) {
+    const int b = blockIdx.x, u = blockIdx.y, t = threadIdx.x;
+    const int e = index_map[static_cast<int64_t>(u) * nb + b];
+    const int slot = (e > 0 ? e : -e) - 1;
+    uint16_t* out = dst + (static_cast<uint64_t>(u) * nb + b) * kBlock * kHeadDim;
+    if (e == 0 || (e > 0 && slot >= dense_count) || (e < 0 && slot >= sparse_count)) {
+        if (t == 0) atomicExch(bad, 1);
+        return;
+    }
+    for (int i = t; i < kBlock * kHeadDim; i += kThreads) {
+        // stored coordinates (sr, sc) of logical element i = (lr, lc)
+        const int lr = i / kHeadDim, lc = i % kHeadDim;
+        const int sr = AXIS == 0 ? lr : lc, sc = AXIS == 0 ? lc : lr;
+        const int scols = AXIS == 0 ? kHeadDim : kBlock;
+        uint16_t v;
+        if (e > 0) {
+            v = dense_pool[(static_cast<uint64_t>(u) * dense_count + slot) * kBlock * kHeadDim + sr * scols + sc];
+        } else {
+            const uint64_t sb = static_cast<uint64_t>(u) * sparse_count + slot;
+            const uint16_t* nnz = nnz_pool + sb * (kBlock * kHeadDim / 2) + sr * (scols / 2);
+            const uint16_t* meta = meta_pool + sb * (kBlock * kHeadDim / 16) + sr * (scols / 16);
+            const int g = sc >> 2, pos = sc & 3;
+            const uint32_t code = (meta[g >> 2] >> (4 * (g & 3))) & 0xF;
+            const int p0 = code & 3, p1 = code >> 2;
+            if (p1 <= p0) atomicExch(bad, 2);  // unpack_metadata: codes not increasing
+            v = pos == p0 ? nnz[2 * g] : (pos == p1 ? nnz[2 * g + 1] : static_cast<uint16_t>(0));
+        }
+        out[i] = v;
+    }
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- launchers
+template <typename T>
+static cudaError_t launch_block_kernel(int axis, int mode, const PackArgs& a, int n_units,
+                                       cudaStream_t s) {
+    const dim3 grid(a.nb, n_units);
+#define HS_LAUNCH(AX, MD) block_kernel<T, AX, MD><<<grid, kThreads, 0, s>>>(a)
+    if (axis == 0) {
+        if (mode == 0) HS_LAUNCH(0, 0); else if (mode == 1) HS_LAUNCH(0, 1); else HS_LAUNCH(0, 2);
+    } else {
+        if (mode == 0) HS_LAUNCH(1, 0); else if (mode == 1) HS_LAUNCH(1, 1); else HS_LAUNCH(1, 2);
+    }
+#undef HS_LAUNCH
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
+    PackArgs a;
+    a.src = static_cast<const uint16_t*>(L.src);
+    a.src_stride = L.src_unit_stride;
+    a.nb = L.nb;
+    a.dense_count = L.dense_count;
+    a.sparse_count = L.sparse_count;
+    a.index_map = L.index_map;
+    a.dense_pool = static_cast<uint16_t*>(L.dense_pool);
+    a.nnz_pool = static_cast<uint16_t*>(L.nnz_pool);
+    a.meta_pool = L.meta_pool;
+    a.losses = L.losses;
+    auto blocks = [&](int mode) {
+        return L.bf16 ? launch_block_kernel<__nv_bfloat16>(L.axis, mode, a, L.n_units, s)
+                      : launch_block_kernel<__half>(L.axis, mode, a, L.n_units, s);
+    };
+    cudaError_t err;
+    if (L.flags_in) {
+        // fused_magnitude_compress under an explicit BlockMask.
+        assign_slots_kernel<<<L.n_units, 1024, 0, s>>>(L.flags_in, L.nb, 0, 0, 0, L.dense_count,
+                                                       L.index_map, L.slot_block, L.flags_out);
+        if ((err = cudaGetLastError())) return err;
+        return blocks(1);
+    }
+    if (L.static_selection) {
+        assign_slots_kernel<<<L.n_units, 1024, 0, s>>>(nullptr, L.nb, L.prefix, L.suffix,
+                                                       L.all_sparse, L.dense_count, L.index_map,
+                                                       L.slot_block, L.flags_out);
+        if ((err = cudaGetLastError())) return err;
+        return blocks(L.losses ? 2 : 1);
+    }
+    // Loss-driven selection: classify -> rank -> assign -> pack.
+    if ((err = blocks(0))) return err;
+    rank_kernel<<<dim3((L.nb + 255) / 256, L.n_units), 256, 0, s>>>(L.losses, L.nb, L.prefix,
+                                                                     L.suffix, L.quota, L.flags_tmp);
+    if ((err = cudaGetLastError())) return err;
+    assign_slots_kernel<<<L.n_units, 1024, 0, s>>>(L.flags_tmp, L.nb, 0, 0, 0, L.dense_count,
+                                                   L.index_map, L.slot_block, L.flags_out);
+    if ((err = cudaGetLastError())) return err;
+    return blocks(1);
+}
+
+cudaError_t launch_decompress(const DecompressLaunch& L, cudaStream_t s) {
+    const dim3 grid(L.nb, L.n_units);
+    if (L.axis == 0)
+        decompress_kernel<0><<<grid, kThreads, 0, s>>>(L.index_map, L.nb, L.dense_count, L.sparse_count,
+                                                       static_cast<const uint16_t*>(L.dense_pool),
+                                                       static_cast<const uint16_t*>(L.nnz_pool),
+                                                       L.meta_pool, static_cast<uint16_t*>(L.dst), L.bad);
+    else
+        decompress_kernel<1><<<grid, kThreads, 0, s>>>(L.index_map, L.nb, L.dense_count, L.sparse_count,
+                                                       static_cast<const uint16_t*>(L.dense_pool),
+                                                       static_cast<const uint16_t*>(L.nnz_pool),
+                                                       L.meta_pool, static_cast<uint16_t*>(L.dst), L.bad);
+    return cudaGetLastError();
+}
+
+}  // namespace hs

@@ -1,0 +1,465 @@
+// Split-KV sparse decode attention over pooled HieraSparse caches (sm_100a).
+//
+// Reference semantics: attend_range (attention.hpp:249-304) over contiguous
+// block ranges, online softmax (attention.hpp:171-239), LSE combine
+// (attention.hpp:387-407).  Trans-Both orientation: S^T = K_b * Q^T and
+// O^T += V_b^T * P^T, so the pruned K and V^T blocks are the 2:4 *A* operand of
+// the sparse tensor-core MMA and the canonical metadata words feed the MMA
+// metadata register unchanged.
+//
+// Data path (HBM-bound): one producer warp streams each block's surviving
+// values (TMA 2-D tiles, hardware swizzle) and metadata (1-D bulk copies) into
+// an mbarrier ring; consumer warps each own a block at a time:
+//   GEMM1  mma.sp m16n8k32  K nnz [64 keys x 64] x Q^T (GQA rows stacked on N)
+//   softmax in registers (fp32), warp shuffles over the key lanes
+//   P^T    movmatrix relayout of the accumulator fragment (the paper's
+//          "RelayoutFragment"); bf16 P as a hi+lo pair
+//   GEMM2  mma.sp m16n8k32  V^T nnz [128 ch x 32] x P^T
+// Dense blocks take the dense m16n8k16 path.  Warps, then CTAs of a unit,
+// merge (m, l, O) with the reference combine; the last CTA per unit finishes.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hs {
+namespace {
+
+constexpr int kMaxGqa = 8;
+
+struct StageLayout {
+    uint32_t k_bytes, v_bytes, stage_bytes;
+};
+
+template <typename T>
+__device__ __forceinline__ uint32_t ld_pair(const T* p) {
+    return *reinterpret_cast<const uint32_t*>(p);
+}
+
+__device__ __forceinline__ uint32_t meta_sel(uint32_t lo_row, uint32_t hi_row, uint32_t half) {
+    return __byte_perm(lo_row, hi_row, half ? 0x7632 : 0x5410);
+}
+
+template <typename T, int NW, bool HILO>
+__global__ void __launch_bounds__(32 * (NW + 1)) decode_kernel(const __grid_constant__ DecodeLaunch L,
+                                                               int spw, StageLayout lay) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t full_bar[16];
+    __shared__ __align__(8) uint64_t empty_bar[16];
+    __shared__ int s_ticket;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int split = blockIdx.x, u = blockIdx.y;
+    const int gqa = L.gqa;
+    // Block range of this CTA (attention.hpp:380-381 partition of [begin, end)).
+    const int span = L.block_end - L.block_begin;
+    const int b0 = L.block_begin + static_cast<int>(static_cast<int64_t>(span) * split / L.nsplit);
+    const int b1 = L.block_begin + static_cast<int>(static_cast<int64_t>(span) * (split + 1) / L.nsplit);
+    const int nblk = b1 - b0;
+    const bool with_tail = L.include_tail && split == L.nsplit - 1 && L.tail > 0;
+
+    const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* const base_ptr = smem_raw + (base - smem_u32(smem_raw));
+
+    const int stages = NW * spw;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    const int16_t* kidx = L.k_index + static_cast<int64_t>(u) * L.nb;
+    const int16_t* vidx = L.v_index + static_cast<int64_t>(u) * L.nb;
+
+    if (warp == NW) {
+        // ------------------------------------------------------ producer ----
+        if (lane == 0) {
+            prefetch_tmap(&L.tm_knnz);
+            prefetch_tmap(&L.tm_vnnz);
+            prefetch_tmap(&L.tm_kden);
+            prefetch_tmap(&L.tm_vden);
+            for (int i = 0; i < nblk; ++i) {
+                // Block i belongs to consumer warp i % NW; each warp owns `spw`
+                // private slots, so no waiter is ever more than one phase ahead.
+                const int k = i / NW;
+                const int s = (i % NW) * spw + k % spw;
+                mbar_wait(&empty_bar[s], ((k / spw) & 1) ^ 1);
+                const int b = b0 + i;
+                const int ke = kidx[b], ve = vidx[b];
+                uint8_t* kreg = base_ptr + s * lay.stage_bytes;
+                uint8_t* vreg = kreg + lay.k_bytes;
+                const uint32_t bytes = (ke > 0 ? 16384u : 9216u) + (ve > 0 ? 16384u : 9216u);
+                mbar_arrive_expect_tx(&full_bar[s], bytes);
+                if (ke > 0) {
+                    const int row = (u * L.k_dense_count + ke - 1) * kBlock;
+                    tma_tile_g2s(kreg, &L.tm_kden, 0, row, &full_bar[s]);
+                    tma_tile_g2s(kreg + 8192, &L.tm_kden, 64, row, &full_bar[s]);
+                } else {
+                    const int sb = u * L.k_sparse_count + (-ke - 1);
+                    tma_tile_g2s(kreg, &L.tm_knnz, 0, sb * kBlock, &full_bar[s]);
+                    tma_bulk_g2s(kreg + 8192, L.k_meta + static_cast<int64_t>(sb) * 512, 1024, &full_bar[s]);
+                }
+                if (ve > 0) {
+                    const int row = (u * L.v_dense_count + ve - 1) * kHeadDim;
+                    tma_tile_g2s(vreg, &L.tm_vden, 0, row, &full_bar[s]);
+                } else {
+                    const int sb = u * L.v_sparse_count + (-ve - 1);
+                    tma_tile_g2s(vreg, &L.tm_vnnz, 0, sb * kHeadDim, &full_bar[s]);
+                    tma_bulk_g2s(vreg + 8192, L.v_meta + static_cast<int64_t>(sb) * 512, 1024, &full_bar[s]);
+                }
+            }
+        }
+        __syncwarp();  // reconverge before the CTA-wide barrier below
+    }
+
+    // ------------------------------------------------------- consumers ----
+    const int g = lane >> 2, t = lane & 3, half = t & 1;
+    float m_run[2] = {-INFINITY, -INFINITY};
+    float l_run[2] = {0.f, 0.f};
+    float o[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[i][k] = 0.f;
+
+    if (warp < NW) {
+        // Q^T fragments for GEMM1 (B operand, k = channel, n = query row g).
+        const T* q = static_cast<const T*>(L.q) + static_cast<int64_t>(u) * gqa * kHeadDim;
+        uint32_t qb[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+                qb[j][x] = g < gqa ? ld_pair(q + g * kHeadDim + 32 * j + 8 * x + 2 * t) : 0u;
+
+        for (int i = warp; i < nblk; i += NW) {
+            const int k = i / NW;
+            const int s = warp * spw + k % spw;
+            mbar_wait(&full_bar[s], (k / spw) & 1);
+            const int b = b0 + i;
+            const bool kd = kidx[b] > 0, vd = vidx[b] > 0;
+            const uint32_t kreg = base + s * lay.stage_bytes;
+            const uint32_t vreg = kreg + lay.k_bytes;
+
+            // ---------------- GEMM1: S^T[64 keys][8 q] ----------------
+            float sc[4][4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) sc[mi][k] = 0.f;
+            const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8;
+            const int lch = lane >> 4;
+            if (!kd) {
+                const uint8_t* kmeta = base_ptr + (kreg - base) + 8192;
+#pragma unroll
+                for (int mi = 0; mi < 4; ++mi) {
+                    const uint4 mlo = *reinterpret_cast<const uint4*>(kmeta + (16 * mi + g) * 16);
+                    const uint4 mhi = *reinterpret_cast<const uint4*>(kmeta + (16 * mi + g + 8) * 16);
+                    const uint32_t e[4] = {meta_sel(mlo.x, mhi.x, half), meta_sel(mlo.y, mhi.y, half),
+                                           meta_sel(mlo.z, mhi.z, half), meta_sel(mlo.w, mhi.w, half)};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint32_t a[4];
+                        ldmatrix_x4(kreg + sw128(16 * mi + lrow, 2 * j + lch), a);
+                        mma_sp_16832<T>(sc[mi], a, qb[j], e[j]);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        uint32_t a[4];
+                        const uint32_t tile = kreg + (kk >> 2) * 8192;
+                        ldmatrix_x4(tile + sw128(16 * mi + lrow, 2 * (kk & 3) + lch), a);
+                        mma_16816<T>(sc[mi], a, qb[kk >> 1][(kk & 1) * 2], qb[kk >> 1][(kk & 1) * 2 + 1]);
+                    }
+            }
+
+            // ---------------- online softmax (log2 domain) ----------------
+            float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    sc[mi][k] *= L.scale_log2;
+                    mx[k & 1] = fmaxf(mx[k & 1], sc[mi][k]);
+                }
+            float alpha[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                mx[e] = fmaxf(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], 4));
+                mx[e] = fmaxf(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], 8));
+                mx[e] = fmaxf(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], 16));
+                const float mnew = fmaxf(m_run[e], mx[e]);
+                alpha[e] = fast_exp2(m_run[e] - mnew);
+                m_run[e] = mnew;
+            }
+            float psum[2] = {0.f, 0.f};
+            uint32_t bt_hi[4][2], bt_lo[4][2];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+                float p[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    p[k] = fast_exp2(sc[mi][k] - m_run[k & 1]);
+                    psum[k & 1] += p[k];
+                }
+                const uint32_t top = F16Traits<T>::pack(p[0], p[1]);
+                const uint32_t bot = F16Traits<T>::pack(p[2], p[3]);
+                bt_hi[mi][0] = movmatrix_trans(top);
+                bt_hi[mi][1] = movmatrix_trans(bot);
+                if (HILO) {
+                    const float2 th = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&top));
+                    const float2 bh = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bot));
+                    bt_lo[mi][0] = movmatrix_trans(F16Traits<T>::pack(p[0] - th.x, p[1] - th.y));
+                    bt_lo[mi][1] = movmatrix_trans(F16Traits<T>::pack(p[2] - bh.x, p[3] - bh.y));
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) l_run[e] = l_run[e] * alpha[e] + psum[e];
+#pragma unroll
+            for (int mi = 0; mi < 8; ++mi) {
+                o[mi][0] *= alpha[0];
+                o[mi][2] *= alpha[0];
+                o[mi][1] *= alpha[1];
+                o[mi][3] *= alpha[1];
+            }
+
+            // ---------------- GEMM2: O^T[128 ch][8 q] += V^T P^T ----------------
+            if (!vd) {
+                const uint8_t* vmeta = base_ptr + (vreg - base) + 8192;
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi) {
+                    const uint2 mlo = *reinterpret_cast<const uint2*>(vmeta + (16 * mi + g) * 8);
+                    const uint2 mhi = *reinterpret_cast<const uint2*>(vmeta + (16 * mi + g + 8) * 8);
+                    const uint32_t e[2] = {meta_sel(mlo.x, mhi.x, half), meta_sel(mlo.y, mhi.y, half)};
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        uint32_t a[4];
+                        ldmatrix_x4(vreg + sw64(16 * mi + lrow, 2 * j + lch), a);
+                        const uint32_t bh[4] = {bt_hi[2 * j][0], bt_hi[2 * j][1], bt_hi[2 * j + 1][0],
+                                                bt_hi[2 * j + 1][1]};
+                        mma_sp_16832<T>(o[mi], a, bh, e[j]);
+                        if (HILO) {
+                            const uint32_t bl[4] = {bt_lo[2 * j][0], bt_lo[2 * j][1], bt_lo[2 * j + 1][0],
+                                                    bt_lo[2 * j + 1][1]};
+                            mma_sp_16832<T>(o[mi], a, bl, e[j]);
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        uint32_t a[4];
+                        ldmatrix_x4(vreg + sw128(16 * mi + lrow, 2 * kk + lch), a);
+                        mma_16816<T>(o[mi], a, bt_hi[kk][0], bt_hi[kk][1]);
+                        if (HILO) mma_16816<T>(o[mi], a, bt_lo[kk][0], bt_lo[kk][1]);
+                    }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[s]);
+        }
+
+        // ---------------- dense tail (attention.hpp:289-297) ----------------
+        if (with_tail && warp == 0) {
+            const T* kt = static_cast<const T*>(L.k_tail) + static_cast<int64_t>(u) * L.tail * kHeadDim;
+            const T* vt = static_cast<const T*>(L.v_tail) + static_cast<int64_t>(u) * L.tail * kHeadDim;
+            for (int tok = 0; tok < L.tail; ++tok) {
+                float kv[4];
+                for (int x = 0; x < 4; ++x)
+                    kv[x] = F16Traits<T>::to_float(reinterpret_cast<const uint16_t*>(kt)[tok * kHeadDim + 4 * lane + x]);
+                float sv2[2] = {0.f, 0.f};
+#pragma unroll
+                for (int qq = 0; qq < kMaxGqa; ++qq) {
+                    float part = 0.f;
+                    if (qq < gqa)
+                        for (int x = 0; x < 4; ++x)
+                            part += F16Traits<T>::to_float(reinterpret_cast<const uint16_t*>(q)[qq * kHeadDim + 4 * lane + x]) * kv[x];
+                    for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+                    if (qq == 2 * t) sv2[0] = part * L.scale_log2;
+                    if (qq == 2 * t + 1) sv2[1] = part * L.scale_log2;
+                }
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const float sv = sv2[e];
+                    const float mnew = fmaxf(m_run[e], sv);
+                    const float al = fast_exp2(m_run[e] - mnew);
+                    const float p = fast_exp2(sv - mnew);
+                    l_run[e] = l_run[e] * al + (g == 0 ? p : 0.f);
+                    m_run[e] = mnew;
+#pragma unroll
+                    for (int mi = 0; mi < 8; ++mi) {
+                        const float v0 = F16Traits<T>::to_float(reinterpret_cast<const uint16_t*>(vt)[tok * kHeadDim + 16 * mi + g]);
+                        const float v1 = F16Traits<T>::to_float(reinterpret_cast<const uint16_t*>(vt)[tok * kHeadDim + 16 * mi + g + 8]);
+                        o[mi][e] = o[mi][e] * al + p * v0;
+                        o[mi][2 + e] = o[mi][2 + e] * al + p * v1;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            l_run[e] += __shfl_xor_sync(0xffffffffu, l_run[e], 4);
+            l_run[e] += __shfl_xor_sync(0xffffffffu, l_run[e], 8);
+            l_run[e] += __shfl_xor_sync(0xffffffffu, l_run[e], 16);
+        }
+    }
+
+    // ---------------- merge warps (attention.hpp:387-407 formula) ----------------
+    __syncthreads();  // all stages consumed; reuse the ring as scratch
+    float* s_o = reinterpret_cast<float*>(base_ptr);            // [NW][gqa][128]
+    float* s_m = s_o + NW * kMaxGqa * kHeadDim;                 // [NW][gqa]
+    float* s_l = s_m + NW * kMaxGqa;
+    if (warp < NW) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int qq = 2 * t + e;
+            if (qq < gqa) {
+                if (g == 0) {
+                    s_m[warp * kMaxGqa + qq] = m_run[e];
+                    s_l[warp * kMaxGqa + qq] = l_run[e];
+                }
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi) {
+                    s_o[(warp * kMaxGqa + qq) * kHeadDim + 16 * mi + g] = o[mi][e];
+                    s_o[(warp * kMaxGqa + qq) * kHeadDim + 16 * mi + g + 8] = o[mi][2 + e];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int nthr = 32 * (NW + 1);
+    const int stride_p = gqa * (kHeadDim + 2);
+    float* part = L.partial + (static_cast<int64_t>(u) * L.nsplit + split) * stride_p;
+    constexpr float kLn2 = 0.6931471805599453f;
+    for (int idx = threadIdx.x; idx < gqa * (kHeadDim + 1); idx += nthr) {
+        const int qq = idx / (kHeadDim + 1), c = idx % (kHeadDim + 1);
+        float M = -INFINITY;
+        for (int w = 0; w < NW; ++w) M = fmaxf(M, s_m[w * kMaxGqa + qq]);
+        float acc = 0.f;
+        for (int w = 0; w < NW; ++w) {
+            const float mw = s_m[w * kMaxGqa + qq];
+            const float wt = (mw == -INFINITY) ? 0.f : fast_exp2(mw - M);
+            acc += wt * (c < kHeadDim ? s_o[(w * kMaxGqa + qq) * kHeadDim + c] : s_l[w * kMaxGqa + qq]);
+        }
+        if (c < kHeadDim) {
+            part[qq * (kHeadDim + 2) + c] = acc;
+        } else {
+            part[qq * (kHeadDim + 2) + kHeadDim] = M * kLn2;   // m in natural-log units
+            part[qq * (kHeadDim + 2) + kHeadDim + 1] = acc;    // l
+        }
+    }
+    if (L.out == nullptr) return;
+
+    // ---------------- last CTA of the unit combines all splits ----------------
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_ticket = atomicAdd(&L.counters[u], 1);
+    __syncthreads();
+    if (s_ticket != L.nsplit - 1) return;
+    __threadfence();
+    const float* P = L.partial + static_cast<int64_t>(u) * L.nsplit * stride_p;
+    constexpr float kLog2e = 1.4426950408889634f;
+    for (int idx = threadIdx.x; idx < gqa * kHeadDim; idx += nthr) {
+        const int qq = idx / kHeadDim, c = idx % kHeadDim;
+        float M = -INFINITY;
+        for (int sp = 0; sp < L.nsplit; ++sp) M = fmaxf(M, __ldcg(P + sp * stride_p + qq * (kHeadDim + 2) + kHeadDim));
+        float acc = 0.f, lsum = 0.f;
+        for (int sp = 0; sp < L.nsplit; ++sp) {
+            const float* ps = P + sp * stride_p + qq * (kHeadDim + 2);
+            const float ms = __ldcg(ps + kHeadDim);
+            const float wt = ms == -INFINITY ? 0.f : fast_exp2((ms - M) * kLog2e);
+            lsum += __ldcg(ps + kHeadDim + 1) * wt;
+            acc += __ldcg(ps + c) * wt;
+        }
+        if (L.out_mode == 0) {
+            L.out[(static_cast<int64_t>(u) * gqa + qq) * kHeadDim + c] = acc / lsum;
+        } else {
+            float* po = L.out + (static_cast<int64_t>(u) * gqa + qq) * (kHeadDim + 2);
+            po[c] = acc;
+            if (c == 0) {
+                po[kHeadDim] = M;
+                po[kHeadDim + 1] = lsum;
+            }
+        }
+    }
+    if (threadIdx.x == 0) L.counters[u] = 0;
+}
+
+// Standalone LSE combine of n_parts partials (cross-GPU sequence split).
+__global__ void combine_kernel(const float* partials, int n_parts, int n_units, int gqa, int d,
+                               float* out) {
+    const int u = blockIdx.x;
+    const int stride_u = gqa * (d + 2);
+    constexpr float kLog2e = 1.4426950408889634f;
+    for (int idx = threadIdx.x; idx < gqa * d; idx += blockDim.x) {
+        const int qq = idx / d, c = idx % d;
+        float M = -INFINITY;
+        for (int p = 0; p < n_parts; ++p)
+            M = fmaxf(M, partials[(static_cast<int64_t>(p) * n_units + u) * stride_u + qq * (d + 2) + d]);
+        float acc = 0.f, lsum = 0.f;
+        for (int p = 0; p < n_parts; ++p) {
+            const float* ps = partials + (static_cast<int64_t>(p) * n_units + u) * stride_u + qq * (d + 2);
+            const float wt = ps[d] == -INFINITY ? 0.f : exp2f((ps[d] - M) * kLog2e);
+            lsum += ps[d + 1] * wt;
+            acc += ps[c] * wt;
+        }
+        out[(static_cast<int64_t>(u) * gqa + qq) * d + c] = acc / lsum;
+    }
+}
+
+template <typename T, int NW, bool HILO>
+cudaError_t launch_t(const DecodeLaunch& L, int spw, StageLayout lay, size_t smem,
+                     cudaStream_t s) {
+    auto k = decode_kernel<T, NW, HILO>;
+    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err) return err;
+    k<<<dim3(L.nsplit, L.n_units), 32 * (NW + 1), smem, s>>>(L, spw, lay);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int decode_warps() {
+    const char* env = getenv("HS_DECODE_WARPS");
+    return env && atoi(env) == 8 ? 8 : 4;
+}
+
+cudaError_t launch_decode(const DecodeLaunch& L, cudaStream_t s) {
+    StageLayout lay;
+    lay.k_bytes = L.k_dense_count > 0 ? 16384u : 9216u;
+    lay.v_bytes = L.v_dense_count > 0 ? 16384u : 9216u;
+    lay.stage_bytes = lay.k_bytes + lay.v_bytes;
+    const int NW = decode_warps();
+    // Ring budget per CTA (decode_ctas_per_sm() CTAs share an SM's 227 KB).
+    const uint32_t budget = (decode_ctas_per_sm() == 1 ? 200u : 100u) * 1024u;
+    int spw = static_cast<int>(budget / (NW * lay.stage_bytes));
+    if (const char* env = getenv("HS_DECODE_SPW")) spw = atoi(env);
+    spw = spw < 1 ? 1 : (spw * NW > 16 ? 16 / NW : spw);
+    size_t smem = static_cast<size_t>(NW * spw) * lay.stage_bytes + 1024;
+    const size_t scratch = (NW * kMaxGqa * kHeadDim + 2 * NW * kMaxGqa) * sizeof(float) + 1024;
+    if (smem < scratch) smem = scratch;
+    if (NW == 8) {
+        if (L.bf16) return launch_t<__nv_bfloat16, 8, true>(L, spw, lay, smem, s);
+        return launch_t<__half, 8, false>(L, spw, lay, smem, s);
+    }
+    if (L.bf16) return launch_t<__nv_bfloat16, 4, true>(L, spw, lay, smem, s);
+    return launch_t<__half, 4, false>(L, spw, lay, smem, s);
+}
+
+int decode_ctas_per_sm() {
+    const char* env = getenv("HS_DECODE_CTAS_PER_SM");
+    return env && atoi(env) == 2 ? 2 : 1;
+}
+
+cudaError_t launch_combine(const float* partials, int n_parts, int n_units, int gqa, int d,
+                           float* out, cudaStream_t s) {
+    combine_kernel<<<n_units, 256, 0, s>>>(partials, n_parts, n_units, gqa, d, out);
+    return cudaGetLastError();
+}
+
+}  // namespace hs

@@ -1,0 +1,95 @@
+// Internal launch descriptors shared by the C-ABI layer and the kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hs {
+
+constexpr int kBlock = 64;    // B: tokens per block (masks.hpp:76 default)
+constexpr int kHeadDim = 128; // d: Llama-3.1-8B head dim
+
+struct CompressLaunch {
+    bool bf16;
+    int axis;
+    int n_units;
+    int nb;
+    int dense_count, sparse_count;
+    int prefix, suffix, quota;
+    bool static_selection;   // quota is 0 or all prunable blocks
+    bool all_sparse;         // static: prunable blocks are sparse
+    const void* src;
+    uint64_t src_unit_stride;
+    const uint8_t* flags_in; // explicit BlockMask (hs_compress_with_flags)
+    uint8_t* flags_tmp;      // scratch for loss-driven selection
+    uint8_t* flags_out;      // optional
+    double* losses;          // optional in static mode, required otherwise
+    int16_t* index_map;
+    int32_t* slot_block;
+    void* dense_pool;
+    void* nnz_pool;
+    uint16_t* meta_pool;
+};
+cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s);
+
+struct DecompressLaunch {
+    int axis, n_units, nb, dense_count, sparse_count;
+    const int16_t* index_map;
+    const void* dense_pool;
+    const void* nnz_pool;
+    const uint16_t* meta_pool;
+    void* dst;
+    int* bad;
+};
+cudaError_t launch_decompress(const DecompressLaunch& L, cudaStream_t s);
+
+// Split-KV decode over pooled caches (attention.hpp:249-304, :360-409).
+struct DecodeLaunch {
+    bool bf16;
+    int n_units, nb, gqa, tail;
+    int k_dense_count, k_sparse_count, v_dense_count, v_sparse_count;
+    float scale_log2;        // scale * log2(e)
+    const void* q;           // [u][gqa][d]
+    const int16_t* k_index;  // [u][nb]
+    const int16_t* v_index;
+    const uint16_t* k_meta;  // [u][sparse][512]
+    const uint16_t* v_meta;
+    const void* k_tail;      // [u][tail][d]
+    const void* v_tail;
+    // split geometry: unit u, split s covers blocks [nb*s/nsplit, nb*(s+1)/nsplit)
+    int nsplit;
+    int block_begin, block_end;  // restrict to a block range (partial API)
+    int include_tail;
+    // outputs
+    float* partial;          // [u][nsplit][gqa][d+2] (O, m, l)
+    float* out;              // fused combine target or nullptr (split partials only)
+    int out_mode;            // 0: normalised [u][gqa][d]; 1: merged partial [u][gqa][d+2]
+    int* counters;           // [u] arrival counters for the fused combine
+    CUtensorMap tm_knnz, tm_kden, tm_vnnz, tm_vden;
+};
+cudaError_t launch_decode(const DecodeLaunch& L, cudaStream_t s);
+int decode_ctas_per_sm();  // CTAs the decode ring is sized for (1 or 2)
+cudaError_t launch_combine(const float* partials, int n_parts, int n_units, int gqa, int d,
+                           float* out, cudaStream_t s);
+
+// Causal / non-causal prefill (attention.hpp:323-354).
+struct PrefillLaunch {
+    bool bf16;
+    int n_units, nb, gqa, n_q, tail, causal;
+    int k_dense_count, k_sparse_count, v_dense_count, v_sparse_count;
+    float scale_log2;
+    const void* q;
+    const int16_t* k_index;
+    const int16_t* v_index;
+    const int32_t* k_slot_block;
+    const uint16_t* k_meta;
+    const uint16_t* v_meta;
+    const void* k_tail;
+    const void* v_tail;
+    float* out;
+    CUtensorMap tm_q, tm_knnz, tm_kden, tm_vnnz, tm_vden;
+};
+cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s);
+
+}  // namespace hs

@@ -1,0 +1,288 @@
+"""Host-side mirror of the reference's hot-path API over device-resident caches.
+
+Same names and argument meaning as /root/reference/proj/include/hierasparse
+(prune_cache, fused_magnitude_compress, decompress, decode_attention,
+prefill_attention, measure_size, flop_and_byte_count), batched over "units"
+(request, KV-head pairs).  PyTorch only provides device memory and the current
+stream; every computation runs in the sm_100a kernels behind the C ABI
+(include/hierasparse_b200.h) — there is no CPU or eager fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import capi
+from .errors import ConfigError
+
+BLOCK = 64
+HEAD_DIM = 128
+HEADER_BYTES = 8 + 2 + 5 * 4 + 4 * 2  # container.hpp:42 kContainerHeaderBytes
+
+
+def _dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.bfloat16:
+        return capi.DTYPE_BF16
+    if dt == torch.float16:
+        return capi.DTYPE_F16
+    raise ConfigError(f"unsupported dtype {dt}: device kernels take bfloat16 or float16")
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None or t.numel() == 0 else t.data_ptr()
+
+
+@dataclass
+class SparsityConfig:
+    """masks.hpp:73-99 (2:4 pattern)."""
+
+    s_key: float = 0.0
+    s_value: float = 0.0
+    block_size: int = BLOCK
+    sink_tokens: int = 0
+    local_window: int = 0
+
+    def c(self) -> capi.SparsityConfigC:
+        return capi.SparsityConfigC(self.s_key, self.s_value, self.block_size, 0, self.sink_tokens,
+                                    self.local_window)
+
+    def protected_prefix_blocks(self) -> int:
+        return (self.sink_tokens + self.block_size - 1) // self.block_size
+
+    def protected_suffix_blocks(self) -> int:
+        return (self.local_window + self.block_size - 1) // self.block_size
+
+
+def pool_counts(rows: int, cfg: SparsityConfig, sparsity: float):
+    """(logical_blocks, dense_count, sparse_count, prefix, suffix) before any data is seen
+    (pruner.hpp:106-108, :127-131)."""
+    lib = capi.load()
+    out = [C.c_uint32() for _ in range(5)]
+    c = cfg.c()
+    capi.check(lib.hs_pool_counts(rows, C.byref(c), sparsity, *[C.byref(o) for o in out]))
+    return tuple(o.value for o in out)
+
+
+class DeviceCompressedCache:
+    """CompressedCache (compressed_cache.hpp:37-110) for n_units units on one GPU,
+    in the reference's canonical layout (see include/hierasparse_b200.h)."""
+
+    def __init__(self, dtype: torch.dtype, axis: int, n_units: int, logical_blocks: int,
+                 dense_count: int, sparse_count: int, device=None, head_dim: int = HEAD_DIM,
+                 block_size: int = BLOCK, cfg: SparsityConfig | None = None):
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.dtype, self.axis, self.n_units = dtype, axis, n_units
+        self.head_dim, self.block_size = head_dim, block_size
+        self.logical_blocks, self.dense_count, self.sparse_count = logical_blocks, dense_count, sparse_count
+        self.cfg = cfg
+        be = block_size * head_dim
+        U = n_units
+        self.index_map = torch.empty((U, logical_blocks), dtype=torch.int16, device=dev)
+        self.dense_pool = torch.empty((U, dense_count, be), dtype=dtype, device=dev)
+        self.nnz_pool = torch.empty((U, sparse_count, be // 2), dtype=dtype, device=dev)
+        self.meta_pool = torch.empty((U, sparse_count, be // 16), dtype=torch.int16, device=dev)
+        self.slot_block = torch.empty((U, logical_blocks), dtype=torch.int32, device=dev)
+        self.flags = torch.empty((U, logical_blocks), dtype=torch.uint8, device=dev)
+        self.losses = torch.empty((U, logical_blocks), dtype=torch.float64, device=dev)
+
+    @property
+    def sequence_length(self) -> int:
+        return self.logical_blocks * self.block_size
+
+    def c(self) -> capi.DeviceCacheC:
+        return capi.DeviceCacheC(_dtype_code(self.dtype), self.axis, self.head_dim, self.block_size,
+                                 self.n_units, self.logical_blocks, self.dense_count, self.sparse_count,
+                                 _ptr(self.index_map), _ptr(self.dense_pool), _ptr(self.nnz_pool),
+                                 _ptr(self.meta_pool), _ptr(self.slot_block))
+
+    def measure_size(self) -> dict:
+        """measure_size (compressed_cache.hpp:303-310), per unit."""
+        be = self.block_size * self.head_dim
+        return dict(size_idx=self.logical_blocks * 2, size_den=self.dense_count * be * 2,
+                    size_nnz=self.sparse_count * (be // 2) * 2, size_e=self.sparse_count * (be // 16) * 2)
+
+    def nbytes(self) -> int:
+        """Bytes a full traversal of every unit reads (pools + index map)."""
+        return self.n_units * sum(self.measure_size().values())
+
+
+def _check_src(x: torch.Tensor) -> torch.Tensor:
+    if not x.is_cuda:
+        raise ConfigError("source must be a CUDA tensor (use the host-buffer entry points for host data)")
+    if x.dim() == 2:
+        x = x.unsqueeze(0)
+    if x.dim() != 3:
+        raise ConfigError("source must be [units, rows, head_dim]")
+    if x.stride(2) != 1 or x.stride(1) != x.shape[2] or (x.shape[0] > 1 and x.stride(0) < x.shape[1] * x.shape[2]):
+        x = x.contiguous()
+    return x
+
+
+def _unit_stride(x: torch.Tensor) -> int:
+    return x.stride(0) if x.shape[0] > 1 else x.shape[1] * x.shape[2]
+
+
+def prune_compress(x: torch.Tensor, cfg: SparsityConfig, sparsity: float, axis: int,
+                   out: DeviceCompressedCache | None = None) -> DeviceCompressedCache:
+    """hierarchical_mask_for (pruner.hpp:121-158) + fused_magnitude_compress
+    (compressed_cache.hpp:232-267) for one cache kind of every unit."""
+    x = _check_src(x)
+    U, rows, d = x.shape
+    nb, dc, sc, _, _ = pool_counts(rows, cfg, sparsity)
+    if out is None:
+        out = DeviceCompressedCache(x.dtype, axis, U, nb, dc, sc, x.device, d, cfg.block_size, cfg)
+    lib = capi.load()
+    c, cc = out.c(), cfg.c()
+    capi.check(lib.hs_prune_compress(x.data_ptr(), _unit_stride(x), rows, C.byref(cc), sparsity, C.byref(c),
+                                     out.losses.data_ptr(), out.flags.data_ptr(), _stream()))
+    return out
+
+
+def prune_cache(key: torch.Tensor, value: torch.Tensor, cfg: SparsityConfig):
+    """prune_cache (pruner.hpp:165-176) followed by compression of both caches:
+    key along channels at S_K, value along the sequence at S_V."""
+    if key.shape[-2] != value.shape[-2]:
+        raise ConfigError("prune_cache: key/value sequence lengths differ")
+    if key.shape[-1] % 4:
+        raise ConfigError("prune_cache: head dimension not divisible by m_group")
+    return (prune_compress(key, cfg, cfg.s_key, capi.AXIS_CHANNEL),
+            prune_compress(value, cfg, cfg.s_value, capi.AXIS_SEQUENCE))
+
+
+def fused_magnitude_compress(x: torch.Tensor, flags: torch.Tensor, cfg: SparsityConfig,
+                             axis: int) -> DeviceCompressedCache:
+    """fused_magnitude_compress (compressed_cache.hpp:262-267) under a given BlockMask
+    (flags u8 [units, blocks], 1 = dense)."""
+    x = _check_src(x)
+    U, rows, d = x.shape
+    if rows % cfg.block_size:
+        raise ConfigError("compress: sequence length not divisible by block_size")
+    flags = flags.to(device=x.device, dtype=torch.uint8).reshape(U, -1).contiguous()
+    nb = rows // cfg.block_size
+    dc = int(flags[0].sum().item()) if nb else 0
+    out = DeviceCompressedCache(x.dtype, axis, U, nb, dc, nb - dc, x.device, d, cfg.block_size, cfg)
+    c = out.c()
+    capi.check(capi.load().hs_compress_with_flags(x.data_ptr(), _unit_stride(x), rows, flags.data_ptr(),
+                                                  C.byref(c), _stream()))
+    out.flags.copy_(flags)
+    return out
+
+
+def decompress(c: DeviceCompressedCache) -> torch.Tensor:
+    """decompress (compressed_cache.hpp:271-298) -> [units, rows, d]."""
+    out = torch.empty((c.n_units, c.sequence_length, c.head_dim), dtype=c.dtype, device=c.index_map.device)
+    cs = c.c()
+    capi.check(capi.load().hs_decompress(C.byref(cs), out.data_ptr(), _stream()))
+    return out
+
+
+def _tails(k_tail, v_tail, U, d):
+    if k_tail is None or k_tail.numel() == 0:
+        return None, None, 0
+    k_tail = k_tail.reshape(U, -1, d).contiguous()
+    v_tail = v_tail.reshape(U, -1, d).contiguous()
+    if k_tail.shape != v_tail.shape:
+        raise ConfigError("attention: key/value token counts differ")
+    return k_tail, v_tail, k_tail.shape[1]
+
+
+def decode_attention(q: torch.Tensor, k: DeviceCompressedCache, v: DeviceCompressedCache,
+                     k_tail: torch.Tensor | None = None, v_tail: torch.Tensor | None = None,
+                     scale: float | None = None, splits: int = 0,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    """decode_attention (attention.hpp:360-409) for every unit: q [units, gqa, d] -> fp32."""
+    U = k.n_units
+    q = q.reshape(U, -1, k.head_dim).contiguous()
+    gqa = q.shape[1]
+    kt, vt, tail = _tails(k_tail, v_tail, U, k.head_dim)
+    scale = 1.0 / math.sqrt(k.head_dim) if scale is None else scale
+    if out is None:
+        out = torch.empty((U, gqa, k.head_dim), dtype=torch.float32, device=q.device)
+    kc, vc = k.c(), v.c()
+    capi.check(capi.load().hs_decode(q.data_ptr(), C.byref(kc), C.byref(vc), _ptr(kt), _ptr(vt), tail, gqa,
+                                     scale, splits, out.data_ptr(), _stream()))
+    return out
+
+
+def decode_partial(q, k: DeviceCompressedCache, v: DeviceCompressedCache, block_begin: int, block_end: int,
+                   k_tail=None, v_tail=None, include_tail: bool = True, scale: float | None = None):
+    """attend_range (attention.hpp:249-304) over [block_begin, block_end) as an
+    unnormalised SplitPartial per unit: float [units, gqa, d + 2] = (O, m, l)."""
+    U = k.n_units
+    q = q.reshape(U, -1, k.head_dim).contiguous()
+    gqa = q.shape[1]
+    kt, vt, tail = _tails(k_tail, v_tail, U, k.head_dim)
+    scale = 1.0 / math.sqrt(k.head_dim) if scale is None else scale
+    out = torch.empty((U, gqa, k.head_dim + 2), dtype=torch.float32, device=q.device)
+    kc, vc = k.c(), v.c()
+    capi.check(capi.load().hs_decode_partial(q.data_ptr(), C.byref(kc), C.byref(vc), _ptr(kt), _ptr(vt), tail,
+                                             gqa, scale, block_begin, block_end, int(include_tail),
+                                             out.data_ptr(), _stream()))
+    return out
+
+
+def decode_combine(partials: torch.Tensor) -> torch.Tensor:
+    """LSE combine (attention.hpp:387-407) of partials [parts, units, gqa, d + 2]."""
+    partials = partials.contiguous()
+    P, U, gqa, d2 = partials.shape
+    out = torch.empty((U, gqa, d2 - 2), dtype=torch.float32, device=partials.device)
+    capi.check(capi.load().hs_decode_combine(partials.data_ptr(), P, U, gqa, d2 - 2, out.data_ptr(), _stream()))
+    return out
+
+
+def prefill_attention(q: torch.Tensor, k: DeviceCompressedCache, v: DeviceCompressedCache,
+                      k_tail=None, v_tail=None, causal: bool = True, scale: float | None = None,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+    """prefill_attention (attention.hpp:323-354): q [units, gqa, n_q, d] -> fp32."""
+    U = k.n_units
+    if q.dim() == 3:
+        q = q.unsqueeze(1)
+    q = q.contiguous()
+    _, gqa, n_q, d = q.shape
+    kt, vt, tail = _tails(k_tail, v_tail, U, k.head_dim)
+    scale = 1.0 / math.sqrt(k.head_dim) if scale is None else scale
+    if out is None:
+        out = torch.empty((U, gqa, n_q, d), dtype=torch.float32, device=q.device)
+    kc, vc = k.c(), v.c()
+    capi.check(capi.load().hs_prefill(q.data_ptr(), n_q, gqa, C.byref(kc), C.byref(vc), _ptr(kt), _ptr(vt), tail,
+                                      int(causal), scale, out.data_ptr(), _stream()))
+    return out
+
+
+def flop_and_byte_count(n_q: int, k: DeviceCompressedCache, v: DeviceCompressedCache, tail: int = 0,
+                        causal: bool = False, unit: int = 0) -> tuple[int, int]:
+    """flop_and_byte_count (attention.hpp:426-467) for one unit, from the index maps."""
+    d, B = k.head_dim, k.block_size
+    kd = (k.index_map[unit] > 0).cpu().tolist() if k.sparse_count and k.dense_count else \
+        [k.sparse_count == 0] * k.logical_blocks
+    vd = (v.index_map[unit] > 0).cpu().tolist() if v.sparse_count and v.dense_count else \
+        [v.sparse_count == 0] * v.logical_blocks
+    nb = k.logical_blocks
+    prefix = nb * B
+    n_kv = prefix + tail
+    # per-block flop weight: width * d * (2 dense | 1 sparse) for each GEMM
+    w = [(2 if kd[b] else 1) + (2 if vd[b] else 1) for b in range(nb)]
+    flops = 0
+    if not causal:
+        flops = n_q * (sum(w) * B * d + (4 * tail * d if tail else 0))
+    else:
+        for i in range(n_q):
+            vis = n_kv - n_q + i + 1
+            full = min(nb, vis // B)
+            flops += sum(w[:full]) * B * d
+            if full < nb and full * B < vis:
+                flops += w[full] * (vis - full * B) * d
+            if vis > prefix:
+                flops += 4 * (vis - prefix) * d
+    nbytes = 0
+    for c in (k, v):
+        nbytes += HEADER_BYTES + sum(c.measure_size().values())
+    nbytes += 2 * tail * d * 2
+    return flops, nbytes

@@ -1,0 +1,183 @@
+"""GPU parity: hierarchical pruning + pooled 2:4 compression must match the
+oracle bit for bit (index map, block flags, FP64 losses, dense / nnz / metadata
+pools), through the C ABI (include/hierasparse_b200.h)."""
+import os
+
+import numpy as np
+import pytest
+
+from tests.helpers import device_to_oracle, gen_units, parallel, to_torch
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_vectors.npz")
+
+
+@pytest.fixture(scope="module")
+def hs():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2604_16864_b200 import hierasparse
+    return hierasparse
+
+
+def assert_cache_equal(dev, u, want, label=""):
+    got = device_to_oracle(dev, u)
+    assert got.dense_count == want.dense_count and got.sparse_count == want.sparse_count, label
+    assert (got.index_map == want.index_map).all(), label
+    assert (got.flags == want.flags).all(), label
+    assert got.losses.tobytes() == want.losses.tobytes(), f"{label}: losses differ"
+    if want.dense_count:
+        assert (got.dense_pool == want.dense_pool).all(), f"{label}: dense pool"
+    if want.sparse_count:
+        assert (got.nnz_pool == want.nnz_pool).all(), f"{label}: nnz pool"
+        assert (got.meta_pool == want.meta_pool).all(), f"{label}: meta pool"
+
+
+CASES = [
+    # rows, s, sink, window
+    (4096, 1.0, 0, 0),
+    (4096, 0.5, 64, 100),
+    (2048, 0.25, 0, 0),
+    (1024, 0.0, 0, 0),
+    (512, 0.75, 1, 9),
+    (640, 1.0, 70, 130),
+]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("rows,s,sink,window", CASES)
+def test_prune_compress_matches_oracle(hs, port, dtype, rows, s, sink, window):
+    from oracle.oracle import SparsityConfig as OCfg
+    U = 3
+    cfg = hs.SparsityConfig(s, s, 64, sink, window)
+    ocfg = OCfg(s, s, 64, sink, window)
+    for axis, role in ((0, 0), (1, 1)):
+        x = gen_units(port, U, rows, 128, seed=11 + rows, role=role, dtype=dtype)
+        dev = hs.prune_compress(to_torch(x, dtype), cfg, s, axis)
+        wants = parallel(lambda u: port.prune_compress(x[u], ocfg, axis, s), range(U))
+        for u in range(U):
+            assert_cache_equal(dev, u, wants[u], f"axis={axis} unit={u}")
+        # slot_block inverts the index map (dense slots first, then sparse slots)
+        im = dev.index_map.cpu().numpy()
+        sb = dev.slot_block.cpu().numpy()
+        for u in range(U):
+            for b, e in enumerate(im[u]):
+                slot = e - 1 if e > 0 else dev.dense_count + (-e - 1)
+                assert sb[u, slot] == b
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+def test_ties_zeros_and_signed_zero(hs, port, dtype):
+    from oracle.oracle import SparsityConfig as OCfg
+    rng = np.random.default_rng(3)
+    vals = np.array([0.0, -0.0, 1.0, -1.0, 2.0, -2.0, 0.5], np.float32)
+    x = rng.choice(vals, size=(2, 1024, 128)).astype(np.float32)
+    x[:, :64] = 0.0  # an all-zero block: ties keep positions {0, 1}
+    for s in (1.0, 0.5):
+        cfg, ocfg = hs.SparsityConfig(s, s, 64), OCfg(s, s, 64)
+        for axis in (0, 1):
+            dev = hs.prune_compress(to_torch(x, dtype), cfg, s, axis)
+            for u in range(2):
+                assert_cache_equal(dev, u, port.prune_compress(x[u], ocfg, axis, s), f"s={s} axis={axis}")
+
+
+def test_loss_fallback_wide_dynamic_range(hs, port):
+    """bf16 blocks whose pruned magnitudes span > 2^33 take the sequential
+    FP64 path; losses must still be bit-identical to pruner.hpp:85-87."""
+    from oracle.oracle import SparsityConfig as OCfg
+    x = gen_units(port, 1, 512, 128, seed=5, role=0, dtype="bf16")
+    x[0, ::7, ::5] *= np.float32(2.0 ** 60)
+    x[0, 3::11, 1::3] *= np.float32(2.0 ** -60)
+    x = port.round_to(x, "bf16")
+    for s in (1.0, 0.5):
+        for axis in (0, 1):
+            dev = hs.prune_compress(to_torch(x, "bf16"), hs.SparsityConfig(s, s, 64), s, axis)
+            assert_cache_equal(dev, 0, port.prune_compress(x[0], OCfg(s, s, 64), axis, s), f"axis={axis}")
+
+
+def test_compress_with_flags(hs, port):
+    import torch
+    from oracle.oracle import SparsityConfig as OCfg
+    x = gen_units(port, 2, 1024, 128, seed=9, role=0, dtype="bf16")
+    flags = np.zeros((2, 16), np.uint8)
+    flags[:, [0, 3, 4, 9, 15]] = 1
+    for axis in (0, 1):
+        dev = hs.fused_magnitude_compress(to_torch(x, "bf16"), torch.from_numpy(flags), hs.SparsityConfig(), axis)
+        for u in range(2):
+            want = port.compress_with_flags(x[u], OCfg(block_size=64), axis, flags[u])
+            got = device_to_oracle(dev, u)
+            assert (got.index_map == want.index_map).all()
+            assert (got.dense_pool == want.dense_pool).all()
+            assert (got.nnz_pool == want.nnz_pool).all()
+            assert (got.meta_pool == want.meta_pool).all()
+
+
+@pytest.mark.parametrize("s", [1.0, 0.5])
+def test_decompress_matches_oracle(hs, port, s):
+    from oracle.oracle import SparsityConfig as OCfg
+    x = gen_units(port, 2, 2048, 128, seed=21, role=1, dtype="f16")
+    for axis in (0, 1):
+        dev = hs.prune_compress(to_torch(x, "f16"), hs.SparsityConfig(s, s, 64, 64, 64), s, axis)
+        got = hs.decompress(dev).float().cpu().numpy()
+        for u in range(2):
+            want = port.decompress(port.prune_compress(x[u], OCfg(s, s, 64, 64, 64), axis, s))
+            assert (got[u] == want).all()
+
+
+def test_decompress_rejects_corrupt_index_map(hs, port):
+    from paper_2604_16864_b200 import DataError
+    x = gen_units(port, 1, 256, 128, seed=1, role=0, dtype="bf16")
+    dev = hs.prune_compress(to_torch(x, "bf16"), hs.SparsityConfig(1, 1, 64), 1.0, 0)
+    dev.index_map[0, 1] = 0
+    with pytest.raises(DataError):
+        hs.decompress(dev)
+
+
+def test_golden_reference_vectors_on_gpu(hs):
+    """Pools must equal the committed outputs of the compiled reference."""
+    g = np.load(GOLD)
+    to_f = lambda b: (b.astype(np.uint32) << 16).view(np.float32)  # noqa: E731
+    key = to_f(g["key"]).reshape(-1, 128)[:256]
+    val = to_f(g["val"]).reshape(-1, 128)[:256]
+    for name in ("s50", "s100w", "s25"):
+        for axis, x in ((0, key), (1, val)):
+            p = f"{name}_{'k' if axis == 0 else 'v'}"
+            s, sink, window = g[p + "_cfg"]
+            dev = hs.prune_compress(to_torch(x[None], "bf16"), hs.SparsityConfig(s, s, 64, int(sink), int(window)),
+                                    float(s), axis)
+            got = device_to_oracle(dev, 0)
+            assert (got.index_map == g[p + "_index_map"]).all()
+            assert (got.flags == g[p + "_flags"]).all()
+            assert got.losses.tobytes() == g[p + "_losses"].tobytes()
+            if got.dense_count:
+                assert (got.dense_pool == to_f(g[p + "_dense_pool"])).all()
+            if got.sparse_count:
+                assert (got.nnz_pool == to_f(g[p + "_nnz_pool"])).all()
+                assert (got.meta_pool == g[p + "_meta_pool"]).all()
+
+
+def test_config2_full_size_compression(hs, port):
+    """Config 2 geometry (8 KV heads x 128K, S=1): bit-exact on two heads,
+    structural properties on all (every sparse block decodes to a 2:4 pattern
+    whose kept values are the group's two largest magnitudes)."""
+    from oracle.oracle import SparsityConfig as OCfg
+    import torch
+    U, L = 8, 131072
+    torch.manual_seed(0)
+    x = torch.randn(U, L, 128, device="cuda").to(torch.bfloat16)
+    for axis in (0, 1):
+        dev = hs.prune_compress(x, hs.SparsityConfig(1, 1, 64), 1.0, axis)
+        assert dev.sparse_count == 2048 and dev.dense_count == 0
+        xs = x[[0, 5]].float().cpu().numpy()
+        for i, u in enumerate((0, 5)):
+            assert_cache_equal(dev, u, port.prune_compress(xs[i], OCfg(1, 1, 64), axis, 1.0), f"unit {u}")
+        # round trip on every unit: decompress keeps exactly the top-2 per group
+        dec = hs.decompress(dev).float()
+        grp = (x.float().reshape(U, L, 32, 4) if axis == 0 else
+               x.float().reshape(U, L // 4, 4, 128).transpose(2, 3))
+        dgrp = (dec.reshape(U, L, 32, 4) if axis == 0 else dec.reshape(U, L // 4, 4, 128).transpose(2, 3))
+        assert ((dgrp != 0).sum(-1) <= 2).all()
+        kept = torch.where(dgrp != 0, grp.abs(), torch.zeros_like(grp)).sum(-1)
+        top2 = grp.abs().topk(2, dim=-1).values.sum(-1)
+        assert torch.equal(kept, top2)

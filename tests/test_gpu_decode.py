@@ -1,0 +1,125 @@
+"""GPU parity: split-KV sparse decode (attention.hpp:360-409) against the fp32
+oracle on identical 16-bit inputs, within the north-star bar
+(max-abs 2e-2, mean-rel = sum|e| / sum|ref| 1e-3)."""
+import math
+
+import numpy as np
+import pytest
+
+from tests.helpers import MAX_ABS_TOL, MEAN_REL_TOL, device_to_oracle, err_stats, gen_units, parallel, to_torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hs():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2604_16864_b200 import hierasparse
+    return hierasparse
+
+
+def build_caches(hs, port, U, L, s, dtype, sink=0, window=0, seed=1):
+    kx = gen_units(port, U, L, 128, seed, 0, dtype)
+    vx = gen_units(port, U, L, 128, seed, 1, dtype)
+    cfg = hs.SparsityConfig(s, s, 64, sink, window)
+    kc, vc = hs.prune_cache(to_torch(kx, dtype), to_torch(vx, dtype), cfg)
+    return kx, vx, kc, vc
+
+
+def decode_queries(port, U, gqa, dtype, seed=1):
+    # decode Q streams: role 32 + g (pipeline.hpp:249)
+    q = np.stack([np.stack([port.random_gaussian(1, 128, port.head_seed(seed, u, 32 + g))[0]
+                            for g in range(gqa)]) for u in range(U)])
+    return port.round_to(q, dtype).reshape(U, gqa, 128)
+
+
+def oracle_decode(port, kc, vc, q, scale, splits, k_tail=None, v_tail=None):
+    U = q.shape[0]
+
+    def one(u):
+        kt = None if k_tail is None else k_tail[u]
+        vt = None if v_tail is None else v_tail[u]
+        return port.decode(q[u], device_to_oracle(kc, u), device_to_oracle(vc, u), kt, vt, scale, splits)
+    return np.stack(parallel(one, range(U)))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("L,s,sink,window,gqa,tail", [
+    (4096, 1.0, 0, 0, 1, 0),     # config 1: single head, 4K, 2:4 K+V
+    (4096, 1.0, 0, 0, 4, 0),
+    (4096, 0.5, 64, 256, 4, 0),  # mixed dense/sparse, protected sink + window
+    (2048, 0.0, 0, 0, 4, 0),     # all dense
+    (1024, 0.75, 0, 0, 8, 17),   # ragged dense tail, 8 query rows
+    (64, 1.0, 0, 0, 4, 63),      # one block + tail
+])
+def test_decode_matches_oracle(hs, port, dtype, L, s, sink, window, gqa, tail):
+    U = 3
+    kx, vx, kc, vc = build_caches(hs, port, U, L, s, dtype, sink, window)
+    q = decode_queries(port, U, gqa, dtype)
+    scale = np.float32(1.0 / math.sqrt(128))
+    kt = vt = None
+    if tail:
+        kt = gen_units(port, U, tail, 128, 77, 0, dtype)
+        vt = gen_units(port, U, tail, 128, 77, 1, dtype)
+    want = oracle_decode(port, kc, vc, q, scale, 4, kt, vt)
+    for splits in (0, 1, 7):
+        got = hs.decode_attention(to_torch(q, dtype), kc, vc,
+                                  None if kt is None else to_torch(kt, dtype),
+                                  None if vt is None else to_torch(vt, dtype),
+                                  float(scale), splits=splits).cpu().numpy()
+        mx, mr = err_stats(got, want)
+        assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (splits, mx, mr)
+
+
+def test_decode_gqa_rows_independent(hs, port):
+    """Each GQA row equals its own single-row decode (test_attention.cpp:356-364),
+    within float rounding of the kernel."""
+    U, L = 2, 2048
+    kx, vx, kc, vc = build_caches(hs, port, U, L, 1.0, "f16")
+    q = decode_queries(port, U, 4, "f16")
+    full = hs.decode_attention(to_torch(q, "f16"), kc, vc, splits=3).cpu().numpy()
+    for g in range(4):
+        one = hs.decode_attention(to_torch(q[:, g:g + 1], "f16"), kc, vc, splits=3).cpu().numpy()
+        assert np.abs(one[:, 0] - full[:, g]).max() < 1e-6
+
+
+def test_decode_partial_and_combine(hs, port):
+    """Sequence split across 'devices': partials over contiguous block ranges,
+    LSE-combined, equal the single decode (attention.hpp:380-407)."""
+    import torch
+    U, L = 2, 8192
+    kx, vx, kc, vc = build_caches(hs, port, U, L, 1.0, "bf16")
+    q = to_torch(decode_queries(port, U, 4, "bf16"), "bf16")
+    kt = to_torch(gen_units(port, U, 5, 128, 3, 0, "bf16"), "bf16")
+    vt = to_torch(gen_units(port, U, 5, 128, 3, 1, "bf16"), "bf16")
+    ref = hs.decode_attention(q, kc, vc, kt, vt)
+    nb, parts = kc.logical_blocks, 4
+    ps = [hs.decode_partial(q, kc, vc, nb * r // parts, nb * (r + 1) // parts, kt, vt, include_tail=(r == parts - 1))
+          for r in range(parts)]
+    out = hs.decode_combine(torch.stack(ps))
+    assert (out - ref).abs().max().item() < 1e-5
+
+
+def test_decode_config2_full_size(hs, port):
+    """Config 2: 8 KV heads x 128K tokens, GQA 4, S_K = S_V = 1, bf16 — every
+    head against the oracle's decode_attention."""
+    U, L = 8, 131072
+    kx, vx, kc, vc = build_caches(hs, port, U, L, 1.0, "bf16", seed=2)
+    q = decode_queries(port, U, 4, "bf16", seed=2)
+    scale = np.float32(1.0 / math.sqrt(128))
+    got = hs.decode_attention(to_torch(q, "bf16"), kc, vc, scale=float(scale)).cpu().numpy()
+    want = oracle_decode(port, kc, vc, q, scale, 1)
+    mx, mr = err_stats(got, want)
+    assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
+
+
+def test_decode_rejects_invalid(hs, port):
+    from paper_2604_16864_b200 import ConfigError
+    U = 1
+    kx, vx, kc, vc = build_caches(hs, port, U, 512, 1.0, "bf16")
+    q = to_torch(decode_queries(port, U, 4, "bf16"), "bf16")
+    with pytest.raises(ConfigError):
+        hs.decode_attention(q, vc, kc)          # swapped caches (test_attention.cpp:392-395)
+    with pytest.raises(ConfigError):
+        hs.decode_attention(q.repeat(1, 3, 1), kc, vc)  # 12 rows > 8
