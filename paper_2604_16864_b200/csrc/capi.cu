@@ -5,6 +5,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
+
+#include <cmath>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -76,7 +78,8 @@ void* dummy_buffer() {
     return p;
 }
 
-// 2-D tile map over a row-major [outer][inner] 16-bit array.
+// 2-D tile map over a row-major [outer][inner] 16-bit array.  Encoded maps are
+// cached by (pointer, geometry, swizzle) so steady-state calls skip the driver.
 bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
               uint32_t box_outer, CUtensorMapSwizzle sw) {
     EncodeTiledFn fn = encode_fn();
@@ -86,13 +89,31 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
         outer = box_outer;
         if (!ptr) return false;
     }
+    using Key = std::tuple<const void*, uint64_t, uint64_t, uint32_t, uint32_t, int>;
+    static std::mutex mu;
+    static std::map<Key, CUtensorMap> cache;
+    const Key key{ptr, inner, outer, box_inner, box_outer, static_cast<int>(sw)};
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *m = it->second;
+            return true;
+        }
+    }
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {inner * 2};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t es[2] = {1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    const bool ok = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    if (ok) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (cache.size() > 4096) cache.clear();
+        cache[key] = *m;
+    }
+    return ok;
 }
 
 // ------------------------------------------------------------ workspaces ---
@@ -212,12 +233,12 @@ int choose_splits(int n_units, int nb) {
     const int slots = hs::decode_ctas_per_sm() * sm_count();
     int best = 1;
     double best_cost = 1e30;
-    for (int s = 1; s <= nb && s <= 256; ++s) {
+    for (int s = 1; s <= nb && s <= 1024; ++s) {
         const int ctas = n_units * s;
         const int waves = (ctas + slots - 1) / slots;
-        const double per_cta = static_cast<double>(nb) / s;  // blocks per CTA
-        // wave-quantised time + per-CTA fixed overhead (~2 blocks) + combine cost
-        const double cost = waves * (per_cta + 2.0) + 0.02 * s;
+        const double per_cta = std::ceil(static_cast<double>(nb) / s);  // blocks per CTA
+        // wave-quantised time + per-CTA fixed overhead (~3 blocks) + combine cost
+        const double cost = waves * (per_cta + 3.0) + 0.02 * s;
         if (cost < best_cost - 1e-9) {
             best_cost = cost;
             best = s;
@@ -421,6 +442,13 @@ static hs_status decode_common(const void* q, const hs_device_cache* k, const hs
     L.v_index = v->index_map;
     L.k_meta = k->meta_pool;
     L.v_meta = v->meta_pool;
+    L.k_nnz = k->nnz_pool;
+    L.v_nnz = v->nnz_pool;
+    L.k_dense = k->dense_pool;
+    L.v_dense = v->dense_pool;
+    L.prefetch_distance = 1;
+    if (const char* env = getenv("HS_DECODE_PF")) L.prefetch_distance = atoi(env);
+    if (const char* env = getenv("HS_DECODE_DEBUG_STREAM_ONLY")) L.debug_stream_only = atoi(env);
     L.k_tail = k_tail;
     L.v_tail = v_tail;
     L.block_begin = block_begin;
@@ -431,6 +459,10 @@ static hs_status decode_common(const void* q, const hs_device_cache* k, const hs
     if (ns > span) ns = span;  // attention.hpp:373-374 clamp
     if (ns < 1) ns = 1;
     L.nsplit = ns;
+    L.max_blocks_per_cta = (span + ns - 1) / ns + 1;
+    HS_CHECK_CONFIG(L.max_blocks_per_cta <= 8192,
+                    "decode_attention: %d blocks per CTA exceeds the index stage; use more splits",
+                    L.max_blocks_per_cta);
     if ((st = fill_decode_maps(L, k, v))) return st;
     const size_t part_bytes = static_cast<size_t>(L.n_units) * ns * gqa * (hs::kHeadDim + 2) * sizeof(float);
     const size_t cnt_bytes = ((static_cast<size_t>(L.n_units) * sizeof(int) + 255) / 256) * 256;

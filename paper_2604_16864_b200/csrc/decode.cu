@@ -39,11 +39,10 @@ __device__ __forceinline__ uint32_t meta_sel(uint32_t lo_row, uint32_t hi_row, u
 }
 
 template <typename T, int NW, bool HILO>
-__global__ void __launch_bounds__(32 * (NW + 1)) decode_kernel(const __grid_constant__ DecodeLaunch L,
-                                                               int spw, StageLayout lay) {
+__global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__ DecodeLaunch L,
+                                                         int spw, StageLayout lay) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[16];
-    __shared__ __align__(8) uint64_t empty_bar[16];
     __shared__ int s_ticket;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -56,62 +55,95 @@ __global__ void __launch_bounds__(32 * (NW + 1)) decode_kernel(const __grid_cons
     const int nblk = b1 - b0;
     const bool with_tail = L.include_tail && split == L.nsplit - 1 && L.tail > 0;
 
-    const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-    uint8_t* const base_ptr = smem_raw + (base - smem_u32(smem_raw));
+    // Dynamic smem: [index entries of this range (int16 k, v)] [1 KB pad] [ring]
+    const uint32_t raw = smem_u32(smem_raw);
+    int16_t* s_kidx = reinterpret_cast<int16_t*>(smem_raw);
+    int16_t* s_vidx = s_kidx + L.max_blocks_per_cta;
+    const uint32_t idx_bytes = static_cast<uint32_t>(L.max_blocks_per_cta) * 4u;
+    const uint32_t base = (raw + idx_bytes + 1023u) & ~1023u;
+    uint8_t* const base_ptr = smem_raw + (base - raw);
 
-    const int stages = NW * spw;
+    const int16_t* kidx = L.k_index + static_cast<int64_t>(u) * L.nb;
+    const int16_t* vidx = L.v_index + static_cast<int64_t>(u) * L.nb;
+    for (int i = threadIdx.x; i < nblk; i += 32 * NW) {
+        s_kidx[i] = kidx[b0 + i];
+        s_vidx[i] = vidx[b0 + i];
+    }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < stages; ++s) {
-            mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], 1);
-        }
+        for (int s = 0; s < NW * spw; ++s) mbar_init(&full_bar[s], 1);
         fence_barrier_init();
     }
     __syncthreads();
 
-    const int16_t* kidx = L.k_index + static_cast<int64_t>(u) * L.nb;
-    const int16_t* vidx = L.v_index + static_cast<int64_t>(u) * L.nb;
-
-    if (warp == NW) {
-        // ------------------------------------------------------ producer ----
-        if (lane == 0) {
+    // Each consumer warp streams its own blocks (i = warp + NW*k) into its own
+    // `spw` ring slots: it issues block k+spw right after finishing block k, so
+    // no empty barriers are needed and a waiter is never a phase ahead.
+    auto issue = [&](int k) {
+        const int i = warp + NW * k;
+        const int s = warp * spw + k % spw;
+        const int b = b0 + i;
+        const int ke = s_kidx[i], ve = s_vidx[i];
+        uint8_t* kreg = base_ptr + s * lay.stage_bytes;
+        uint8_t* vreg = kreg + lay.k_bytes;
+        const uint32_t bytes = (ke > 0 ? 16384u : 9216u) + (ve > 0 ? 16384u : 9216u);
+        mbar_arrive_expect_tx(&full_bar[s], bytes);
+        if (ke > 0) {
+            const int row = (u * L.k_dense_count + ke - 1) * kBlock;
+            tma_tile_g2s(kreg, &L.tm_kden, 0, row, &full_bar[s]);
+            tma_tile_g2s(kreg + 8192, &L.tm_kden, 64, row, &full_bar[s]);
+        } else {
+            const int sb = u * L.k_sparse_count + (-ke - 1);
+            if (L.debug_stream_only == 2)
+                tma_bulk_g2s(kreg, static_cast<const uint16_t*>(L.k_nnz) + static_cast<int64_t>(sb) * 4096, 8192, &full_bar[s]);
+            else
+                tma_tile_g2s(kreg, &L.tm_knnz, 0, sb * kBlock, &full_bar[s]);
+            tma_bulk_g2s(kreg + 8192, L.k_meta + static_cast<int64_t>(sb) * 512, 1024, &full_bar[s]);
+        }
+        if (ve > 0) {
+            const int row = (u * L.v_dense_count + ve - 1) * kHeadDim;
+            tma_tile_g2s(vreg, &L.tm_vden, 0, row, &full_bar[s]);
+        } else {
+            const int sb = u * L.v_sparse_count + (-ve - 1);
+            if (L.debug_stream_only == 2)
+                tma_bulk_g2s(vreg, static_cast<const uint16_t*>(L.v_nnz) + static_cast<int64_t>(sb) * 4096, 8192, &full_bar[s]);
+            else
+                tma_tile_g2s(vreg, &L.tm_vnnz, 0, sb * kHeadDim, &full_bar[s]);
+            tma_bulk_g2s(vreg + 8192, L.v_meta + static_cast<int64_t>(sb) * 512, 1024, &full_bar[s]);
+        }
+        (void)b;
+    };
+    // L2 prefetch of a future block of this warp (pools are contiguous per slot).
+    auto prefetch = [&](int k) {
+        const int i = warp + NW * k;
+        const int ke = s_kidx[i], ve = s_vidx[i];
+        const uint16_t* kd = static_cast<const uint16_t*>(L.k_dense);
+        const uint16_t* vd = static_cast<const uint16_t*>(L.v_dense);
+        if (ke > 0) {
+            prefetch_l2(kd + (static_cast<int64_t>(u) * L.k_dense_count + ke - 1) * (kBlock * kHeadDim), 16384);
+        } else {
+            const int64_t sb = static_cast<int64_t>(u) * L.k_sparse_count + (-ke - 1);
+            prefetch_l2(static_cast<const uint16_t*>(L.k_nnz) + sb * (kBlock * kHeadDim / 2), 8192);
+            prefetch_l2(L.k_meta + sb * 512, 1024);
+        }
+        if (ve > 0) {
+            prefetch_l2(vd + (static_cast<int64_t>(u) * L.v_dense_count + ve - 1) * (kBlock * kHeadDim), 16384);
+        } else {
+            const int64_t sb = static_cast<int64_t>(u) * L.v_sparse_count + (-ve - 1);
+            prefetch_l2(static_cast<const uint16_t*>(L.v_nnz) + sb * (kBlock * kHeadDim / 2), 8192);
+            prefetch_l2(L.v_meta + sb * 512, 1024);
+        }
+    };
+    const int nk = nblk > warp ? (nblk - warp + NW - 1) / NW : 0;  // blocks of this warp
+    const int pf = L.prefetch_distance;
+    if (lane == 0) {
+        if (warp == 0) {
             prefetch_tmap(&L.tm_knnz);
             prefetch_tmap(&L.tm_vnnz);
-            prefetch_tmap(&L.tm_kden);
-            prefetch_tmap(&L.tm_vden);
-            for (int i = 0; i < nblk; ++i) {
-                // Block i belongs to consumer warp i % NW; each warp owns `spw`
-                // private slots, so no waiter is ever more than one phase ahead.
-                const int k = i / NW;
-                const int s = (i % NW) * spw + k % spw;
-                mbar_wait(&empty_bar[s], ((k / spw) & 1) ^ 1);
-                const int b = b0 + i;
-                const int ke = kidx[b], ve = vidx[b];
-                uint8_t* kreg = base_ptr + s * lay.stage_bytes;
-                uint8_t* vreg = kreg + lay.k_bytes;
-                const uint32_t bytes = (ke > 0 ? 16384u : 9216u) + (ve > 0 ? 16384u : 9216u);
-                mbar_arrive_expect_tx(&full_bar[s], bytes);
-                if (ke > 0) {
-                    const int row = (u * L.k_dense_count + ke - 1) * kBlock;
-                    tma_tile_g2s(kreg, &L.tm_kden, 0, row, &full_bar[s]);
-                    tma_tile_g2s(kreg + 8192, &L.tm_kden, 64, row, &full_bar[s]);
-                } else {
-                    const int sb = u * L.k_sparse_count + (-ke - 1);
-                    tma_tile_g2s(kreg, &L.tm_knnz, 0, sb * kBlock, &full_bar[s]);
-                    tma_bulk_g2s(kreg + 8192, L.k_meta + static_cast<int64_t>(sb) * 512, 1024, &full_bar[s]);
-                }
-                if (ve > 0) {
-                    const int row = (u * L.v_dense_count + ve - 1) * kHeadDim;
-                    tma_tile_g2s(vreg, &L.tm_vden, 0, row, &full_bar[s]);
-                } else {
-                    const int sb = u * L.v_sparse_count + (-ve - 1);
-                    tma_tile_g2s(vreg, &L.tm_vnnz, 0, sb * kHeadDim, &full_bar[s]);
-                    tma_bulk_g2s(vreg + 8192, L.v_meta + static_cast<int64_t>(sb) * 512, 1024, &full_bar[s]);
-                }
-            }
         }
-        __syncwarp();  // reconverge before the CTA-wide barrier below
+        for (int k = 0; k < spw && k < nk; ++k) issue(k);
+        for (int k = spw; k < spw + pf && k < nk; ++k) prefetch(k);
     }
+    __syncwarp();
 
     // ------------------------------------------------------- consumers ----
     const int g = lane >> 2, t = lane & 3, half = t & 1;
@@ -123,7 +155,7 @@ __global__ void __launch_bounds__(32 * (NW + 1)) decode_kernel(const __grid_cons
 #pragma unroll
         for (int k = 0; k < 4; ++k) o[i][k] = 0.f;
 
-    if (warp < NW) {
+    {
         // Q^T fragments for GEMM1 (B operand, k = channel, n = query row g).
         const T* q = static_cast<const T*>(L.q) + static_cast<int64_t>(u) * gqa * kHeadDim;
         uint32_t qb[4][4];
@@ -133,12 +165,17 @@ __global__ void __launch_bounds__(32 * (NW + 1)) decode_kernel(const __grid_cons
             for (int x = 0; x < 4; ++x)
                 qb[j][x] = g < gqa ? ld_pair(q + g * kHeadDim + 32 * j + 8 * x + 2 * t) : 0u;
 
-        for (int i = warp; i < nblk; i += NW) {
-            const int k = i / NW;
+        for (int k = 0; k < nk; ++k) {
+            const int i = warp + NW * k;
             const int s = warp * spw + k % spw;
             mbar_wait(&full_bar[s], (k / spw) & 1);
-            const int b = b0 + i;
-            const bool kd = kidx[b] > 0, vd = vidx[b] > 0;
+            const bool kd = s_kidx[i] > 0, vd = s_vidx[i] > 0;
+            if (L.debug_stream_only) {  // pipeline-only measurement mode (tools/)
+                __syncwarp();
+                if (lane == 0 && k + spw < nk) issue(k + spw);
+                __syncwarp();
+                continue;
+            }
             const uint32_t kreg = base + s * lay.stage_bytes;
             const uint32_t vreg = kreg + lay.k_bytes;
 
@@ -152,18 +189,23 @@ __global__ void __launch_bounds__(32 * (NW + 1)) decode_kernel(const __grid_cons
             const int lch = lane >> 4;
             if (!kd) {
                 const uint8_t* kmeta = base_ptr + (kreg - base) + 8192;
+                uint32_t e[4][4];
 #pragma unroll
                 for (int mi = 0; mi < 4; ++mi) {
                     const uint4 mlo = *reinterpret_cast<const uint4*>(kmeta + (16 * mi + g) * 16);
                     const uint4 mhi = *reinterpret_cast<const uint4*>(kmeta + (16 * mi + g + 8) * 16);
-                    const uint32_t e[4] = {meta_sel(mlo.x, mhi.x, half), meta_sel(mlo.y, mhi.y, half),
-                                           meta_sel(mlo.z, mhi.z, half), meta_sel(mlo.w, mhi.w, half)};
+                    e[mi][0] = meta_sel(mlo.x, mhi.x, half);
+                    e[mi][1] = meta_sel(mlo.y, mhi.y, half);
+                    e[mi][2] = meta_sel(mlo.z, mhi.z, half);
+                    e[mi][3] = meta_sel(mlo.w, mhi.w, half);
+                }
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        uint32_t a[4];
-                        ldmatrix_x4(kreg + sw128(16 * mi + lrow, 2 * j + lch), a);
-                        mma_sp_16832<T>(sc[mi], a, qb[j], e[j]);
-                    }
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t a[4][4];
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi) ldmatrix_x4(kreg + sw128(16 * mi + lrow, 2 * j + lch), a[mi]);
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi) mma_sp_16832<T>(sc[mi], a[mi], qb[j], e[mi][j]);
                 }
             } else {
 #pragma unroll
@@ -231,21 +273,25 @@ __global__ void __launch_bounds__(32 * (NW + 1)) decode_kernel(const __grid_cons
             if (!vd) {
                 const uint8_t* vmeta = base_ptr + (vreg - base) + 8192;
 #pragma unroll
-                for (int mi = 0; mi < 8; ++mi) {
-                    const uint2 mlo = *reinterpret_cast<const uint2*>(vmeta + (16 * mi + g) * 8);
-                    const uint2 mhi = *reinterpret_cast<const uint2*>(vmeta + (16 * mi + g + 8) * 8);
-                    const uint32_t e[2] = {meta_sel(mlo.x, mhi.x, half), meta_sel(mlo.y, mhi.y, half)};
+                for (int j = 0; j < 2; ++j) {
+                    const uint32_t bh[4] = {bt_hi[2 * j][0], bt_hi[2 * j][1], bt_hi[2 * j + 1][0], bt_hi[2 * j + 1][1]};
+                    const uint32_t bl[4] = {bt_lo[2 * j][0], bt_lo[2 * j][1], bt_lo[2 * j + 1][0], bt_lo[2 * j + 1][1]};
 #pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        uint32_t a[4];
-                        ldmatrix_x4(vreg + sw64(16 * mi + lrow, 2 * j + lch), a);
-                        const uint32_t bh[4] = {bt_hi[2 * j][0], bt_hi[2 * j][1], bt_hi[2 * j + 1][0],
-                                                bt_hi[2 * j + 1][1]};
-                        mma_sp_16832<T>(o[mi], a, bh, e[j]);
+                    for (int mh = 0; mh < 2; ++mh) {
+                        uint32_t a[4][4], e[4];
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) {
+                            const int mi = 4 * mh + x;
+                            const uint32_t mlo = *reinterpret_cast<const uint32_t*>(vmeta + (16 * mi + g) * 8 + 4 * j);
+                            const uint32_t mhi = *reinterpret_cast<const uint32_t*>(vmeta + (16 * mi + g + 8) * 8 + 4 * j);
+                            e[x] = meta_sel(mlo, mhi, half);
+                            ldmatrix_x4(vreg + sw64(16 * mi + lrow, 2 * j + lch), a[x]);
+                        }
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) mma_sp_16832<T>(o[4 * mh + x], a[x], bh, e[x]);
                         if (HILO) {
-                            const uint32_t bl[4] = {bt_lo[2 * j][0], bt_lo[2 * j][1], bt_lo[2 * j + 1][0],
-                                                    bt_lo[2 * j + 1][1]};
-                            mma_sp_16832<T>(o[mi], a, bl, e[j]);
+#pragma unroll
+                            for (int x = 0; x < 4; ++x) mma_sp_16832<T>(o[4 * mh + x], a[x], bl, e[x]);
                         }
                     }
                 }
@@ -260,8 +306,10 @@ __global__ void __launch_bounds__(32 * (NW + 1)) decode_kernel(const __grid_cons
                         if (HILO) mma_16816<T>(o[mi], a, bt_lo[kk][0], bt_lo[kk][1]);
                     }
             }
+            __syncwarp();  // every lane is done with slot s
+            if (lane == 0 && k + spw < nk) issue(k + spw);
+            if (lane == 0 && k + spw + pf < nk) prefetch(k + spw + pf);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[s]);
         }
 
         // ---------------- dense tail (attention.hpp:289-297) ----------------
@@ -314,7 +362,7 @@ __global__ void __launch_bounds__(32 * (NW + 1)) decode_kernel(const __grid_cons
     float* s_o = reinterpret_cast<float*>(base_ptr);            // [NW][gqa][128]
     float* s_m = s_o + NW * kMaxGqa * kHeadDim;                 // [NW][gqa]
     float* s_l = s_m + NW * kMaxGqa;
-    if (warp < NW) {
+    {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const int qq = 2 * t + e;
@@ -332,7 +380,7 @@ __global__ void __launch_bounds__(32 * (NW + 1)) decode_kernel(const __grid_cons
         }
     }
     __syncthreads();
-    const int nthr = 32 * (NW + 1);
+    const int nthr = 32 * NW;
     const int stride_p = gqa * (kHeadDim + 2);
     float* part = L.partial + (static_cast<int64_t>(u) * L.nsplit + split) * stride_p;
     constexpr float kLn2 = 0.6931471805599453f;
@@ -416,9 +464,13 @@ template <typename T, int NW, bool HILO>
 cudaError_t launch_t(const DecodeLaunch& L, int spw, StageLayout lay, size_t smem,
                      cudaStream_t s) {
     auto k = decode_kernel<T, NW, HILO>;
-    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err) return err;
-    k<<<dim3(L.nsplit, L.n_units), 32 * (NW + 1), smem, s>>>(L, spw, lay);
+    static int configured_smem = 0;  // per instantiation; raise the opt-in once
+    if (static_cast<int>(smem) > configured_smem) {
+        cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (err) return err;
+        configured_smem = static_cast<int>(smem);
+    }
+    k<<<dim3(L.nsplit, L.n_units), 32 * NW, smem, s>>>(L, spw, lay);
     return cudaGetLastError();
 }
 
@@ -426,34 +478,48 @@ cudaError_t launch_t(const DecodeLaunch& L, int spw, StageLayout lay, size_t sme
 
 int decode_warps() {
     const char* env = getenv("HS_DECODE_WARPS");
-    return env && atoi(env) == 8 ? 8 : 4;
-}
-
-cudaError_t launch_decode(const DecodeLaunch& L, cudaStream_t s) {
-    StageLayout lay;
-    lay.k_bytes = L.k_dense_count > 0 ? 16384u : 9216u;
-    lay.v_bytes = L.v_dense_count > 0 ? 16384u : 9216u;
-    lay.stage_bytes = lay.k_bytes + lay.v_bytes;
-    const int NW = decode_warps();
-    // Ring budget per CTA (decode_ctas_per_sm() CTAs share an SM's 227 KB).
-    const uint32_t budget = (decode_ctas_per_sm() == 1 ? 200u : 100u) * 1024u;
-    int spw = static_cast<int>(budget / (NW * lay.stage_bytes));
-    if (const char* env = getenv("HS_DECODE_SPW")) spw = atoi(env);
-    spw = spw < 1 ? 1 : (spw * NW > 16 ? 16 / NW : spw);
-    size_t smem = static_cast<size_t>(NW * spw) * lay.stage_bytes + 1024;
-    const size_t scratch = (NW * kMaxGqa * kHeadDim + 2 * NW * kMaxGqa) * sizeof(float) + 1024;
-    if (smem < scratch) smem = scratch;
-    if (NW == 8) {
-        if (L.bf16) return launch_t<__nv_bfloat16, 8, true>(L, spw, lay, smem, s);
-        return launch_t<__half, 8, false>(L, spw, lay, smem, s);
-    }
-    if (L.bf16) return launch_t<__nv_bfloat16, 4, true>(L, spw, lay, smem, s);
-    return launch_t<__half, 4, false>(L, spw, lay, smem, s);
+    const int w = env ? atoi(env) : 8;
+    return w == 4 ? 4 : 8;
 }
 
 int decode_ctas_per_sm() {
     const char* env = getenv("HS_DECODE_CTAS_PER_SM");
     return env && atoi(env) == 2 ? 2 : 1;
+}
+
+size_t decode_smem_bytes(const DecodeLaunch& L, int* nw_out, int* spw_out, StageLayout* lay_out) {
+    StageLayout lay;
+    lay.k_bytes = L.k_dense_count > 0 ? 16384u : 9216u;
+    lay.v_bytes = L.v_dense_count > 0 ? 16384u : 9216u;
+    lay.stage_bytes = lay.k_bytes + lay.v_bytes;
+    const uint32_t idx_bytes = static_cast<uint32_t>(L.max_blocks_per_cta) * 4u;
+    const uint32_t budget = (decode_ctas_per_sm() == 1 ? 225u : 112u) * 1024u - idx_bytes - 2048u;
+    int NW = decode_warps();
+    while (NW > 4 && static_cast<uint32_t>(NW) * lay.stage_bytes > budget) NW = 4;  // dense stages are 32 KB
+    int spw = static_cast<int>(budget / (NW * lay.stage_bytes));
+    if (const char* env = getenv("HS_DECODE_SPW")) spw = atoi(env);
+    if (spw * NW > 16) spw = 16 / NW;
+    if (spw < 1) spw = 1;
+    size_t smem = static_cast<size_t>(NW * spw) * lay.stage_bytes;
+    const size_t scratch = (NW * kMaxGqa * kHeadDim + 2 * NW * kMaxGqa) * sizeof(float);
+    if (smem < scratch) smem = scratch;
+    smem += idx_bytes + 1024;
+    *nw_out = NW;
+    *spw_out = spw;
+    *lay_out = lay;
+    return smem;
+}
+
+cudaError_t launch_decode(const DecodeLaunch& L, cudaStream_t s) {
+    int nw, spw;
+    StageLayout lay;
+    const size_t smem = decode_smem_bytes(L, &nw, &spw, &lay);
+    if (nw == 4) {
+        if (L.bf16) return launch_t<__nv_bfloat16, 4, true>(L, spw, lay, smem, s);
+        return launch_t<__half, 4, false>(L, spw, lay, smem, s);
+    }
+    if (L.bf16) return launch_t<__nv_bfloat16, 8, true>(L, spw, lay, smem, s);
+    return launch_t<__half, 8, false>(L, spw, lay, smem, s);
 }
 
 cudaError_t launch_combine(const float* partials, int n_parts, int n_units, int gqa, int d,

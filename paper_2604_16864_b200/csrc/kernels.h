@@ -55,11 +55,18 @@ struct DecodeLaunch {
     const int16_t* v_index;
     const uint16_t* k_meta;  // [u][sparse][512]
     const uint16_t* v_meta;
+    const void* k_nnz;       // pools (for L2 prefetch; TMA reads through the maps)
+    const void* v_nnz;
+    const void* k_dense;
+    const void* v_dense;
+    int prefetch_distance;   // blocks per warp prefetched into L2 ahead of the ring
+    int debug_stream_only;   // tools only: stream the ring without math
     const void* k_tail;      // [u][tail][d]
     const void* v_tail;
     // split geometry: unit u, split s covers blocks [nb*s/nsplit, nb*(s+1)/nsplit)
     int nsplit;
     int block_begin, block_end;  // restrict to a block range (partial API)
+    int max_blocks_per_cta;      // ceil(span / nsplit): sizes the smem index stage
     int include_tail;
     // outputs
     float* partial;          // [u][nsplit][gqa][d+2] (O, m, l)

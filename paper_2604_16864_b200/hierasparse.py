@@ -35,6 +35,10 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+def _LIB():
+    return capi._lib if capi._lib is not None else capi.load()
+
+
 def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None or t.numel() == 0 else t.data_ptr()
 
@@ -97,10 +101,20 @@ class DeviceCompressedCache:
         return self.logical_blocks * self.block_size
 
     def c(self) -> capi.DeviceCacheC:
-        return capi.DeviceCacheC(_dtype_code(self.dtype), self.axis, self.head_dim, self.block_size,
-                                 self.n_units, self.logical_blocks, self.dense_count, self.sparse_count,
-                                 _ptr(self.index_map), _ptr(self.dense_pool), _ptr(self.nnz_pool),
-                                 _ptr(self.meta_pool), _ptr(self.slot_block))
+        """The C-ABI descriptor (built once; the pool tensors never move)."""
+        cs = getattr(self, "_c_struct", None)
+        if cs is None:
+            cs = capi.DeviceCacheC(_dtype_code(self.dtype), self.axis, self.head_dim, self.block_size,
+                                   self.n_units, self.logical_blocks, self.dense_count, self.sparse_count,
+                                   _ptr(self.index_map), _ptr(self.dense_pool), _ptr(self.nnz_pool),
+                                   _ptr(self.meta_pool), _ptr(self.slot_block))
+            self._c_struct = cs
+            self._c_ref = C.byref(cs)
+        return cs
+
+    def cref(self):
+        self.c()
+        return self._c_ref
 
     def measure_size(self) -> dict:
         """measure_size (compressed_cache.hpp:303-310), per unit."""
@@ -199,16 +213,47 @@ def decode_attention(q: torch.Tensor, k: DeviceCompressedCache, v: DeviceCompres
                      out: torch.Tensor | None = None) -> torch.Tensor:
     """decode_attention (attention.hpp:360-409) for every unit: q [units, gqa, d] -> fp32."""
     U = k.n_units
-    q = q.reshape(U, -1, k.head_dim).contiguous()
+    if q.dim() != 3 or q.shape[0] != U or not q.is_contiguous():
+        q = q.reshape(U, -1, k.head_dim).contiguous()
     gqa = q.shape[1]
     kt, vt, tail = _tails(k_tail, v_tail, U, k.head_dim)
     scale = 1.0 / math.sqrt(k.head_dim) if scale is None else scale
     if out is None:
         out = torch.empty((U, gqa, k.head_dim), dtype=torch.float32, device=q.device)
-    kc, vc = k.c(), v.c()
-    capi.check(capi.load().hs_decode(q.data_ptr(), C.byref(kc), C.byref(vc), _ptr(kt), _ptr(vt), tail, gqa,
-                                     scale, splits, out.data_ptr(), _stream()))
+    capi.check(_LIB().hs_decode(q.data_ptr(), k.cref(), v.cref(), _ptr(kt), _ptr(vt), tail, gqa,
+                                scale, splits, out.data_ptr(), _stream()))
     return out
+
+
+class DecodePlan:
+    """A decode step captured once as a CUDA graph and replayed per token:
+    hs_decode's kernels with fixed caches, query and output buffers (the host
+    enqueue cost disappears from the step; inputs are refreshed in place)."""
+
+    def __init__(self, q: torch.Tensor, k: DeviceCompressedCache, v: DeviceCompressedCache,
+                 scale: float | None = None, splits: int = 0):
+        self.q = q.contiguous().clone()
+        self.k, self.v = k, v
+        self.out = torch.empty((k.n_units, self.q.shape[1], k.head_dim), dtype=torch.float32, device=q.device)
+        # Warm up on the capture stream so its workspace and TMA descriptors exist
+        # before capture (no allocation may happen inside the graph).
+        self.stream = torch.cuda.Stream()
+        self.stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.stream):
+            decode_attention(self.q, k, v, scale=scale, splits=splits, out=self.out)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        n0 = capi.kernel_launches()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            decode_attention(self.q, k, v, scale=scale, splits=splits, out=self.out)
+        torch.cuda.synchronize()
+        self.kernels_per_step = capi.kernel_launches() - n0  # native kernels inside the graph
+
+    def __call__(self, q: torch.Tensor | None = None) -> torch.Tensor:
+        if q is not None:
+            self.q.copy_(q, non_blocking=True)
+        self.graph.replay()
+        return self.out
 
 
 def decode_partial(q, k: DeviceCompressedCache, v: DeviceCompressedCache, block_begin: int, block_end: int,
