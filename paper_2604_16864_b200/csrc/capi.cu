@@ -507,9 +507,62 @@ HS_API hs_status hs_decode_combine(const float* partials, uint32_t n_parts, uint
 HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_device_cache* k,
                             const hs_device_cache* v, const void* k_tail, const void* v_tail, uint32_t tail,
                             int causal, float scale, float* out, void* stream) {
-    (void)q; (void)n_q; (void)gqa; (void)k; (void)v; (void)k_tail; (void)v_tail; (void)tail;
-    (void)causal; (void)scale; (void)out; (void)stream;
-    return fail(HS_ERR_CONFIG, "prefill_attention: device kernel not built yet");
+    hs_status st = check_pair(k, v);
+    if (st) return st;
+    HS_CHECK_CONFIG(q != nullptr && out != nullptr, "prefill_attention: null argument");
+    HS_CHECK_CONFIG(gqa >= 1 && n_q >= 1, "prefill_attention: empty query set");
+    const uint64_t n_kv = static_cast<uint64_t>(k->logical_blocks) * k->block_size + tail;
+    HS_CHECK_CONFIG(n_kv > 0, "prefill_attention: empty key/value cache");
+    HS_CHECK_CONFIG(!causal || n_kv >= n_q, "prefill_attention: causal queries exceed key sequence");
+    HS_CHECK_CONFIG(tail == 0 && k_tail == nullptr,
+                    "prefill_attention: the tcgen05 kernel takes block-aligned caches (dense tail not supported)");
+    HS_CHECK_CONFIG(k->logical_blocks / 2 + 8 <= 1280,
+                    "prefill_attention: %u blocks exceed the kernel's key-tile list", k->logical_blocks);
+    HS_CHECK_CONFIG(k->slot_block != nullptr, "prefill_attention: key cache needs slot_block");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    hs::PrefillLaunch L{};
+    L.bf16 = k->dtype == HS_DTYPE_BF16;
+    L.n_units = k->n_units;
+    L.nb = k->logical_blocks;
+    L.gqa = gqa;
+    L.n_q = n_q;
+    L.tail = 0;
+    L.causal = causal;
+    L.k_dense_count = k->dense_count;
+    L.k_sparse_count = k->sparse_count;
+    L.v_dense_count = v->dense_count;
+    L.v_sparse_count = v->sparse_count;
+    L.scale_log2 = scale * 1.4426950408889634f;
+    L.q = q;
+    L.k_index = k->index_map;
+    L.v_index = v->index_map;
+    L.k_slot_block = k->slot_block;
+    L.k_meta = k->meta_pool;
+    L.v_meta = v->meta_pool;
+    L.out = out;
+    static int* dbg = nullptr;
+    if (getenv("HS_DEBUG_WAIT")) {
+        if (!dbg) cudaMalloc(&dbg, 64);
+        cudaMemsetAsync(dbg, 0, 64, s);
+        L.dbg = dbg;
+    }
+    const uint64_t U = k->n_units;
+    bool ok = make_map(&L.tm_q, q, 128, U * gqa * n_q, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_map(&L.tm_knnz, k->nnz_pool, 64, U * k->sparse_count * 64, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_map(&L.tm_kden, k->dense_pool, 128, U * k->dense_count * 64, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_map(&L.tm_vnnz, v->nnz_pool, 32, U * v->sparse_count * 128, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
+    ok &= make_map(&L.tm_vden, v->dense_pool, 64, U * v->dense_count * 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (!ok) return fail(HS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    cudaError_t e = hs::launch_prefill(L, s);
+    count_launch();
+    if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
+    if (L.dbg) {
+        int h[4] = {0, 0, 0, 0};
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, L.dbg, sizeof h, cudaMemcpyDeviceToHost);
+        if (h[0]) return fail(HS_ERR_CUDA, "prefill watchdog: barrier tag %d parity %d block %d thread %d", h[0], h[1], h[2], h[3]);
+    }
+    return HS_OK;
 }
 
 }  // extern "C"

@@ -81,6 +81,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Bounded wait for debugging pipelines: after `limit` failed probes records
+// (tag, parity, block, warp) into dbg[0..3] and traps, so a protocol bug shows
+// up as an error with a location instead of a hang.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int* dbg, int tag) {
+    if (dbg == nullptr) {
+        mbar_wait(bar, parity);
+        return;
+    }
+    for (long long i = 0; !mbar_try(bar, parity); ++i) {
+        if (i > (1ll << 24)) {
+            if (atomicCAS(dbg, 0, tag) == 0) {
+                dbg[1] = static_cast<int>(parity);
+                dbg[2] = static_cast<int>(blockIdx.x + 1000 * blockIdx.y + 100000 * blockIdx.z);
+                dbg[3] = static_cast<int>(threadIdx.x);
+                __threadfence_system();
+            }
+            asm volatile("trap;");
+        }
+    }
+}
+
 // ------------------------------------------------------------------ TMA ---
 // 1-D bulk copy global -> shared, completion on an mbarrier (UBLKCP).
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,

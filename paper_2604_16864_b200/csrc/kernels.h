@@ -95,6 +95,7 @@ struct PrefillLaunch {
     const void* k_tail;
     const void* v_tail;
     float* out;
+    int* dbg;                // optional pipeline watchdog record (debug)
     CUtensorMap tm_q, tm_knnz, tm_kden, tm_vnnz, tm_vden;
 };
 cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s);

@@ -1,0 +1,86 @@
+"""GPU parity: tcgen05 Trans-Both prefill (attention.hpp:323-354) against the
+fp32 oracle on identical 16-bit inputs, within max-abs 2e-2 / mean-rel 1e-3.
+Large shapes are checked on sampled query rows through attend_range with
+explicit positions (attention.hpp:249-253), exactly the reference arithmetic
+restricted to those rows."""
+import math
+
+import numpy as np
+import pytest
+
+from tests.helpers import MAX_ABS_TOL, MEAN_REL_TOL, device_to_oracle, err_stats, gen_units, parallel, to_torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hs():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2604_16864_b200 import hierasparse
+    return hierasparse
+
+
+def setup(hs, port, U, L, s, dtype, gqa, n_q, sink=0, window=0, seed=3):
+    kx = gen_units(port, U, L, 128, seed, 0, dtype)
+    vx = gen_units(port, U, L, 128, seed, 1, dtype)
+    kc, vc = hs.prune_cache(to_torch(kx, dtype), to_torch(vx, dtype), hs.SparsityConfig(s, s, 64, sink, window))
+    # prefill Q streams: role 2 + g (pipeline.hpp:202-203), last n_q rows
+    q = np.stack([np.stack([port.round_to(port.random_gaussian(n_q, 128, port.head_seed(seed, u, 2 + g)), dtype)
+                            for g in range(gqa)]) for u in range(U)])
+    return kc, vc, q
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("L,n_q,s,sink,window,causal", [
+    (512, 512, 1.0, 0, 0, True),
+    (512, 512, 0.0, 0, 0, True),
+    (1024, 1024, 0.5, 64, 128, True),
+    (1024, 300, 0.75, 0, 0, True),    # queries at the end of the sequence, partial tile
+    (768, 256, 0.25, 0, 0, False),
+    (640, 640, 1.0, 70, 200, True),   # odd block count, protected sink/window
+])
+def test_prefill_matches_oracle(hs, port, dtype, L, n_q, s, sink, window, causal):
+    U, gqa = 2, 2
+    kc, vc, q = setup(hs, port, U, L, s, dtype, gqa, n_q, sink, window)
+    scale = np.float32(1.0 / math.sqrt(128))
+    got = hs.prefill_attention(to_torch(q, dtype), kc, vc, causal=causal, scale=float(scale)).cpu().numpy()
+
+    def one(ug):
+        u, g = divmod(ug, gqa)
+        return port.prefill(q[u, g], device_to_oracle(kc, u), device_to_oracle(vc, u), None, None, causal, scale, 64)
+    want = np.stack(parallel(one, range(U * gqa))).reshape(U, gqa, n_q, 128)
+    mx, mr = err_stats(got, want)
+    assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
+
+
+@pytest.mark.parametrize("s", [1.0, 0.5])
+def test_prefill_sampled_rows_8k(hs, port, s):
+    """8K causal prefill; 96 sampled query rows per head (block boundaries,
+    first/last rows, random) through the oracle's attend_range."""
+    U, gqa, L = 1, 2, 8192
+    kc, vc, q = setup(hs, port, U, L, s, "f16", gqa, L, seed=5)
+    scale = np.float32(1.0 / math.sqrt(128))
+    got = hs.prefill_attention(to_torch(q, "f16"), kc, vc, causal=True, scale=float(scale)).cpu().numpy()
+    rng = np.random.default_rng(0)
+    rows = sorted(set([0, 1, 63, 64, 127, 128, 4095, 4096, L - 1] + list(rng.integers(0, L, 87))))
+    k0, v0 = device_to_oracle(kc, 0), device_to_oracle(vc, 0)
+
+    def one(g):
+        qr = q[0, g][rows]
+        out_t, m, l = port.attend_rows(qr, k0, v0, None, None, 0, k0.logical_blocks, True, scale,
+                                       np.array(rows, np.int64))
+        return (out_t / l[None, :]).T
+    want = np.stack(parallel(one, range(gqa)))
+    mx, mr = err_stats(got[0][:, rows], want)
+    assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
+
+
+def test_prefill_rejects_invalid(hs, port):
+    from paper_2604_16864_b200 import ConfigError
+    kc, vc, q = setup(hs, port, 1, 256, 1.0, "f16", 1, 256)
+    with pytest.raises(ConfigError):
+        hs.prefill_attention(to_torch(q, "f16"), vc, kc)  # swapped caches
+    big = np.zeros((1, 1, 512, 128), np.float32)
+    with pytest.raises(ConfigError):
+        hs.prefill_attention(to_torch(big, "f16"), kc, vc, causal=True)  # n_q > n_kv

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(128) probe(Args a) {
     uint8_t* sB = base + 32768;    // 32 KB
     uint8_t* sE = base + 65536;    // 2 KB
     const int K = a.K;
-    const bool sparse = a.test == 2 || a.test == 3 || a.test == 5;
+    const bool sparse = a.test == 2 || a.test == 3 || a.test == 5 || a.test == 6;
     // ---- fill A
     if (!sparse) {
         for (int i = tid; i < 128 * K; i += 128) {  // K == 64
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(128) probe(Args a) {
         const int kp = K / 2;  // physical columns
         for (int i = tid; i < 128 * kp; i += 128) {
             const int r = i / kp, k = i % kp;
-            const uint32_t o = (a.test == 5) ? off_k64(r, k) : off_k128(r, k);
+            const uint32_t o = (a.test >= 5) ? off_k64(r, k) : off_k128(r, k);
             *reinterpret_cast<uint16_t*>(sA + o) = a.A[i];
         }
     }
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(128) probe(Args a) {
     tc_fence_after();
     const uint32_t tD = tbase, tE = tbase + 128;
     // ---- T3/T5: metadata via tcgen05.st, lane L = m0 + 8*k1 + 16*m2, column j = k-step
-    if (a.test == 3 || a.test == 5) {
+    if (a.test == 3 || a.test >= 5) {
         const int L = tid, m0 = L & 7, k1 = (L >> 3) & 1, m2 = L >> 4;
         const int rlo = m0 + 16 * m2, rhi = rlo + 8, words = K / 16;
         uint32_t v[4] = {0, 0, 0, 0};
@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(128) probe(Args a) {
     __syncthreads();
     tc_fence_after();
     if (tid == 0) {
-        const uint32_t idesc = umma_idesc_f16(true, 128, 128, false, a.test == 4, sparse);
+        uint32_t idesc = umma_idesc_f16(true, 128, 128, false, a.test == 4, sparse);
+        if (a.test == 6) idesc &= ~(7u << 10);  // B format = F16
         if (a.test == 2) tmem_cp_128x128b(tE, umma_desc(smem_u32(sE), 16, 128, kLayoutNone));
         if (!sparse) {
             for (int j = 0; j < K / 16; ++j) {
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(128) probe(Args a) {
             }
         } else {
             for (int j = 0; j < K / 32; ++j) {
-                const uint64_t ad = (a.test == 5) ? umma_desc(smem_u32(sA) + 32 * j, 16, 512, kLayoutSW64)
+                const uint64_t ad = (a.test >= 5) ? umma_desc(smem_u32(sA) + 32 * j, 16, 512, kLayoutSW64)
                                                   : umma_desc(smem_u32(sA) + 32 * j, 16, 1024, kLayoutSW128);
                 const uint64_t bd = umma_desc(smem_u32(sB) + (j / 2) * 16384 + (j % 2) * 64, 16, 1024, kLayoutSW128);
                 umma_sp_f16(tD, ad, bd, tE + j, idesc, j > 0);
@@ -142,19 +143,20 @@ int main(int argc, char** argv) {
     srand(7);
     const int only = argc > 1 ? atoi(argv[1]) : 0;
     const char* names[] = {"", "T1 dense K-major SW128", "T2 sparse SW128 meta tcgen05.cp", "T3 sparse SW128 meta tcgen05.st",
-                           "T4 dense B MN-major SW128", "T5 sparse A SW64 meta tcgen05.st"};
+                           "T4 dense B MN-major SW128", "T5 sparse A SW64 meta tcgen05.st", "T6 mixed A bf16 x B f16"};
     float* dD; uint16_t *dA, *dB, *dM;
     cudaMalloc(&dD, 128 * 128 * 4); cudaMalloc(&dA, 128 * 128 * 2); cudaMalloc(&dB, 128 * 128 * 2); cudaMalloc(&dM, 128 * 16 * 2);
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
-    for (int test = 1; test <= 5; ++test) {
+    for (int test = 1; test <= 6; ++test) {
         if (only && test != only) { for (int i = 0; i < 3; ++i) rand(); continue; }
-        const bool sparse = test == 2 || test == 3 || test == 5;
-        const int K = (test == 1 || test == 4 || test == 5) ? 64 : 128;
+        const bool sparse = test == 2 || test == 3 || test >= 5;
+        const int K = (test == 1 || test >= 4) ? 64 : 128;
         std::vector<float> A(128 * K), B(128 * K);
         std::vector<uint16_t> Ab, Bb(128 * K), meta(128 * K / 16, 0);
         for (int i = 0; i < 128 * K; ++i) B[i] = fb(bf((rand() % 2001 - 1000) / 500.0f));
         for (auto& x : B) {}
         for (int i = 0; i < 128 * K; ++i) Bb[i] = bf(B[i]);
+        if (test == 6) for (int i = 0; i < 128 * K; ++i) { float x = (rand() % 2001 - 1000) / 512.0f; B[i] = x; __half h = __float2half_rn(x); B[i] = __half2float(h); memcpy(&Bb[i], &h, 2); }
         if (!sparse) {
             for (int i = 0; i < 128 * K; ++i) { A[i] = fb(bf((rand() % 2001 - 1000) / 500.0f)); Ab.push_back(bf(A[i])); }
         } else {
