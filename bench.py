@@ -250,8 +250,8 @@ def run_ours(args):
     e2e_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in zip(e_s, e_t)), world)
     e2e_value = total_bytes / (e2e_ms * 1e-3) / 1e9
 
-    # ---- prefill (configs[2]) once the tcgen05 kernel is available
-    prefill = None
+    # ---- prefill (configs[2]): 32 q / 8 kv heads, 64K causal, S in {0,.25,.5,.75}
+    prefill = None if args.no_prefill else run_prefill(hs, dev, rank, args)
 
     # ---- CPU baseline: the reference's decode on this host's cores (rank 0, N=1)
     cpu = None
@@ -314,6 +314,45 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def run_prefill(hs, dev, rank, args):
+    """configs[2]: Llama-3.1-8B prefill attention at 64K context, causal,
+    hierarchical mixed dense/2:4 blocks at block sparsity S_K = S_V in
+    {0, .25, .5, .75}; fp16 (P in fp16 meets the 1e-3 bar).
+    TFLOPS counts flop_and_byte_count flops (sparse blocks at half)."""
+    import torch
+    _, dense_peak, peak_kind = peaks()
+    Lp, Up, G = args.prefill_ctx, 8, 4
+    g = torch.Generator(device=dev).manual_seed(99 + rank)
+    q = torch.randn((Up, G, Lp, D), generator=g, device=dev, dtype=torch.float32).half()
+    out = torch.empty((Up, G, Lp, D), dtype=torch.float32, device=dev)
+    res = {}
+    for s in (0.0, 0.25, 0.5, 0.75):
+        key = torch.randn((Up, Lp, D), generator=g, device=dev, dtype=torch.float32).half()
+        val = torch.randn((Up, Lp, D), generator=g, device=dev, dtype=torch.float32).half()
+        kc, vc = hs.prune_cache(key, val, hs.SparsityConfig(s, s, 64))
+        del key, val
+        flops = sum(hs.flop_and_byte_count(Lp, kc, vc, 0, True, unit=u)[0] for u in range(Up)) * G
+        hs.prefill_attention(q, kc, vc, causal=True, out=out)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(args.prefill_steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            hs.prefill_attention(q, kc, vc, causal=True, out=out)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = statistics.median(times)
+        tflops = flops / (ms * 1e-3) / 1e12
+        res[str(s)] = {"ms": round(ms, 3), "counted_tflops": round(tflops, 1),
+                       "frac": round(tflops / dense_peak, 4), "counted_flops": flops}
+        del kc, vc
+    return {"workload": f"configs[2]: Llama-3.1-8B prefill, 32 q / 8 kv heads, d=128, {Lp} ctx, causal, fp16",
+            "metric": "counted TFLOPS (flop_and_byte_count; sparse blocks at half) / dense bf16 peak",
+            "peak": dense_peak, "peak_kind": peak_kind, "by_block_sparsity": res,
+            "kernel": "hs::prefill_kernel (tcgen05.mma.sp, TMEM accumulators)"}
 
 
 # ---------------------------------------------------------- reference arm ---
@@ -381,6 +420,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-cpu", action="store_true", help="skip the CPU-baseline leg")
     ap.add_argument("--profile", action="store_true", help="profiling run: no CPU leg, no clock soak")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the configs[2] prefill leg")
+    ap.add_argument("--prefill-ctx", type=int, default=65536)
+    ap.add_argument("--prefill-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -540,6 +540,12 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     L.k_meta = k->meta_pool;
     L.v_meta = v->meta_pool;
     L.out = out;
+    static long long* trace = nullptr;
+    if (getenv("HS_PREFILL_TRACE")) {
+        if (!trace) cudaMalloc(&trace, 4096 * 8 * sizeof(long long));
+        cudaMemsetAsync(trace, 0, 4096 * 8 * sizeof(long long), s);
+        L.trace = trace;
+    }
     static int* dbg = nullptr;
     if (getenv("HS_DEBUG_WAIT")) {
         if (!dbg) cudaMalloc(&dbg, 64);
@@ -556,6 +562,15 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     cudaError_t e = hs::launch_prefill(L, s);
     count_launch();
     if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
+    if (L.trace) {
+        static std::vector<long long> host(4096 * 8);
+        cudaStreamSynchronize(s);
+        cudaMemcpy(host.data(), L.trace, host.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+        if (FILE* f = fopen(getenv("HS_PREFILL_TRACE"), "wb")) {
+            fwrite(host.data(), sizeof(long long), host.size(), f);
+            fclose(f);
+        }
+    }
     if (L.dbg) {
         int h[4] = {0, 0, 0, 0};
         cudaStreamSynchronize(s);

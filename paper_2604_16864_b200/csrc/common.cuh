@@ -81,6 +81,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Wait with a hardware suspend hint: the thread sleeps in try_wait until the
+// phase completes (or the hint expires) instead of spinning on issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+        "@!p bra WAITS_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // Bounded wait for debugging pipelines: after `limit` failed probes records
 // (tag, parity, block, warp) into dbg[0..3] and traps, so a protocol bug shows
 // up as an error with a location instead of a hang.
@@ -97,7 +109,7 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int* dbg, int tag) {
     if (dbg == nullptr) {
-        mbar_wait(bar, parity);
+        mbar_wait_sleep(bar, parity);
         return;
     }
     for (long long i = 0; !mbar_try(bar, parity); ++i) {

@@ -96,6 +96,7 @@ struct PrefillLaunch {
     const void* v_tail;
     float* out;
     int* dbg;                // optional pipeline watchdog record (debug)
+    long long* trace;        // optional per-tile event clocks of CTA (0,0,0) (tools)
     CUtensorMap tm_q, tm_knnz, tm_kden, tm_vnnz, tm_vden;
 };
 cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s);

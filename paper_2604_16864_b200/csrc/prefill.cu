@@ -13,14 +13,16 @@
 // sparse pairs, then dense pairs, then single/mixed and diagonal blocks (order
 // only changes float rounding; attention is order invariant over visible keys).
 //
-// Warp roles (224 threads):
-//   0-3  softmax: TMEM lane r = key row r; exact per-tile column max (redux.f32
-//        + smem), running max updated only when it grows by > 2^8 (FA4-style
-//        lazy rescale), P^T written to smem (MN-major SW128) for GEMM2, O^T / l
-//        rescaled only on the rare max update; epilogue normalises O.
-//   4    TMA producer: Q once; per key tile K/V pools + canonical metadata.
-//   5    MMA issuer: tcgen05.cp metadata -> TMEM, GEMM1 (t), GEMM2 (t-1).
-//   6    metadata: permutes canonical 2-bit codes (nm_metadata.hpp:42-46) into
+// Warp roles (352 threads):
+//   0-7  softmax, two warpgroups: WG g owns query columns 64g..64g+63; warp w
+//        reads TMEM lanes 32(w%4).. (key row r of the tile = d row of O^T).
+//        Exact per-tile column max (redux.f32 + smem), running max updated only
+//        when it grows by > 2^8 (FA4-style lazy rescale), P^T written to smem
+//        (MN-major SW128, N-atom g) for GEMM2, O^T / l rescaled only on the rare
+//        max update; epilogue normalises O.
+//   8    TMA producer: Q once; per key tile K/V pools + canonical metadata.
+//   9    MMA issuer: tcgen05.cp metadata -> TMEM, GEMM1 (t), GEMM2 (t-1).
+//   10   metadata: permutes canonical 2-bit codes (nm_metadata.hpp:42-46) into
 //        the tcgen05 TMEM metadata atom (pinned by tools/probes/umma_probe.cu).
 #include <type_traits>
 
@@ -30,7 +32,7 @@
 namespace hs {
 namespace {
 
-constexpr int kThreads = 224;
+constexpr int kThreads = 352;  // 2 softmax warpgroups + TMA + MMA + metadata warps
 constexpr int kMaxTiles = 1280;   // key tiles per query tile (<= 32767 blocks / 2 + a few)
 constexpr float kTau = 8.0f;      // lazy-rescale threshold (log2 units): P <= 2^8
 
@@ -63,6 +65,12 @@ __device__ __forceinline__ uint32_t pt_chunk_off(int r, int q8 /*query/8 in 0..1
     return h * 16384 + (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
 }
 
+// Per-tile event timestamps of CTA (0,0,0) for pipeline analysis (tools only).
+__device__ __forceinline__ void trace(const PrefillLaunch& L, int t, int ev) {
+    if (L.trace != nullptr && t < 4096 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        L.trace[t * 8 + ev] = clock64();
+}
+
 template <typename T, bool HILO>
 __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_constant__ PrefillLaunch L,
                                                                PrefillLayout lay) {
@@ -70,7 +78,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     __shared__ __align__(8) uint64_t bar_q, bar_full[4], bar_meta[4], bar_empty[4];
     __shared__ __align__(8) uint64_t bar_sfull[2], bar_sempty[2], bar_pfull, bar_pempty;
     __shared__ uint32_t s_tmem;
-    __shared__ int s_ntiles, s_rescale[2];
+    __shared__ int s_ntiles, s_rescale[2][2];
     __shared__ float s_red[4][128];
     __shared__ float s_mnew[128], s_alpha[128];
     __shared__ TileInfo s_tiles[kMaxTiles];
@@ -90,7 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     const uint32_t sQ = base + lay.off_q, sP = base + lay.off_p, sStage = base + lay.off_stage;
 
     // ------------------------------------------------------------ setup ----
-    if (warp == 5) tmem_alloc(&s_tmem, 512);
+    if (warp == 9) tmem_alloc(&s_tmem, 512);
     if (tid == 0) {
         mbar_init(&bar_q, 1);
         for (uint32_t s = 0; s < lay.stages; ++s) {
@@ -100,13 +108,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bar_sfull[i], 1);
-            mbar_init(&bar_sempty[i], 4);
+            mbar_init(&bar_sempty[i], 8);
         }
-        mbar_init(&bar_pfull, 4);
+        mbar_init(&bar_pfull, 8);
         mbar_init(&bar_pempty, 1);
         fence_barrier_init();
     }
-    if (warp == 4 && lane == 0) {
+    if (warp == 8 && lane == 0) {
         // Key-tile list (see header).  Block b is fully visible iff its last key
         // <= the tile's first query position; visible iff its first key <= the last.
         const int16_t* kidx = L.k_index + static_cast<int64_t>(u) * L.nb;
@@ -166,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     const uint32_t oK = 0, oV = lay.k_bytes, oKm = lay.k_bytes + 2 * lay.vblk_bytes, oVm = oKm + 2048,
                    oEK = oVm + 2048, oEV = oEK + 2048;
 
-    if (warp == 4) {
+    if (warp == 8) {
         // ------------------------------------------------------- TMA producer
         if (lane == 0) {
             prefetch_tmap(&L.tm_q);
@@ -213,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             }
         }
         __syncwarp();
-    } else if (warp == 6) {
+    } else if (warp == 10) {
         // ------------------------------------------------ metadata permuter
         // E atom u16 index for (row m, word w): 8(m&7) + ((m>>3)&1) + 128(m>>4)
         // + 64(w&1) + 2(w>>1) (+4 for the second V block); rows m and m+8 are
@@ -266,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_meta[s]);
         }
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         // ------------------------------------------------------- MMA issuer
         if (lane == 0) {
             const bool bf = std::is_same<T, __nv_bfloat16>::value;
@@ -284,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 const TileInfo ti = s_tiles[tp];
                 mbar_wait_dbg(&bar_pfull, tp & 1, L.dbg, 7);
                 tc_fence_after();
+                trace(L, tp, 5);
                 const int nb_t = ti.b1 >= 0 ? 2 : 1;
                 for (int pass = 0; pass < (HILO ? 2 : 1); ++pass) {
                     const uint32_t pbase = sP + pass * 32768;
@@ -307,6 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                         }
                     }
                 }
+                trace(L, tp, 6);
                 umma_commit(&bar_pempty);   // P^T buffer and O^T (for the softmax rescale)
                 umma_commit(&bar_empty[s]); // K/V stage can be refilled
             };
@@ -321,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 mbar_wait_dbg(&bar_meta[s], (t / lay.stages) & 1, L.dbg, 3);
                 if (t >= 2) mbar_wait_dbg(&bar_sempty[sb], ((t >> 1) - 1) & 1, L.dbg, 6);
                 tc_fence_after();
+                trace(L, t, 4);
                 // metadata -> TMEM (ordered before the MMAs that read it)
                 if (!ti.kd) tmem_cp_128x128b(tEK + 4 * sb, umma_desc(st + oEK, 16, 128, kLayoutNone));
                 if (!ti.vd0 || (ti.b1 >= 0 && !ti.vd1))
@@ -345,69 +356,82 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         }
         __syncwarp();
     } else {
-        // ------------------------------------------------------- softmax WG
-        const int r = tid;  // TMEM lane = key row of the tile = d row of O^T
-        const uint32_t lane_off = static_cast<uint32_t>(32 * warp) << 16;
-        float l_part[128];
+        // ------------------------------------------------------- softmax WGs
+        const int wg = warp >> 2, wq = warp & 3;
+        const int r = 32 * wq + lane;  // TMEM lane = key row of the tile = d row of O^T
+        const int cbase = 64 * wg;     // this warpgroup's query columns
+        const int bar_id = 1 + wg;
+        const uint32_t lane_off = static_cast<uint32_t>(32 * wq) << 16;
+        float l_part[64];
 #pragma unroll
-        for (int c = 0; c < 128; ++c) l_part[c] = 0.f;
-        float m_col = -INFINITY;  // running max of column r (this thread owns it)
+        for (int c = 0; c < 64; ++c) l_part[c] = 0.f;
+        float m_col = -INFINITY;  // running max of column cbase + r (threads r < 64)
+        uint8_t* pbuf = base_ptr + lay.off_p;
         for (int t = 0; t < ntiles; ++t) {
             const int sb = t & 1;
             const TileInfo ti = s_tiles[t];
             mbar_wait_dbg(&bar_sfull[sb], (t >> 1) & 1, L.dbg, 5);
             tc_fence_after();
+            if (tid == 0) trace(L, t, 0);
             // masks: invalid rows of single-block tiles; causal (attention.hpp:181-190)
             const bool row_valid = r < 64 || ti.b1 >= 0;
             const int key_pos = (r < 64 ? ti.b0 : ti.b1) * kBlock + (r & 63);
             // column c (query q0 + c at position off + q0 + c) sees this key iff c >= c_first
             const int c_first = row_valid ? (ti.diag ? key_pos - off - q0 : 0) : 1 << 30;
-            // pass 1: exact column max of the raw scores (scale > 0 commutes with max)
+            // warp-uniform fast path: every (row, column) of this warp visible
+            const bool fast = __all_sync(0xffffffffu, c_first <= cbase);
+            const uint32_t tS = tS0 + 128 * sb + lane_off + cbase;
+            // pass 1: exact column max of the raw scores (scale > 0 commutes with max);
+            // the redux result is warp-uniform, so every lane stores it (no select)
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
+            for (int ch = 0; ch < 2; ++ch) {
                 uint32_t v[32];
-                tmem_ld32(tS0 + 128 * sb + lane_off + 32 * ch, v);
+                tmem_ld32(tS + 32 * ch, v);
                 tmem_ld_wait();
-                float mine = -INFINITY;
+                float* dst = &s_red[wq][cbase + 32 * ch];
+                if (fast) {
 #pragma unroll
-                for (int k = 0; k < 32; ++k) {
-                    const float x = (32 * ch + k >= c_first) ? __uint_as_float(v[k]) : -INFINITY;
-                    const float wm = redux_max(x);
-                    if (lane == k) mine = wm;
+                    for (int k = 0; k < 32; ++k) dst[k] = redux_max(__uint_as_float(v[k]));
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k)
+                        dst[k] = redux_max(cbase + 32 * ch + k >= c_first ? __uint_as_float(v[k]) : -INFINITY);
                 }
-                s_red[warp][32 * ch + lane] = mine;
             }
-            if (tid == 0) s_rescale[t & 1] = 0;
-            named_bar(1, 128);
-            {
-                float tm = fmaxf(fmaxf(s_red[0][r], s_red[1][r]), fmaxf(s_red[2][r], s_red[3][r]));
+            if (r == 0) s_rescale[wg][t & 1] = 0;
+            named_bar(bar_id, 128);
+            if (r < 64) {
+                const int c = cbase + r;
+                float tm = fmaxf(fmaxf(s_red[0][c], s_red[1][c]), fmaxf(s_red[2][c], s_red[3][c]));
                 tm = tm * L.scale_log2;
                 float mnew = m_col, alpha = 1.f;
                 if (tm > -INFINITY && (m_col == -INFINITY || tm > m_col + kTau)) {
                     mnew = tm;
                     alpha = m_col == -INFINITY ? 1.f : fast_exp2(m_col - mnew);
-                    if (m_col != -INFINITY) s_rescale[t & 1] = 1;
+                    if (m_col != -INFINITY) s_rescale[wg][t & 1] = 1;
                 }
                 m_col = mnew;
-                s_mnew[r] = mnew;
-                s_alpha[r] = alpha;
+                s_mnew[c] = mnew;
+                s_alpha[c] = alpha;
             }
-            named_bar(1, 128);
+            named_bar(bar_id, 128);
+            if (tid == 0) trace(L, t, 1);
             // P^T buffer free + O^T stable (GEMM2(t-1) complete)
             if (t >= 1) mbar_wait_dbg(&bar_pempty, (t - 1) & 1, L.dbg, 8);
             tc_fence_after();
-            if (s_rescale[t & 1]) {
+            if (tid == 0) trace(L, t, 2);
+            if (s_rescale[wg][t & 1]) {
 #pragma unroll
-                for (int cc = 0; cc < 128; ++cc) l_part[cc] *= s_alpha[cc];
+                for (int cc = 0; cc < 64; ++cc) l_part[cc] *= s_alpha[cbase + cc];
                 if (t >= 1) {
 #pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) {
+                    for (int ch = 0; ch < 2; ++ch) {
                         uint32_t v[32];
-                        tmem_ld32(tO + lane_off + 32 * ch, v);
+                        tmem_ld32(tO + lane_off + cbase + 32 * ch, v);
                         tmem_ld_wait();
 #pragma unroll
                         for (int k = 0; k < 32; k += 4) {
-                            const float4 a4 = *reinterpret_cast<const float4*>(&s_alpha[32 * ch + k]);
+                            const float4 a4 = *reinterpret_cast<const float4*>(&s_alpha[cbase + 32 * ch + k]);
                             v[k] = __float_as_uint(__uint_as_float(v[k]) * a4.x);
                             v[k + 1] = __float_as_uint(__uint_as_float(v[k + 1]) * a4.y);
                             v[k + 2] = __float_as_uint(__uint_as_float(v[k + 2]) * a4.z);
@@ -415,31 +439,38 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                         }
 #pragma unroll
                         for (int k = 0; k < 32; k += 4)
-                            tmem_st4(tO + lane_off + 32 * ch + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
+                            tmem_st4(tO + lane_off + cbase + 32 * ch + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
                     }
                     tmem_st_wait();
                 }
             }
             // pass 2: probabilities, row sums, P^T (+ residual for bf16)
-            uint8_t* pbuf = base_ptr + lay.off_p;
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
+            for (int ch = 0; ch < 2; ++ch) {
                 uint32_t v[32];
-                tmem_ld32(tS0 + 128 * sb + lane_off + 32 * ch, v);
+                tmem_ld32(tS + 32 * ch, v);
                 tmem_ld_wait();
 #pragma unroll
-                for (int q8 = 4 * ch; q8 < 4 * ch + 4; ++q8) {
+                for (int g8 = 0; g8 < 4; ++g8) {
+                    const int q8 = (cbase >> 3) + 4 * ch + g8;  // 8-query chunk index in 0..15
                     const float4 ma = *reinterpret_cast<const float4*>(&s_mnew[8 * q8]);
                     const float4 mb = *reinterpret_cast<const float4*>(&s_mnew[8 * q8 + 4]);
                     const float mm[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
                     float p[8];
+                    if (fast) {
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const int cc = 8 * q8 + k;
-                        const float x = fmaf(__uint_as_float(v[cc - 32 * ch]), L.scale_log2, -mm[k]);
-                        p[k] = (cc >= c_first && mm[k] != -INFINITY) ? fast_exp2(x) : 0.f;
-                        l_part[cc] += p[k];
+                        for (int k = 0; k < 8; ++k)
+                            p[k] = fast_exp2(fmaf(__uint_as_float(v[8 * g8 + k]), L.scale_log2, -mm[k]));
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const float x = fmaf(__uint_as_float(v[8 * g8 + k]), L.scale_log2, -mm[k]);
+                            const int cc = 8 * q8 + k;
+                            p[k] = (cc >= c_first && mm[k] != -INFINITY) ? fast_exp2(x) : 0.f;
+                        }
                     }
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) l_part[32 * ch + 8 * g8 + k] += p[k];
                     const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
                                                 F16Traits<T>::pack(p[4], p[5]), F16Traits<T>::pack(p[6], p[7]));
                     *reinterpret_cast<uint4*>(pbuf + pt_chunk_off(r, q8)) = hi;
@@ -457,11 +488,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     }
                 }
             }
+            if (tid == 0) trace(L, t, 3);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_sempty[sb]);  // S^T[sb] fully read
+            if (lane == 0) mbar_arrive(&bar_sempty[sb]);  // this warp is done with S^T[sb]
             fence_async_smem();
-            tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_pfull);
         }
@@ -469,31 +500,33 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         if (ntiles > 0) mbar_wait_dbg(&bar_pempty, (ntiles - 1) & 1, L.dbg, 8);
         tc_fence_after();
         // l[c] = sum over the 128 key lanes of l_part[c]: transpose through smem
-        float* s_l = reinterpret_cast<float*>(base_ptr + lay.off_stage);  // 128 x 129 floats
-        named_bar(1, 128);
+        float* s_l = reinterpret_cast<float*>(base_ptr + lay.off_stage) + wg * (128 * 65);
+        named_bar(bar_id, 128);
 #pragma unroll
-        for (int c = 0; c < 128; ++c) s_l[r * 129 + c] = l_part[c];
-        named_bar(1, 128);
-        float lsum = 0.f;
-        for (int k = 0; k < 128; ++k) lsum += s_l[k * 129 + r];
-        s_alpha[r] = lsum > 0.f ? 1.f / lsum : 0.f;
-        named_bar(1, 128);
+        for (int c = 0; c < 64; ++c) s_l[r * 65 + c] = l_part[c];
+        named_bar(bar_id, 128);
+        if (r < 64) {
+            float lsum = 0.f;
+            for (int k = 0; k < 128; ++k) lsum += s_l[k * 65 + r];
+            s_alpha[cbase + r] = lsum > 0.f ? 1.f / lsum : 0.f;
+        }
+        named_bar(bar_id, 128);
         float* out = L.out + (static_cast<int64_t>(u * L.gqa + h) * L.n_q + q0) * kHeadDim;
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
+        for (int ch = 0; ch < 2; ++ch) {
             uint32_t v[32];
-            tmem_ld32(tO + lane_off + 32 * ch, v);
+            tmem_ld32(tO + lane_off + cbase + 32 * ch, v);
             tmem_ld_wait();
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
-                const int c = 32 * ch + k;
+                const int c = cbase + 32 * ch + k;
                 if (c < rows_q) out[c * kHeadDim + r] = __uint_as_float(v[k]) * s_alpha[c];
             }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) tmem_dealloc(tmem, 512);
+    if (warp == 9) tmem_dealloc(tmem, 512);
 }
 
 }  // namespace
@@ -514,7 +547,7 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     if (stages < 1) return cudaErrorInvalidConfiguration;
     lay.stages = stages;
     size_t smem = lay.off_stage + static_cast<size_t>(stages) * lay.stage_bytes + 1024;
-    const size_t epi = lay.off_stage + 128 * 129 * 4 + 1024;
+    const size_t epi = lay.off_stage + 2 * 128 * 65 * 4 + 1024;
     if (smem < epi) smem = epi;
     const dim3 grid((L.n_q + 127) / 128, L.gqa, L.n_units);
     if (L.bf16) {

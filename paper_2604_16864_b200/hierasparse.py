@@ -301,33 +301,50 @@ def prefill_attention(q: torch.Tensor, k: DeviceCompressedCache, v: DeviceCompre
     return out
 
 
+def flop_count(k_dense, v_dense, block: int, d: int, n_q: int, tail: int = 0, causal: bool = False) -> int:
+    """Counted GEMM flops of flop_and_byte_count (attention.hpp:426-456) in closed
+    form: per (query row, visible key) 2*d per GEMM on a dense block, d on a
+    sparse one, 4*d on the dense tail; causal at row granularity."""
+    import numpy as np
+    kd = np.asarray(k_dense, dtype=np.int64)
+    vd = np.asarray(v_dense, dtype=np.int64)
+    nb = kd.shape[0]
+    w = (1 + kd) + (1 + vd)                       # per-key flop weight / d
+    prefix = nb * block
+    n_kv = prefix + tail
+    if not causal:
+        return int(n_q * (int(w.sum()) * block * d + 4 * tail * d))
+    off = n_kv - n_q                              # query i sits at position off + i
+    lo, hi = off, off + n_q - 1                   # query positions
+    b = np.arange(nb, dtype=np.int64)
+    start = b * block
+    # keys seen in block b by a query at position p: clamp(p - start + 1, 0, block)
+    full_from = start + block - 1                 # p >= full_from -> whole block
+    n_full = np.clip(hi - np.maximum(full_from, lo) + 1, 0, None)
+    a = np.maximum(start, lo)                     # partial range p in [a, e]
+    e = np.minimum(full_from - 1, hi)
+    cnt = np.clip(e - a + 1, 0, None)
+    first = a - start + 1
+    partial = np.where(cnt > 0, cnt * first + cnt * (cnt - 1) // 2, 0)
+    keys = n_full * block + partial
+    flops = int((keys * w).sum()) * d
+    if tail:
+        # tail keys seen by query p: clamp(p - prefix + 1, 0, tail)
+        p = np.arange(lo, hi + 1, dtype=np.int64)
+        flops += int(np.clip(p - prefix + 1, 0, tail).sum()) * 4 * d
+    return flops
+
+
 def flop_and_byte_count(n_q: int, k: DeviceCompressedCache, v: DeviceCompressedCache, tail: int = 0,
                         causal: bool = False, unit: int = 0) -> tuple[int, int]:
     """flop_and_byte_count (attention.hpp:426-467) for one unit, from the index maps."""
-    d, B = k.head_dim, k.block_size
-    kd = (k.index_map[unit] > 0).cpu().tolist() if k.sparse_count and k.dense_count else \
-        [k.sparse_count == 0] * k.logical_blocks
-    vd = (v.index_map[unit] > 0).cpu().tolist() if v.sparse_count and v.dense_count else \
-        [v.sparse_count == 0] * v.logical_blocks
-    nb = k.logical_blocks
-    prefix = nb * B
-    n_kv = prefix + tail
-    # per-block flop weight: width * d * (2 dense | 1 sparse) for each GEMM
-    w = [(2 if kd[b] else 1) + (2 if vd[b] else 1) for b in range(nb)]
-    flops = 0
-    if not causal:
-        flops = n_q * (sum(w) * B * d + (4 * tail * d if tail else 0))
-    else:
-        for i in range(n_q):
-            vis = n_kv - n_q + i + 1
-            full = min(nb, vis // B)
-            flops += sum(w[:full]) * B * d
-            if full < nb and full * B < vis:
-                flops += w[full] * (vis - full * B) * d
-            if vis > prefix:
-                flops += 4 * (vis - prefix) * d
+    def kinds(c):
+        if c.sparse_count and c.dense_count:
+            return (c.index_map[unit] > 0).cpu().numpy()
+        return [1 if c.sparse_count == 0 else 0] * c.logical_blocks
+    flops = flop_count(kinds(k), kinds(v), k.block_size, k.head_dim, n_q, tail, causal)
     nbytes = 0
     for c in (k, v):
         nbytes += HEADER_BYTES + sum(c.measure_size().values())
-    nbytes += 2 * tail * d * 2
+    nbytes += 2 * tail * k.head_dim * 2
     return flops, nbytes

@@ -94,3 +94,28 @@ def test_attention_argument_validation_without_gpu(lib):
     rc = lib.hs_decode(1, C.byref(bad), C.byref(v), None, None, 0, 4, 0.1, 0, 1, None)
     with pytest.raises(ConfigError, match="head_dim"):
         capi.check(rc)
+
+
+def test_closed_form_flop_count_matches_oracle(port):
+    """hierasparse.flop_count == flop_and_byte_count (attention.hpp:426-467) on
+    random masks, causal and not, with and without a dense tail."""
+    import numpy as np
+    from oracle.oracle import SparsityConfig
+    from paper_2604_16864_b200.hierasparse import flop_count
+    rng = np.random.default_rng(4)
+    for it in range(60):
+        B, d = 16, 32
+        nb = 1 + int(rng.integers(0, 12))
+        tail = int(rng.integers(0, B)) if it % 3 == 0 else 0
+        x = np.zeros((nb * B, d), np.float32)
+        kf = rng.integers(0, 2, nb).astype(np.uint8)
+        vf = rng.integers(0, 2, nb).astype(np.uint8)
+        kc = port.compress_with_flags(x, SparsityConfig(block_size=B), 0, kf)
+        vc = port.compress_with_flags(x, SparsityConfig(block_size=B), 1, vf)
+        n_kv = nb * B + tail
+        causal = bool(it % 2)
+        n_q = 1 + int(rng.integers(0, n_kv)) if causal else 1 + int(rng.integers(0, 40))
+        want = port.flop_and_byte_count(n_q, d, kc, vc, tail, causal)[0]
+        kd = kf if (kc.sparse_count and kc.dense_count) else [int(kc.sparse_count == 0)] * nb
+        vd = vf if (vc.sparse_count and vc.dense_count) else [int(vc.sparse_count == 0)] * nb
+        assert flop_count(kd, vd, B, d, n_q, tail, causal) == want, it
