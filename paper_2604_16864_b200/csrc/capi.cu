@@ -516,8 +516,9 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     HS_CHECK_CONFIG(!causal || n_kv >= n_q, "prefill_attention: causal queries exceed key sequence");
     HS_CHECK_CONFIG(tail == 0 && k_tail == nullptr,
                     "prefill_attention: the tcgen05 kernel takes block-aligned caches (dense tail not supported)");
-    HS_CHECK_CONFIG(k->logical_blocks / 2 + 8 <= 1280,
-                    "prefill_attention: %u blocks exceed the kernel's key-tile list", k->logical_blocks);
+    HS_CHECK_CONFIG(k->logical_blocks / 2 + 8 <= 4096,
+                    "prefill_attention: %u blocks exceed the kernel's key-tile list (max 8184 blocks)",
+                    k->logical_blocks);
     HS_CHECK_CONFIG(k->slot_block != nullptr, "prefill_attention: key cache needs slot_block");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     hs::PrefillLaunch L{};
@@ -542,8 +543,8 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     L.out = out;
     static long long* trace = nullptr;
     if (getenv("HS_PREFILL_TRACE")) {
-        if (!trace) cudaMalloc(&trace, 4096 * 8 * sizeof(long long));
-        cudaMemsetAsync(trace, 0, 4096 * 8 * sizeof(long long), s);
+        if (!trace) cudaMalloc(&trace, 4096 * 16 * sizeof(long long));
+        cudaMemsetAsync(trace, 0, 4096 * 16 * sizeof(long long), s);
         L.trace = trace;
     }
     static int* dbg = nullptr;
@@ -552,10 +553,14 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
         cudaMemsetAsync(dbg, 0, 64, s);
         L.dbg = dbg;
     }
+    L.mode = 0;
+    if (const char* env = getenv("HS_PREFILL_MODE")) L.mode = atoi(env);
     const uint64_t U = k->n_units;
     bool ok = make_map(&L.tm_q, q, 128, U * gqa * n_q, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-    ok &= make_map(&L.tm_knnz, k->nnz_pool, 64, U * k->sparse_count * 64, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
-    ok &= make_map(&L.tm_kden, k->dense_pool, 128, U * k->dense_count * 64, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+    // K tiles are two consecutive pool slots (128 rows) per TMA; a single-block
+    // tile's second half is masked in the kernel (and zero-filled past the pool).
+    ok &= make_map(&L.tm_knnz, k->nnz_pool, 64, U * k->sparse_count * 64, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_map(&L.tm_kden, k->dense_pool, 128, U * k->dense_count * 64, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     ok &= make_map(&L.tm_vnnz, v->nnz_pool, 32, U * v->sparse_count * 128, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
     ok &= make_map(&L.tm_vden, v->dense_pool, 64, U * v->dense_count * 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     if (!ok) return fail(HS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -563,7 +568,7 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     count_launch();
     if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
     if (L.trace) {
-        static std::vector<long long> host(4096 * 8);
+        static std::vector<long long> host(4096 * 16);
         cudaStreamSynchronize(s);
         cudaMemcpy(host.data(), L.trace, host.size() * sizeof(long long), cudaMemcpyDeviceToHost);
         if (FILE* f = fopen(getenv("HS_PREFILL_TRACE"), "wb")) {

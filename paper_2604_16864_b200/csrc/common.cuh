@@ -109,7 +109,7 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int* dbg, int tag) {
     if (dbg == nullptr) {
-        mbar_wait_sleep(bar, parity);
+        mbar_wait(bar, parity);
         return;
     }
     for (long long i = 0; !mbar_try(bar, parity); ++i) {
@@ -289,6 +289,20 @@ __device__ __forceinline__ void umma_sp_f16(uint32_t d_tmem, uint64_t a, uint64_
         "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%3], %4, p;\n\t}" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(e_tmem), "r"(idesc), "r"(acc));
 }
+// One elected lane of a converged warp (tcgen05.mma / commit are single-thread
+// instructions; issuing them from a warp-uniform loop lets the descriptors live
+// in uniform registers instead of a per-issue R2UR waterfall).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+        "elect.sync rx|px, %1;\n\t@px mov.s32 %0, 1;\n\t}"
+        : "+r"(pred)
+        : "r"(0xffffffffu));
+    return pred != 0;
+}
+__device__ __forceinline__ int warp_id_uniform() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      smem_u32(bar))

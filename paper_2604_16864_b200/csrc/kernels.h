@@ -96,6 +96,7 @@ struct PrefillLaunch {
     const void* v_tail;
     float* out;
     int* dbg;                // optional pipeline watchdog record (debug)
+    int mode;                // tools only: 1 = softmax skipped, 2 = MMAs skipped, 3 = both
     long long* trace;        // optional per-tile event clocks of CTA (0,0,0) (tools)
     CUtensorMap tm_q, tm_knnz, tm_kden, tm_vnnz, tm_vden;
 };

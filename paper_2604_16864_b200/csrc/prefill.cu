@@ -24,6 +24,8 @@
 //   9    MMA issuer: tcgen05.cp metadata -> TMEM, GEMM1 (t), GEMM2 (t-1).
 //   10   metadata: permutes canonical 2-bit codes (nm_metadata.hpp:42-46) into
 //        the tcgen05 TMEM metadata atom (pinned by tools/probes/umma_probe.cu).
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -33,23 +35,50 @@ namespace hs {
 namespace {
 
 constexpr int kThreads = 352;  // 2 softmax warpgroups + TMA + MMA + metadata warps
-constexpr int kMaxTiles = 1280;   // key tiles per query tile (<= 32767 blocks / 2 + a few)
+
 constexpr float kTau = 8.0f;      // lazy-rescale threshold (log2 units): P <= 2^8
 
+// One key tile = one or two 64-token blocks of the same K kind.  8 bytes:
+//   ke0   K index-map entry of the first block (sign = kind, |ke0|-1 = pool slot);
+//         the second block of a pair is always the next slot of the same pool
+//   ve0/1 V index-map entries of the two blocks (ve1 == 0: single-block tile,
+//         TMEM rows 64..127 invalid)
+//   dblk  first block of a diagonal tile (pair = dblk, dblk+1) needing element
+//         causal masks, -1 otherwise
 struct TileInfo {
-    int16_t b0, b1;   // logical blocks (b1 = -1: single block, rows 64..127 invalid)
-    uint8_t kd;       // K kind of the tile: 1 dense, 0 sparse
-    uint8_t vd0, vd1; // V kinds of b0 / b1
-    uint8_t diag;     // needs element-level causal masking
+    int16_t ke0, ve0, ve1, dblk;
 };
 
+// Shared-memory plan (bytes from the 1024-aligned base):
+//   Q [128 q][128 d] (SW128, two 64-column atoms)            off_q
+//   P^T buffers (n_pbuf x p_bytes; bf16 adds a residual half)  off_p
+//   K ring (nk x k_stage): nnz or dense 128-key tile; sparse stages carry the
+//          canonical metadata (+k_meta) and its TMEM-atom permutation (+k_e)
+//   V ring (nv x v_stage): two 64-key V^T blocks of vblk bytes; metadata + E
+//   tile list (TileInfo x tile_cap)
+// K and V are separate rings: a K stage is recycled as soon as GEMM1 of its
+// tile completes, a V stage after GEMM2, so neither waits for the other.
 struct PrefillLayout {
-    uint32_t k_bytes, vblk_bytes, stage_bytes, stages;
-    uint32_t off_q, off_p, off_stage;
+    uint32_t off_q, off_p, p_bytes, n_pbuf;
+    uint32_t off_k, k_stage, nk, k_meta, k_e;
+    uint32_t off_v, v_stage, nv, vblk, v_meta, v_e;
+    uint32_t off_tiles, tile_cap;
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Barrier over `n` threads of named barrier `id` that also ORs a predicate.
+__device__ __forceinline__ bool bar_red_or(int id, bool v) {
+    uint32_t r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
+        "barrier.cta.red.or.pred p, %2, 128, q;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(r)
+        : "r"(static_cast<uint32_t>(v)), "r"(id)
+        : "memory");
+    return r != 0;
 }
 
 __device__ __forceinline__ float redux_max(float v) {
@@ -68,20 +97,20 @@ __device__ __forceinline__ uint32_t pt_chunk_off(int r, int q8 /*query/8 in 0..1
 // Per-tile event timestamps of CTA (0,0,0) for pipeline analysis (tools only).
 __device__ __forceinline__ void trace(const PrefillLaunch& L, int t, int ev) {
     if (L.trace != nullptr && t < 4096 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
-        L.trace[t * 8 + ev] = clock64();
+        L.trace[t * 16 + ev] = clock64();
 }
 
 template <typename T, bool HILO>
 __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_constant__ PrefillLaunch L,
                                                                PrefillLayout lay) {
     extern __shared__ uint8_t smem_raw[];
-    __shared__ __align__(8) uint64_t bar_q, bar_full[4], bar_meta[4], bar_empty[4];
-    __shared__ __align__(8) uint64_t bar_sfull[2], bar_sempty[2], bar_pfull, bar_pempty;
+    __shared__ __align__(8) uint64_t bar_q, bar_kfull[4], bar_kmeta[4], bar_kempty[4];
+    __shared__ __align__(8) uint64_t bar_vfull[4], bar_vmeta[4], bar_vempty[4];
+    __shared__ __align__(8) uint64_t bar_sfull[2], bar_sempty[2], bar_pfull[2], bar_pempty[2];
     __shared__ uint32_t s_tmem;
-    __shared__ int s_ntiles, s_rescale[2][2];
+    __shared__ int s_ntiles;
     __shared__ float s_red[4][128];
-    __shared__ float s_mnew[128], s_alpha[128];
-    __shared__ TileInfo s_tiles[kMaxTiles];
+    __shared__ float s_mnew[128], s_alpha[128], s_mrun[128];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     const int n_tiles_q = (L.n_q + 127) / 128;
@@ -95,28 +124,38 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* const base_ptr = smem_raw + (base - raw);
-    const uint32_t sQ = base + lay.off_q, sP = base + lay.off_p, sStage = base + lay.off_stage;
+    const uint32_t sQ = base + lay.off_q, sP = base + lay.off_p;
+    const uint32_t sK = base + lay.off_k, sV = base + lay.off_v;
+    TileInfo* const s_tiles = reinterpret_cast<TileInfo*>(base_ptr + lay.off_tiles);
+    const int nk = static_cast<int>(lay.nk), nv = static_cast<int>(lay.nv);
 
     // ------------------------------------------------------------ setup ----
     if (warp == 9) tmem_alloc(&s_tmem, 512);
     if (tid == 0) {
         mbar_init(&bar_q, 1);
-        for (uint32_t s = 0; s < lay.stages; ++s) {
-            mbar_init(&bar_full[s], 1);
-            mbar_init(&bar_meta[s], 1);
-            mbar_init(&bar_empty[s], 1);
+        for (int s = 0; s < nk; ++s) {
+            mbar_init(&bar_kfull[s], 1);
+            mbar_init(&bar_kmeta[s], 1);
+            mbar_init(&bar_kempty[s], 1);
+        }
+        for (int s = 0; s < nv; ++s) {
+            mbar_init(&bar_vfull[s], 1);
+            mbar_init(&bar_vmeta[s], 1);
+            mbar_init(&bar_vempty[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bar_sfull[i], 1);
             mbar_init(&bar_sempty[i], 8);
+            mbar_init(&bar_pfull[i], 8);
+            mbar_init(&bar_pempty[i], 1);
         }
-        mbar_init(&bar_pfull, 8);
-        mbar_init(&bar_pempty, 1);
         fence_barrier_init();
     }
-    if (warp == 8 && lane == 0) {
+    if (warp == 8) {
         // Key-tile list (see header).  Block b is fully visible iff its last key
         // <= the tile's first query position; visible iff its first key <= the last.
+        // The kind-grouped pairs are index arithmetic over the slot lists, so the
+        // 32 lanes fill them in parallel; lane 0 appends the few odd/diagonal tiles.
         const int16_t* kidx = L.k_index + static_cast<int64_t>(u) * L.nb;
         const int16_t* vidx = L.v_index + static_cast<int64_t>(u) * L.nb;
         const int32_t* sb = L.k_slot_block + static_cast<int64_t>(u) * L.nb;
@@ -133,230 +172,308 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             if (sparse_blocks[mid] < fv_end) lo = mid + 1; else hi = mid;
         }
         const int ns = lo, nd = fv_end - ns;
-        int n = 0;
-        auto push = [&](int b0, int b1, int kd, int diag) {
+        const int cap = static_cast<int>(lay.tile_cap);
+        auto make = [&](int b0, int b1, int diag) {
             TileInfo ti;
-            ti.b0 = static_cast<int16_t>(b0);
-            ti.b1 = static_cast<int16_t>(b1);
-            ti.kd = static_cast<uint8_t>(kd);
-            ti.vd0 = vidx[b0] > 0;
-            ti.vd1 = b1 >= 0 ? (vidx[b1] > 0) : 0;
-            ti.diag = static_cast<uint8_t>(diag);
-            if (n < kMaxTiles) s_tiles[n] = ti;
-            ++n;
+            ti.ke0 = kidx[b0];
+            ti.ve0 = vidx[b0];
+            ti.ve1 = b1 >= 0 ? vidx[b1] : int16_t(0);
+            ti.dblk = static_cast<int16_t>(diag ? b0 : -1);
+            return ti;
         };
-        for (int i = 0; i + 1 < ns; i += 2) push(sparse_blocks[i], sparse_blocks[i + 1], 0, 0);
-        for (int i = 0; i + 1 < nd; i += 2) push(sb[i], sb[i + 1], 1, 0);
-        if (ns & 1) push(sparse_blocks[ns - 1], -1, 0, 0);
-        if (nd & 1) push(sb[nd - 1], -1, 1, 0);
-        for (int b = fv_end; b < vis_end; ++b) {
-            const int kd = kidx[b] > 0;
-            if (b + 1 < vis_end && (kidx[b + 1] > 0) == kd) {
-                push(b, b + 1, kd, 1);
-                ++b;
-            } else {
-                push(b, -1, kd, 1);
-            }
+        const int nsp = ns >> 1, ndp = nd >> 1;
+        for (int i = lane; i < nsp + ndp && i < cap; i += 32) {
+            s_tiles[i] = i < nsp ? make(sparse_blocks[2 * i], sparse_blocks[2 * i + 1], 0)
+                                 : make(sb[2 * (i - nsp)], sb[2 * (i - nsp) + 1], 0);
         }
-        s_ntiles = n;
+        if (lane == 0) {
+            int n = nsp + ndp;
+            auto push = [&](int b0, int b1, int diag) {
+                if (n < cap) s_tiles[n] = make(b0, b1, diag);
+                ++n;
+            };
+            if (ns & 1) push(sparse_blocks[ns - 1], -1, 0);
+            if (nd & 1) push(sb[nd - 1], -1, 0);
+            for (int b = fv_end; b < vis_end; ++b) {
+                const int kd = kidx[b] > 0;
+                if (b + 1 < vis_end && (kidx[b + 1] > 0) == kd) {
+                    push(b, b + 1, 1);
+                    ++b;
+                } else {
+                    push(b, -1, 1);
+                }
+            }
+            s_ntiles = min(n, cap);
+        }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = s_tmem;
-    const int ntiles = min(s_ntiles, kMaxTiles);
+    // P^T buffers: tile t uses buffer t % npb; its barrier phase is (t / npb) & 1.
+    const int npb = static_cast<int>(lay.n_pbuf);
+    auto pbuf_of = [npb](int t) { return npb == 2 ? (t & 1) : 0; };
+    auto pphase = [npb](int t) { return static_cast<uint32_t>((npb == 2 ? (t >> 1) : t) & 1); };
+    const int ntiles = s_ntiles;
     // TMEM columns: S[0] 0..127, S[1] 128..255, O 256..383, E_K[2] 384.., E_V[2] 392..
     const uint32_t tS0 = tmem, tO = tmem + 256, tEK = tmem + 384, tEV = tmem + 392;
 
-    const uint8_t* stage_ptr0 = base_ptr + lay.off_stage;
-    auto stage_base = [&](int s) { return sStage + s * lay.stage_bytes; };
-    // stage sub-layout
-    const uint32_t oK = 0, oV = lay.k_bytes, oKm = lay.k_bytes + 2 * lay.vblk_bytes, oVm = oKm + 2048,
-                   oEK = oVm + 2048, oEV = oEK + 2048;
-
-    if (warp == 8) {
-        // ------------------------------------------------------- TMA producer
-        if (lane == 0) {
+    const int warp_u = warp_id_uniform();
+    // Values read from smem are per-thread registers to the compiler; broadcasting
+    // them from lane 0 makes them provably warp-uniform, so the descriptor / TMA
+    // arithmetic below stays in uniform registers and the single-thread
+    // tcgen05 / TMA instructions issue without R2UR waterfall loops.
+    auto uni = [](int v) { return __shfl_sync(0xffffffffu, v, 0); };
+    // Canonical 2-bit metadata rows -> tcgen05 TMEM metadata atom.  E atom u16
+    // index for (row m, word w): 8(m&7) + ((m>>3)&1) + 128(m>>4) + 64(w&1) +
+    // 2(w>>1) (+4 for the second V block); rows m and m+8 are adjacent u16s, so
+    // each store writes a (row m, row m+8) pair.
+    auto permute_k_meta = [&](const uint8_t* meta, uint8_t* e, bool single) {
+        for (int pidx = lane; pidx < 64; pidx += 32) {  // row pairs (m, m+8)
+            const int m = (pidx & 7) + 16 * (pidx >> 3);
+            uint4 lo4 = make_uint4(0x44444444u, 0x44444444u, 0x44444444u, 0x44444444u);
+            uint4 hi4 = lo4;
+            if (!(single && m >= 64)) {
+                lo4 = *reinterpret_cast<const uint4*>(meta + m * 16);
+                hi4 = *reinterpret_cast<const uint4*>(meta + (m + 8) * 16);
+            }
+            const uint32_t lw[4] = {lo4.x, lo4.y, lo4.z, lo4.w}, hw[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const uint32_t a = (lw[w >> 1] >> (16 * (w & 1))) & 0xFFFF;
+                const uint32_t b = (hw[w >> 1] >> (16 * (w & 1))) & 0xFFFF;
+                const int idx = 8 * (m & 7) + 128 * (m >> 4) + 64 * (w & 1) + 2 * (w >> 1);
+                *reinterpret_cast<uint32_t*>(reinterpret_cast<uint16_t*>(e) + idx) = a | (b << 16);
+            }
+        }
+    };
+    auto permute_v_meta = [&](const uint8_t* meta, uint8_t* e, int i) {
+        for (int pidx = lane; pidx < 64; pidx += 32) {
+            const int m = (pidx & 7) + 16 * (pidx >> 3);
+            const uint2 lo2 = *reinterpret_cast<const uint2*>(meta + 1024 * i + m * 8);
+            const uint2 hi2 = *reinterpret_cast<const uint2*>(meta + 1024 * i + (m + 8) * 8);
+            const uint32_t lw[2] = {lo2.x, lo2.y}, hw[2] = {hi2.x, hi2.y};
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const uint32_t a = (lw[w >> 1] >> (16 * (w & 1))) & 0xFFFF;
+                const uint32_t b = (hw[w >> 1] >> (16 * (w & 1))) & 0xFFFF;
+                const int idx = 8 * (m & 7) + 128 * (m >> 4) + 64 * (w & 1) + 2 * (w >> 1) + 4 * i;
+                *reinterpret_cast<uint32_t*>(reinterpret_cast<uint16_t*>(e) + idx) = a | (b << 16);
+            }
+        }
+    };
+    if (warp_u == 8) {
+        // ------------------------------------------- K producer + K metadata
+        // Issue K(t), then permute the metadata of K(t-1) (one tile behind, so the
+        // TMA of the next tile is in flight while this warp waits for a landing;
+        // with a single stage K(t+1) needs K(t) consumed, so no lag).
+        const int lag = nk >= 2 ? 1 : 0;
+        if (elect_one()) {
             prefetch_tmap(&L.tm_q);
             prefetch_tmap(&L.tm_knnz);
-            prefetch_tmap(&L.tm_vnnz);
+            prefetch_tmap(&L.tm_kden);
             const int qrow = (u * L.gqa + h) * L.n_q + q0;
             mbar_arrive_expect_tx(&bar_q, 32768);
             tma_tile_g2s(base_ptr + lay.off_q, &L.tm_q, 0, qrow, &bar_q);
             tma_tile_g2s(base_ptr + lay.off_q + 16384, &L.tm_q, 64, qrow, &bar_q);
-            for (int t = 0; t < ntiles; ++t) {
-                const int s = t % lay.stages;
-                mbar_wait_dbg(&bar_empty[s], ((t / lay.stages) & 1) ^ 1, L.dbg, 4);
-                const TileInfo ti = s_tiles[t];
-                uint8_t* st = const_cast<uint8_t*>(stage_ptr0) + s * lay.stage_bytes;
-                uint32_t bytes = 0;
-                const int nb_t = ti.b1 >= 0 ? 2 : 1;
-                for (int i = 0; i < nb_t; ++i) bytes += ti.kd ? 16384u : 9216u;
-                for (int i = 0; i < nb_t; ++i) bytes += (i == 0 ? ti.vd0 : ti.vd1) ? 16384u : 9216u;
-                mbar_arrive_expect_tx(&bar_full[s], bytes);
-                for (int i = 0; i < nb_t; ++i) {
-                    const int b = i == 0 ? ti.b0 : ti.b1;
-                    const int ke = L.k_index[static_cast<int64_t>(u) * L.nb + b];
-                    if (ti.kd) {
-                        const int row = (u * L.k_dense_count + ke - 1) * kBlock;
-                        tma_tile_g2s(st + oK + 8192 * i, &L.tm_kden, 0, row, &bar_full[s]);
-                        tma_tile_g2s(st + oK + 16384 + 8192 * i, &L.tm_kden, 64, row, &bar_full[s]);
-                    } else {
-                        const int sbk = u * L.k_sparse_count + (-ke - 1);
-                        tma_tile_g2s(st + oK + 8192 * i, &L.tm_knnz, 0, sbk * kBlock, &bar_full[s]);
-                        tma_bulk_g2s(st + oKm + 1024 * i, L.k_meta + static_cast<int64_t>(sbk) * 512, 1024,
-                                     &bar_full[s]);
-                    }
-                    const int ve = L.v_index[static_cast<int64_t>(u) * L.nb + b];
-                    if (ve > 0) {
-                        const int row = (u * L.v_dense_count + ve - 1) * kHeadDim;
-                        tma_tile_g2s(st + oV + lay.vblk_bytes * i, &L.tm_vden, 0, row, &bar_full[s]);
-                    } else {
-                        const int sbv = u * L.v_sparse_count + (-ve - 1);
-                        tma_tile_g2s(st + oV + lay.vblk_bytes * i, &L.tm_vnnz, 0, sbv * kHeadDim, &bar_full[s]);
-                        tma_bulk_g2s(st + oVm + 1024 * i, L.v_meta + static_cast<int64_t>(sbv) * 512, 1024,
-                                     &bar_full[s]);
-                    }
-                }
-            }
         }
         __syncwarp();
-    } else if (warp == 10) {
-        // ------------------------------------------------ metadata permuter
-        // E atom u16 index for (row m, word w): 8(m&7) + ((m>>3)&1) + 128(m>>4)
-        // + 64(w&1) + 2(w>>1) (+4 for the second V block); rows m and m+8 are
-        // adjacent u16s, so each store writes a (row m, row m+8) pair.
-        for (int t = 0; t < ntiles; ++t) {
-            const int s = t % lay.stages;
-            mbar_wait_dbg(&bar_full[s], (t / lay.stages) & 1, L.dbg, 2);
+        auto meta_of = [&](int t) {
+            const int s = t % nk;
+            mbar_wait_dbg(&bar_kfull[s], (t / nk) & 1, L.dbg, 2);
             const TileInfo ti = s_tiles[t];
-            uint8_t* st = const_cast<uint8_t*>(stage_ptr0) + s * lay.stage_bytes;
-            if (!ti.kd) {
-                const bool single = ti.b1 < 0;
-                for (int pidx = lane; pidx < 64; pidx += 32) {  // row pairs (m, m+8)
-                    const int m = (pidx & 7) + 16 * (pidx >> 3);
-                    uint4 lo4 = make_uint4(0x44444444u, 0x44444444u, 0x44444444u, 0x44444444u);
-                    uint4 hi4 = lo4;
-                    if (!(single && m >= 64)) {
-                        lo4 = *reinterpret_cast<const uint4*>(st + oKm + (m >> 6) * 1024 + (m & 63) * 16);
-                        hi4 = *reinterpret_cast<const uint4*>(st + oKm + ((m + 8) >> 6) * 1024 + ((m + 8) & 63) * 16);
-                    }
-                    const uint32_t lw[4] = {lo4.x, lo4.y, lo4.z, lo4.w}, hw[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
-                    uint16_t* e = reinterpret_cast<uint16_t*>(st + oEK);
-#pragma unroll
-                    for (int w = 0; w < 8; ++w) {
-                        const uint32_t a = (lw[w >> 1] >> (16 * (w & 1))) & 0xFFFF;
-                        const uint32_t b = (hw[w >> 1] >> (16 * (w & 1))) & 0xFFFF;
-                        const int idx = 8 * (m & 7) + 128 * (m >> 4) + 64 * (w & 1) + 2 * (w >> 1);
-                        *reinterpret_cast<uint32_t*>(e + idx) = a | (b << 16);
-                    }
-                }
+            if (ti.ke0 < 0) {
+                uint8_t* st = base_ptr + lay.off_k + s * lay.k_stage;
+                permute_k_meta(st + lay.k_meta, st + lay.k_e, ti.ve1 == 0);
+                fence_async_smem();
             }
-            const int nb_t = ti.b1 >= 0 ? 2 : 1;
-            for (int i = 0; i < nb_t; ++i) {
-                if (i == 0 ? ti.vd0 : ti.vd1) continue;
-                for (int pidx = lane; pidx < 64; pidx += 32) {
-                    const int m = (pidx & 7) + 16 * (pidx >> 3);
-                    const uint2 lo2 = *reinterpret_cast<const uint2*>(st + oVm + 1024 * i + m * 8);
-                    const uint2 hi2 = *reinterpret_cast<const uint2*>(st + oVm + 1024 * i + (m + 8) * 8);
-                    const uint32_t lw[2] = {lo2.x, lo2.y}, hw[2] = {hi2.x, hi2.y};
-                    uint16_t* e = reinterpret_cast<uint16_t*>(st + oEV);
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        const uint32_t a = (lw[w >> 1] >> (16 * (w & 1))) & 0xFFFF;
-                        const uint32_t b = (hw[w >> 1] >> (16 * (w & 1))) & 0xFFFF;
-                        const int idx = 8 * (m & 7) + 128 * (m >> 4) + 64 * (w & 1) + 2 * (w >> 1) + 4 * i;
-                        *reinterpret_cast<uint32_t*>(e + idx) = a | (b << 16);
-                    }
-                }
-            }
-            fence_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_meta[s]);
+            if (lane == 0) {
+                trace(L, t, 8);
+                mbar_arrive(&bar_kmeta[s]);
+            }
+        };
+        for (int t = 0; t < ntiles; ++t) {
+            const int s = t % nk;
+            const TileInfo ti = s_tiles[t];
+            const int ke0 = uni(ti.ke0), two = uni(ti.ve1 != 0);
+            mbar_wait_dbg(&bar_kempty[s], ((t / nk) & 1) ^ 1, L.dbg, 4);
+            if (lane == 0) trace(L, t, 7);
+            if (elect_one()) {
+                uint8_t* st = base_ptr + lay.off_k + s * lay.k_stage;
+                // both blocks (consecutive slots) in one 128-row box per column half
+                if (ke0 > 0) {
+                    mbar_arrive_expect_tx(&bar_kfull[s], 32768u);
+                    const int row = (u * L.k_dense_count + ke0 - 1) * kBlock;
+                    tma_tile_g2s(st, &L.tm_kden, 0, row, &bar_kfull[s]);
+                    tma_tile_g2s(st + 16384, &L.tm_kden, 64, row, &bar_kfull[s]);
+                } else {
+                    mbar_arrive_expect_tx(&bar_kfull[s], 16384u + 1024u * (1 + two));
+                    const int sbk = u * L.k_sparse_count + (-ke0 - 1);
+                    tma_tile_g2s(st, &L.tm_knnz, 0, sbk * kBlock, &bar_kfull[s]);
+                    tma_bulk_g2s(st + lay.k_meta, L.k_meta + static_cast<int64_t>(sbk) * 512, 1024 * (1 + two),
+                                 &bar_kfull[s]);
+                }
+            }
+            __syncwarp();
+            if (t >= lag) meta_of(t - lag);
         }
-    } else if (warp == 9) {
+        for (int t = max(0, ntiles - lag); t < ntiles; ++t) meta_of(t);
+    } else if (warp_u == 10) {
+        // ------------------------------------------- V producer + V metadata
+        const int lag = nv >= 2 ? 1 : 0;
+        if (elect_one()) {
+            prefetch_tmap(&L.tm_vnnz);
+            prefetch_tmap(&L.tm_vden);
+        }
+        __syncwarp();
+        auto meta_of = [&](int t) {
+            const int s = t % nv;
+            mbar_wait_dbg(&bar_vfull[s], (t / nv) & 1, L.dbg, 2);
+            const TileInfo ti = s_tiles[t];
+            uint8_t* st = base_ptr + lay.off_v + s * lay.v_stage;
+            bool any = false;
+            if (ti.ve0 < 0) { permute_v_meta(st + lay.v_meta, st + lay.v_e, 0); any = true; }
+            if (ti.ve1 < 0) { permute_v_meta(st + lay.v_meta, st + lay.v_e, 1); any = true; }
+            if (any) fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_vmeta[s]);
+        };
+        for (int t = 0; t < ntiles; ++t) {
+            const int s = t % nv;
+            const TileInfo ti = s_tiles[t];
+            const int ve0 = uni(ti.ve0), ve1 = uni(ti.ve1);
+            mbar_wait_dbg(&bar_vempty[s], ((t / nv) & 1) ^ 1, L.dbg, 4);
+            if (elect_one()) {
+                uint8_t* st = base_ptr + lay.off_v + s * lay.v_stage;
+                const int nb_t = ve1 != 0 ? 2 : 1;
+                uint32_t bytes = ve0 > 0 ? 16384u : 9216u;
+                if (nb_t == 2) bytes += ve1 > 0 ? 16384u : 9216u;
+                mbar_arrive_expect_tx(&bar_vfull[s], bytes);
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int ve = i == 0 ? ve0 : ve1;
+                    if (i == 1 && nb_t == 1) break;
+                    if (ve > 0) {
+                        const int row = (u * L.v_dense_count + ve - 1) * kHeadDim;
+                        tma_tile_g2s(st + lay.vblk * i, &L.tm_vden, 0, row, &bar_vfull[s]);
+                    } else {
+                        const int sbv = u * L.v_sparse_count + (-ve - 1);
+                        tma_tile_g2s(st + lay.vblk * i, &L.tm_vnnz, 0, sbv * kHeadDim, &bar_vfull[s]);
+                        tma_bulk_g2s(st + lay.v_meta + 1024 * i, L.v_meta + static_cast<int64_t>(sbv) * 512, 1024,
+                                     &bar_vfull[s]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (t >= lag) meta_of(t - lag);
+        }
+        for (int t = max(0, ntiles - lag); t < ntiles; ++t) meta_of(t);
+    } else if (warp_u == 9) {
         // ------------------------------------------------------- MMA issuer
-        if (lane == 0) {
-            const bool bf = std::is_same<T, __nv_bfloat16>::value;
-            const uint32_t id_g1_sp = umma_idesc_f16(bf, 128, 128, false, false, true);
-            const uint32_t id_g1_de = umma_idesc_f16(bf, 128, 128, false, false, false);
-            const uint32_t id_g2_sp = umma_idesc_f16(bf, 128, 128, false, true, true);
-            const uint32_t id_g2_de = umma_idesc_f16(bf, 128, 128, false, true, false);
-            mbar_wait_dbg(&bar_q, 0, L.dbg, 1);
+        const bool bf = std::is_same<T, __nv_bfloat16>::value;
+        const uint32_t id_g1_sp = umma_idesc_f16(bf, 128, 128, false, false, true);
+        const uint32_t id_g1_de = umma_idesc_f16(bf, 128, 128, false, false, false);
+        const uint32_t id_g2_sp = umma_idesc_f16(bf, 128, 128, false, true, true);
+        const uint32_t id_g2_de = umma_idesc_f16(bf, 128, 128, false, true, false);
+        mbar_wait_dbg(&bar_q, 0, L.dbg, 1);
+        tc_fence_after();
+        // Descriptor bases (start address in 16-byte units in the low 14 bits:
+        // adding (bytes >> 4) advances the start address).
+        const uint64_t dQ = umma_desc(sQ, 16, 1024, kLayoutSW128);
+        const uint64_t dK = umma_desc(sK, 16, 1024, kLayoutSW128);
+        const uint64_t dVden = umma_desc(sV, 16, 1024, kLayoutSW128);
+        const uint64_t dVsp = umma_desc(sV, 16, 512, kLayoutSW64);
+        const uint64_t dP = umma_desc(sP, 16384, 1024, kLayoutSW128);
+        const uint64_t dEK = umma_desc(sK + lay.k_e, 16, 128, kLayoutNone);
+        const uint64_t dEV = umma_desc(sV + lay.v_e, 16, 128, kLayoutNone);
+        const uint32_t kst16 = lay.k_stage >> 4, vst16 = lay.v_stage >> 4, vblk16 = lay.vblk >> 4;
+        bool o_started = false;
+        auto gemm2 = [&](int tp) {
+            // O^T += V^T (tile tp) * P^T ; P^T in smem (hi, then lo for bf16)
+            const int s = tp % nv;
+            const TileInfo ti = s_tiles[tp];
+            const int ve0 = uni(ti.ve0), ve1 = uni(ti.ve1);
+            mbar_wait_dbg(&bar_vmeta[s], (tp / nv) & 1, L.dbg, 3);
+            mbar_wait_dbg(&bar_pfull[pbuf_of(tp)], pphase(tp), L.dbg, 7);
             tc_fence_after();
-            bool o_started = false;
-            auto gemm2 = [&](int tp) {
-                // O^T += V^T (tile tp) * P^T ; P^T in smem (hi, then lo for bf16)
-                const int s = tp % lay.stages;
-                const uint32_t st = stage_base(s);
-                const TileInfo ti = s_tiles[tp];
-                mbar_wait_dbg(&bar_pfull, tp & 1, L.dbg, 7);
-                tc_fence_after();
-                trace(L, tp, 5);
-                const int nb_t = ti.b1 >= 0 ? 2 : 1;
+            if (lane == 0) trace(L, tp, 5);
+            if (elect_one()) {
+                const int nb_t = (L.mode & 2) ? 0 : ve1 != 0 ? 2 : 1;
+                const uint64_t so = static_cast<uint64_t>(s) * vst16;
+                if (ve0 < 0 || ve1 < 0) tmem_cp_128x128b(tEV + 4 * (tp & 1), dEV + so);
+#pragma unroll
                 for (int pass = 0; pass < (HILO ? 2 : 1); ++pass) {
-                    const uint32_t pbase = sP + pass * 32768;
                     for (int i = 0; i < nb_t; ++i) {
-                        const bool vdense = i == 0 ? ti.vd0 : ti.vd1;
-                        const uint32_t va = st + oV + lay.vblk_bytes * i;
+                        const bool vdense = (i == 0 ? ve0 : ve1) > 0;
+                        const uint64_t pb = dP + (pbuf_of(tp) * lay.p_bytes + pass * 32768 + 8192 * i) / 16;
                         if (vdense) {
+#pragma unroll
                             for (int kk = 0; kk < 4; ++kk) {
-                                umma_f16(tO, umma_desc(va + 32 * kk, 16, 1024, kLayoutSW128),
-                                         umma_desc(pbase + 8192 * i + 2048 * kk, 16384, 1024, kLayoutSW128),
-                                         id_g2_de, o_started);
+                                umma_f16(tO, dVden + so + i * vblk16 + 2 * kk, pb + 128 * kk, id_g2_de, o_started);
                                 o_started = true;
                             }
                         } else {
+#pragma unroll
                             for (int j = 0; j < 2; ++j) {
-                                umma_sp_f16(tO, umma_desc(va + 32 * j, 16, 512, kLayoutSW64),
-                                            umma_desc(pbase + 8192 * i + 4096 * j, 16384, 1024, kLayoutSW128),
+                                umma_sp_f16(tO, dVsp + so + i * vblk16 + 2 * j, pb + 256 * j,
                                             tEV + 4 * (tp & 1) + 2 * i + j, id_g2_sp, o_started);
                                 o_started = true;
                             }
                         }
                     }
                 }
-                trace(L, tp, 6);
-                umma_commit(&bar_pempty);   // P^T buffer and O^T (for the softmax rescale)
-                umma_commit(&bar_empty[s]); // K/V stage can be refilled
-            };
-            for (int t = 0; t < ntiles; ++t) {
-                // One stage (bf16 + dense K/V) cannot hold tile t while GEMM2(t-1)
-                // still reads tile t-1: drain GEMM2(t-1) first in that case.
-                if (lay.stages == 1 && t >= 1) gemm2(t - 1);
-                const int s = t % lay.stages, sb = t & 1;
-                const uint32_t st = stage_base(s);
-                const TileInfo ti = s_tiles[t];
-                mbar_wait_dbg(&bar_full[s], (t / lay.stages) & 1, L.dbg, 2);
-                mbar_wait_dbg(&bar_meta[s], (t / lay.stages) & 1, L.dbg, 3);
-                if (t >= 2) mbar_wait_dbg(&bar_sempty[sb], ((t >> 1) - 1) & 1, L.dbg, 6);
-                tc_fence_after();
-                trace(L, t, 4);
+                umma_commit(&bar_pempty[pbuf_of(tp)]);  // P^T buffer free; O^T through tile tp final
+                umma_commit(&bar_vempty[s]);            // V stage can be refilled
+            }
+            __syncwarp();
+            o_started = true;
+            if (lane == 0) trace(L, tp, 6);
+        };
+        for (int t = 0; t < ntiles; ++t) {
+            const int s = t % nk, sb = t & 1;
+            const TileInfo ti = s_tiles[t];
+            const int ke0 = uni(ti.ke0);
+            if (lane == 0) trace(L, t, 11);
+            mbar_wait_dbg(&bar_kmeta[s], (t / nk) & 1, L.dbg, 3);  // K landed (+ metadata permuted)
+            if (lane == 0) trace(L, t, 10);
+            if (t >= 2) mbar_wait_dbg(&bar_sempty[sb], ((t >> 1) - 1) & 1, L.dbg, 6);
+            tc_fence_after();
+            if (lane == 0) trace(L, t, 4);
+            if (elect_one()) {
+                const uint64_t so = static_cast<uint64_t>(s) * kst16;
                 // metadata -> TMEM (ordered before the MMAs that read it)
-                if (!ti.kd) tmem_cp_128x128b(tEK + 4 * sb, umma_desc(st + oEK, 16, 128, kLayoutNone));
-                if (!ti.vd0 || (ti.b1 >= 0 && !ti.vd1))
-                    tmem_cp_128x128b(tEV + 4 * sb, umma_desc(st + oEV, 16, 128, kLayoutNone));
+                if (ke0 < 0) tmem_cp_128x128b(tEK + 4 * sb, dEK + so);
                 // GEMM1: S^T[sb] = K_tile * Q^T
                 const uint32_t tS = tS0 + 128 * sb;
-                if (ti.kd) {
+                if (L.mode & 2) {
+                } else if (ke0 > 0) {
+#pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        umma_f16(tS, umma_desc(st + oK + (j >> 2) * 16384 + 32 * (j & 3), 16, 1024, kLayoutSW128),
-                                 umma_desc(sQ + (j >> 2) * 16384 + 32 * (j & 3), 16, 1024, kLayoutSW128), id_g1_de,
-                                 j > 0);
+                        umma_f16(tS, dK + so + (j >> 2) * 1024 + 2 * (j & 3), dQ + (j >> 2) * 1024 + 2 * (j & 3),
+                                 id_g1_de, j > 0);
                 } else {
+#pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        umma_sp_f16(tS, umma_desc(st + oK + 32 * j, 16, 1024, kLayoutSW128),
-                                    umma_desc(sQ + (j >> 1) * 16384 + 64 * (j & 1), 16, 1024, kLayoutSW128),
-                                    tEK + 4 * sb + j, id_g1_sp, j > 0);
+                        umma_sp_f16(tS, dK + so + 2 * j, dQ + (j >> 1) * 1024 + 4 * (j & 1), tEK + 4 * sb + j,
+                                    id_g1_sp, j > 0);
                 }
                 umma_commit(&bar_sfull[sb]);
-                if (lay.stages > 1 && t >= 1) gemm2(t - 1);
+                umma_commit(&bar_kempty[s]);  // K stage can be refilled once GEMM1(t) read it
             }
-            if (ntiles > 0) gemm2(ntiles - 1);
+            __syncwarp();
+            if (t >= 1) gemm2(t - 1);
         }
-        __syncwarp();
+        if (ntiles > 0) gemm2(ntiles - 1);
     } else {
         // ------------------------------------------------------- softmax WGs
+        // S^T is read from TMEM once per tile and released at once (GEMM1(t+2) may
+        // reuse the buffer).  The running column max m lives in smem; in steady
+        // state a tile needs no cross-lane reduction at all: every thread checks
+        // x = s*scale*log2e - m <= tau for its own values, and one bar.red.or per
+        // warpgroup confirms it (P <= 2^tau fits fp16).  Only when some column grows
+        // past m + tau (first visible tile, rare later) the slow path computes the
+        // exact column max (redux.f32 + smem), updates m and rescales O^T and l.
         const int wg = warp >> 2, wq = warp & 3;
         const int r = 32 * wq + lane;  // TMEM lane = key row of the tile = d row of O^T
         const int cbase = 64 * wg;     // this warpgroup's query columns
@@ -365,114 +482,143 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         float l_part[64];
 #pragma unroll
         for (int c = 0; c < 64; ++c) l_part[c] = 0.f;
-        float m_col = -INFINITY;  // running max of column cbase + r (threads r < 64)
-        uint8_t* pbuf = base_ptr + lay.off_p;
+        if (r < 64) s_mrun[cbase + r] = -INFINITY;
+        named_bar(bar_id, 128);
+        uint8_t* const pbuf0 = base_ptr + lay.off_p;
+        const float sl2 = L.scale_log2;
         for (int t = 0; t < ntiles; ++t) {
             const int sb = t & 1;
             const TileInfo ti = s_tiles[t];
             mbar_wait_dbg(&bar_sfull[sb], (t >> 1) & 1, L.dbg, 5);
             tc_fence_after();
             if (tid == 0) trace(L, t, 0);
+            if (L.mode & 1) {  // tools: pipeline without the softmax
+                if (t >= npb) mbar_wait_dbg(&bar_pempty[pbuf_of(t)], pphase(t - npb), L.dbg, 8);
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&bar_sempty[sb]);
+                    mbar_arrive(&bar_pfull[pbuf_of(t)]);
+                }
+                continue;
+            }
             // masks: invalid rows of single-block tiles; causal (attention.hpp:181-190)
-            const bool row_valid = r < 64 || ti.b1 >= 0;
-            const int key_pos = (r < 64 ? ti.b0 : ti.b1) * kBlock + (r & 63);
+            const bool row_valid = r < 64 || ti.ve1 != 0;
+            const int key_pos = ti.dblk * kBlock + r;  // diagonal pairs are consecutive blocks
             // column c (query q0 + c at position off + q0 + c) sees this key iff c >= c_first
-            const int c_first = row_valid ? (ti.diag ? key_pos - off - q0 : 0) : 1 << 30;
-            // warp-uniform fast path: every (row, column) of this warp visible
-            const bool fast = __all_sync(0xffffffffu, c_first <= cbase);
-            const uint32_t tS = tS0 + 128 * sb + lane_off + cbase;
-            // pass 1: exact column max of the raw scores (scale > 0 commutes with max);
-            // the redux result is warp-uniform, so every lane stores it (no select)
+            const int c_first = row_valid ? (ti.dblk >= 0 ? key_pos - off - q0 : 0) : 1 << 30;
+            // The warpgroup's 64 columns are processed as two 32-column halves
+            // (32 score registers live at a time next to the 64 partial sums).
 #pragma unroll
-            for (int ch = 0; ch < 2; ++ch) {
-                uint32_t v[32];
-                tmem_ld32(tS + 32 * ch, v);
-                tmem_ld_wait();
-                float* dst = &s_red[wq][cbase + 32 * ch];
-                if (fast) {
+            for (int hf = 0; hf < 2; ++hf) {
+                const int c0 = cbase + 32 * hf;  // first column of this half
+                const uint32_t tS = tS0 + 128 * sb + lane_off + c0;
+                // warp-uniform fast path: every (row, column) of this warp visible
+                const bool fast = __all_sync(0xffffffffu, c_first <= c0);
+                float x[32];
+                auto load_s = [&]() {
+                    uint32_t v[32];
+                    tmem_ld32(tS, v);
+                    tmem_ld_wait();
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) dst[k] = redux_max(__uint_as_float(v[k]));
-                } else {
+                    for (int k = 0; k < 32; ++k) x[k] = __uint_as_float(v[k]);
+                };
+                load_s();
+                // x <- s*scale*log2e - m (masked: -inf); does any value exceed m + tau?
+#pragma unroll
+                for (int k = 0; k < 32; k += 4) {
+                    const float4 m4 = *reinterpret_cast<const float4*>(&s_mrun[c0 + k]);
+                    x[k] = fmaf(x[k], sl2, -m4.x);
+                    x[k + 1] = fmaf(x[k + 1], sl2, -m4.y);
+                    x[k + 2] = fmaf(x[k + 2], sl2, -m4.z);
+                    x[k + 3] = fmaf(x[k + 3], sl2, -m4.w);
+                }
+                if (!fast) {
 #pragma unroll
                     for (int k = 0; k < 32; ++k)
-                        dst[k] = redux_max(cbase + 32 * ch + k >= c_first ? __uint_as_float(v[k]) : -INFINITY);
+                        if (c0 + k < c_first) x[k] = -INFINITY;
                 }
-            }
-            if (r == 0) s_rescale[wg][t & 1] = 0;
-            named_bar(bar_id, 128);
-            if (r < 64) {
-                const int c = cbase + r;
-                float tm = fmaxf(fmaxf(s_red[0][c], s_red[1][c]), fmaxf(s_red[2][c], s_red[3][c]));
-                tm = tm * L.scale_log2;
-                float mnew = m_col, alpha = 1.f;
-                if (tm > -INFINITY && (m_col == -INFINITY || tm > m_col + kTau)) {
-                    mnew = tm;
-                    alpha = m_col == -INFINITY ? 1.f : fast_exp2(m_col - mnew);
-                    if (m_col != -INFINITY) s_rescale[wg][t & 1] = 1;
-                }
-                m_col = mnew;
-                s_mnew[c] = mnew;
-                s_alpha[c] = alpha;
-            }
-            named_bar(bar_id, 128);
-            if (tid == 0) trace(L, t, 1);
-            // P^T buffer free + O^T stable (GEMM2(t-1) complete)
-            if (t >= 1) mbar_wait_dbg(&bar_pempty, (t - 1) & 1, L.dbg, 8);
-            tc_fence_after();
-            if (tid == 0) trace(L, t, 2);
-            if (s_rescale[wg][t & 1]) {
+                float xmax = -INFINITY;
 #pragma unroll
-                for (int cc = 0; cc < 64; ++cc) l_part[cc] *= s_alpha[cbase + cc];
-                if (t >= 1) {
+                for (int k = 0; k < 32; k += 4)
+                    xmax = fmaxf(fmaxf(xmax, fmaxf(x[k], x[k + 1])), fmaxf(x[k + 2], x[k + 3]));
+                if (bar_red_or(bar_id, !(xmax <= kTau))) {
+                    // ---- slow path: exact column max of this half-tile, update m (lazy
+                    // rule).  (!(xmax <= tau) also catches a NaN from m = -inf.)
+                    load_s();
 #pragma unroll
-                    for (int ch = 0; ch < 2; ++ch) {
-                        uint32_t v[32];
-                        tmem_ld32(tO + lane_off + cbase + 32 * ch, v);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int k = 0; k < 32; k += 4) {
-                            const float4 a4 = *reinterpret_cast<const float4*>(&s_alpha[cbase + 32 * ch + k]);
-                            v[k] = __float_as_uint(__uint_as_float(v[k]) * a4.x);
-                            v[k + 1] = __float_as_uint(__uint_as_float(v[k + 1]) * a4.y);
-                            v[k + 2] = __float_as_uint(__uint_as_float(v[k + 2]) * a4.z);
-                            v[k + 3] = __float_as_uint(__uint_as_float(v[k + 3]) * a4.w);
-                        }
-#pragma unroll
-                        for (int k = 0; k < 32; k += 4)
-                            tmem_st4(tO + lane_off + cbase + 32 * ch + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
+                    for (int k = 0; k < 32; ++k) {
+                        const bool vis = fast || c0 + k >= c_first;
+                        x[k] = vis ? x[k] * sl2 : -INFINITY;  // s*scale*log2e (scale > 0 commutes with max)
+                        s_red[wq][c0 + k] = redux_max(x[k]);
                     }
-                    tmem_st_wait();
-                }
-            }
-            // pass 2: probabilities, row sums, P^T (+ residual for bf16)
+                    named_bar(bar_id, 128);
+                    bool resc = false;
+                    if (r < 32) {
+                        const int c = c0 + r;
+                        const float tm = fmaxf(fmaxf(s_red[0][c], s_red[1][c]), fmaxf(s_red[2][c], s_red[3][c]));
+                        const float mo = s_mrun[c];
+                        float mnew = mo, alpha = 1.f;
+                        if (tm > -INFINITY && (mo == -INFINITY || tm > mo + kTau)) {
+                            mnew = tm;
+                            if (mo != -INFINITY) {
+                                alpha = fast_exp2(mo - mnew);
+                                resc = true;
+                            }
+                        }
+                        s_mnew[c] = mnew;
+                        s_alpha[c] = alpha;
+                    }
+                    resc = bar_red_or(bar_id, resc);
+                    if (r < 32) s_mrun[c0 + r] = s_mnew[c0 + r];
+                    // x <- x - m_new (masked stay -inf; columns with no visible key yet stay -inf)
 #pragma unroll
-            for (int ch = 0; ch < 2; ++ch) {
-                uint32_t v[32];
-                tmem_ld32(tS + 32 * ch, v);
-                tmem_ld_wait();
+                    for (int k = 0; k < 32; ++k) {
+                        const float mn = s_mnew[c0 + k];
+                        x[k] = mn == -INFINITY ? -INFINITY : x[k] - mn;
+                    }
+                    if (resc) {
+                        // O^T (GEMM2(t-1) complete) and l rescale for the grown columns
+                        if (t >= 1) mbar_wait_dbg(&bar_pempty[pbuf_of(t - 1)], pphase(t - 1), L.dbg, 8);
+                        tc_fence_after();
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) l_part[32 * hf + k] *= s_alpha[c0 + k];
+                        if (t >= 1) {
+                            uint32_t v[32];
+                            tmem_ld32(tO + lane_off + c0, v);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int k = 0; k < 32; ++k)
+                                v[k] = __float_as_uint(__uint_as_float(v[k]) * s_alpha[c0 + k]);
+#pragma unroll
+                            for (int k = 0; k < 32; k += 4)
+                                tmem_st4(tO + lane_off + c0 + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
+                            tmem_st_wait();
+                        }
+                    }
+                    named_bar(bar_id, 128);  // s_mnew / s_alpha reads done before the next slow path
+                }
+                if (hf == 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bar_sempty[sb]);  // this warp is done with S^T[sb]
+                }
+                if (tid == 0) trace(L, t, 1);
+                // P^T buffer free + O^T stable (GEMM2(t-1) complete)
+                if (hf == 0 && t >= npb) mbar_wait_dbg(&bar_pempty[pbuf_of(t)], pphase(t - npb), L.dbg, 8);
+                if (tid == 0) trace(L, t, 2);
+                // probabilities, partial column sums, P^T (+ residual for bf16)
 #pragma unroll
                 for (int g8 = 0; g8 < 4; ++g8) {
-                    const int q8 = (cbase >> 3) + 4 * ch + g8;  // 8-query chunk index in 0..15
-                    const float4 ma = *reinterpret_cast<const float4*>(&s_mnew[8 * q8]);
-                    const float4 mb = *reinterpret_cast<const float4*>(&s_mnew[8 * q8 + 4]);
-                    const float mm[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+                    const int q8 = (c0 >> 3) + g8;  // 8-query chunk index in 0..15
                     float p[8];
-                    if (fast) {
 #pragma unroll
-                        for (int k = 0; k < 8; ++k)
-                            p[k] = fast_exp2(fmaf(__uint_as_float(v[8 * g8 + k]), L.scale_log2, -mm[k]));
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const float x = fmaf(__uint_as_float(v[8 * g8 + k]), L.scale_log2, -mm[k]);
-                            const int cc = 8 * q8 + k;
-                            p[k] = (cc >= c_first && mm[k] != -INFINITY) ? fast_exp2(x) : 0.f;
-                        }
+                    for (int k = 0; k < 8; ++k) {
+                        p[k] = fast_exp2(x[8 * g8 + k]);  // exp2(-inf) = 0
+                        l_part[32 * hf + 8 * g8 + k] += p[k];
                     }
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) l_part[32 * ch + 8 * g8 + k] += p[k];
                     const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
                                                 F16Traits<T>::pack(p[4], p[5]), F16Traits<T>::pack(p[6], p[7]));
+                    uint8_t* const pbuf = pbuf0 + pbuf_of(t) * lay.p_bytes;
                     *reinterpret_cast<uint4*>(pbuf + pt_chunk_off(r, q8)) = hi;
                     if (HILO) {
                         float rr[8];
@@ -490,17 +636,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             }
             if (tid == 0) trace(L, t, 3);
             tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_sempty[sb]);  // this warp is done with S^T[sb]
             fence_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_pfull);
+            if (lane == 0) mbar_arrive(&bar_pfull[pbuf_of(t)]);
         }
         // ---------------------------------------------------- epilogue ----
-        if (ntiles > 0) mbar_wait_dbg(&bar_pempty, (ntiles - 1) & 1, L.dbg, 8);
+        if (ntiles > 0) mbar_wait_dbg(&bar_pempty[pbuf_of(ntiles - 1)], pphase(ntiles - 1), L.dbg, 8);
         tc_fence_after();
         // l[c] = sum over the 128 key lanes of l_part[c]: transpose through smem
-        float* s_l = reinterpret_cast<float*>(base_ptr + lay.off_stage) + wg * (128 * 65);
+        float* s_l = reinterpret_cast<float*>(base_ptr + lay.off_k) + wg * (128 * 65);
         named_bar(bar_id, 128);
 #pragma unroll
         for (int c = 0; c < 64; ++c) s_l[r * 65 + c] = l_part[c];
@@ -531,23 +675,56 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
 
 }  // namespace
 
+int prefill_tile_cap(int nb) { return nb / 2 + 8; }
+
 cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     PrefillLayout lay;
     const bool hilo = L.bf16;
-    lay.k_bytes = L.k_dense_count > 0 ? 32768u : 16384u;
-    lay.vblk_bytes = L.v_dense_count > 0 ? 16384u : 9216u;
-    lay.vblk_bytes = (lay.vblk_bytes + 1023u) & ~1023u;
-    lay.stage_bytes = lay.k_bytes + 2 * lay.vblk_bytes + 8192u;
+    // K stage: dense 128x128 tile, or 128x64 nnz + 2 KB metadata + 2 KB E atom.
+    const bool kden = L.k_dense_count > 0, vden = L.v_dense_count > 0;
+    lay.k_meta = 16384u;
+    lay.k_e = 18432u;
+    lay.k_stage = kden ? 32768u : 20480u;
+    // V stage: two V^T blocks (dense 128x64 or nnz 128x32) + 2 KB metadata + 2 KB E.
+    lay.vblk = vden ? 16384u : 9216u;
+    lay.v_meta = 2 * lay.vblk;
+    lay.v_e = lay.v_meta + 2048u;
+    lay.v_stage = lay.v_e + 2048u;
+    lay.tile_cap = static_cast<uint32_t>(prefill_tile_cap(L.nb));
+    const uint32_t tiles_bytes = (lay.tile_cap * sizeof(TileInfo) + 1023u) & ~1023u;
     lay.off_q = 0;
     lay.off_p = 32768;
-    lay.off_stage = 32768 + (hilo ? 65536u : 32768u);
-    const uint32_t budget = 227u * 1024u - 16384u /*static smem*/ - 1024u - lay.off_stage;
-    uint32_t stages = budget / lay.stage_bytes;
-    if (stages > 4) stages = 4;
-    if (stages < 1) return cudaErrorInvalidConfiguration;
-    lay.stages = stages;
-    size_t smem = lay.off_stage + static_cast<size_t>(stages) * lay.stage_bytes + 1024;
-    const size_t epi = lay.off_stage + 2 * 128 * 65 * 4 + 1024;
+    lay.p_bytes = hilo ? 65536u : 32768u;  // P^T (hi [+ lo]) per buffer
+    const uint32_t budget = 227u * 1024u - 8192u /*static smem*/ - 1024u /*align*/ - tiles_bytes;
+    // Preference order: 2 K + 2 V stages with two P^T buffers, then fewer P^T
+    // buffers, then shallower rings.
+    const uint32_t plans[][3] = {{2, 3, 3}, {2, 2, 3}, {2, 3, 2}, {2, 2, 2}, {1, 2, 2}, {2, 2, 1}, {2, 1, 2},
+                                 {1, 2, 1}, {1, 1, 2}, {1, 1, 1}};
+    bool ok = false;
+    for (const auto& pl : plans) {
+        const uint32_t need = 32768u + pl[0] * lay.p_bytes + pl[1] * lay.k_stage + pl[2] * lay.v_stage;
+        if (need <= budget) {
+            lay.n_pbuf = pl[0];
+            lay.nk = pl[1];
+            lay.nv = pl[2];
+            ok = true;
+            break;
+        }
+    }
+    if (!ok) return cudaErrorInvalidConfiguration;
+    if (const char* env = getenv("HS_PREFILL_PLAN")) {  // tools: "pbuf,nk,nv"
+        unsigned a, b, c;
+        if (sscanf(env, "%u,%u,%u", &a, &b, &c) == 3) {
+            lay.n_pbuf = a;
+            lay.nk = b;
+            lay.nv = c;
+        }
+    }
+    lay.off_k = lay.off_p + lay.n_pbuf * lay.p_bytes;
+    lay.off_v = lay.off_k + lay.nk * lay.k_stage;
+    lay.off_tiles = lay.off_v + lay.nv * lay.v_stage;
+    size_t smem = lay.off_tiles + tiles_bytes + 1024;
+    const size_t epi = lay.off_k + 2 * 128 * 65 * 4 + 1024;
     if (smem < epi) smem = epi;
     const dim3 grid((L.n_q + 127) / 128, L.gqa, L.n_units);
     if (L.bf16) {

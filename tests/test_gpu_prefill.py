@@ -76,6 +76,32 @@ def test_prefill_sampled_rows_8k(hs, port, s):
     assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
 
 
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("s,causal", [(1.0, True), (0.5, True), (0.0, False)])
+def test_prefill_growing_scores(hs, port, dtype, s, causal):
+    """Keys scaled by a ramp along the sequence (and one hot block late in it),
+    so column maxima grow tile after tile: exercises the lazy-rescale slow path
+    (running max update, O^T / l rescale) against the oracle."""
+    U, gqa, L, n_q = 1, 2, 2048, 2048
+    kx = np.stack([port.random_gaussian(L, 128, port.head_seed(11, u, 0)) for u in range(U)])
+    ramp = (1.0 + 3.0 * np.arange(L, dtype=np.float32) / L)[None, :, None]
+    kx = kx * ramp
+    kx[:, 1600:1664] *= 4.0
+    kx = port.round_to(kx.astype(np.float32), dtype)
+    vx = gen_units(port, U, L, 128, 11, 1, dtype)
+    kc, vc = hs.prune_cache(to_torch(kx, dtype), to_torch(vx, dtype), hs.SparsityConfig(s, s, 64))
+    q = np.stack([np.stack([port.round_to(port.random_gaussian(n_q, 128, port.head_seed(11, u, 2 + g)) * 2.0, dtype)
+                            for g in range(gqa)]) for u in range(U)])
+    scale = np.float32(1.0 / math.sqrt(128))
+    got = hs.prefill_attention(to_torch(q, dtype), kc, vc, causal=causal, scale=float(scale)).cpu().numpy()
+
+    def one(g):
+        return port.prefill(q[0, g], device_to_oracle(kc, 0), device_to_oracle(vc, 0), None, None, causal, scale, 64)
+    want = np.stack(parallel(one, range(gqa)))[None]
+    mx, mr = err_stats(got, want)
+    assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
+
+
 def test_prefill_rejects_invalid(hs, port):
     from paper_2604_16864_b200 import ConfigError
     kc, vc, q = setup(hs, port, 1, 256, 1.0, "f16", 1, 256)

@@ -1,31 +1,38 @@
+"""Per-tile event clocks of CTA (0,0,0) (HS_PREFILL_TRACE), median per-tile gaps.
+Events: 0 softmax got S(t); 1 after the max check; 2 P buffer free; 3 P(t) stored;
+4 MMA warp passed full/meta/sempty for GEMM1(t); 5 MMA warp got pfull(t);
+6 GEMM2(t) issued."""
 import os, sys, numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2604_16864_b200 import hierasparse as hs
-L = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+L = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 s = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 torch.manual_seed(0)
-k = torch.randn(8, L, 128, device="cuda").half(); v = torch.randn(8, L, 128, device="cuda").half()
+k = torch.randn(1, L, 128, device="cuda").half(); v = torch.randn(1, L, 128, device="cuda").half()
 kc, vc = hs.prune_cache(k, v, hs.SparsityConfig(s, s, 64))
-q = torch.randn(8, 4, L, 128, device="cuda").half()
+q = torch.randn(1, 1, 128, 128, device="cuda").half()
 hs.prefill_attention(q, kc, vc, causal=True); torch.cuda.synchronize()
 os.environ["HS_PREFILL_TRACE"] = "/tmp/trace.bin"
 hs.prefill_attention(q, kc, vc, causal=True); torch.cuda.synchronize()
-tr = np.fromfile("/tmp/trace.bin", dtype=np.int64).reshape(4096, 8)
-n = int((tr[:, 0] > 0).sum())
-t0 = tr[0, 0]
-d = tr[:n] - t0
-print("tiles", n, "total cycles", tr[n - 1, 3] - t0, "per tile", (tr[n - 1, 3] - tr[n // 2, 3]) / (n - 1 - n // 2))
-names = ["sfull_ok", "pass1_done", "pempty_ok", "pass2_done", "mma_g1_issue", "mma_pfull_ok", "mma_g2_issued"]
-for t in list(range(3)) + list(range(n // 2, n // 2 + 6)):
-    print(t, " ".join(f"{names[e]}={d[t, e]}" for e in range(7)))
-st = tr[n // 4: 3 * n // 4]
-print("median durations (cycles):")
-print(" pass1 (sfull->bar2):", np.median(st[:, 1] - st[:, 0]))
-print(" wait pempty:", np.median(st[:, 2] - st[:, 1]))
-print(" pass2:", np.median(st[:, 3] - st[:, 2]))
-print(" sfull(t+1) after pass2(t):", np.median(tr[n // 4 + 1: 3 * n // 4 + 1, 0] - st[:, 3]))
-print(" pfull->g2 issued:", np.median(st[:, 6] - st[:, 5]))
-print(" g2 issued -> pempty_ok(t+1):", np.median(tr[n // 4 + 1: 3 * n // 4 + 1, 2] - st[:, 6]))
-print(" pass2_done(t) -> mma pfull_ok(t):", np.median(st[:, 5] - st[:, 3]))
-print(" g1 issue(t+1) - pfull? :", np.median(tr[n // 4 + 1: 3 * n // 4 + 1, 4] - st[:, 5]))
+tr = np.fromfile("/tmp/trace.bin", dtype=np.int64).reshape(4096, 16)
+n = int((tr[:, 4] > 0).sum())
+t0 = tr[0, 4]
+d = np.where(tr[:n] > 0, tr[:n] - t0, -1)
+print(f"L={L} s={s} mode={os.environ.get('HS_PREFILL_MODE', '0')} tiles {n} cycles {tr[n - 1, 6] - t0} "
+      f"per tile {(tr[n - 1, 4] - tr[n // 2, 4]) / (n - 1 - n // 2):.0f}")
+for t in list(range(3)) + list(range(n // 2, n // 2 + 4)):
+    print(t, " ".join(f"e{e}={d[t, e]}" for e in range(12)))
+st = slice(n // 4, 3 * n // 4)
+nx = slice(n // 4 + 1, 3 * n // 4 + 1)
+med = lambda a: float(np.median(a))
+print("median gaps (cycles): e4(t+1)-e4(t) %.0f | e0-e4 (sfull seen after g1 issue) %.0f | e5-e4 %.0f | e6-e5 %.0f | e4(t+1)-e6(t) %.0f"
+      % (med(tr[nx, 4] - tr[st, 4]), med(tr[st, 0] - tr[st, 4]), med(tr[st, 5] - tr[st, 4]), med(tr[st, 6] - tr[st, 5]),
+         med(tr[nx, 4] - tr[st, 6])))
+if tr[st, 3].min() > 0:
+    print("softmax: e1-e0 %.0f | e2-e1 %.0f | e3-e2 %.0f | e0(t+1)-e3(t) %.0f | e5(t)-e3(t) %.0f"
+          % (med(tr[st, 1] - tr[st, 0]), med(tr[st, 2] - tr[st, 1]), med(tr[st, 3] - tr[st, 2]),
+             med(tr[nx, 0] - tr[st, 3]), med(tr[st, 5] - tr[st, 3])))
+print("producer/meta: e7(t+1)-e7(t) %.0f | e9-e7 (TMA landed after issue) %.0f | e8-e9 (meta) %.0f | e9-e11 (MMA waited full) %.0f | e4-e10 (sempty wait) %.0f"
+      % (med(tr[nx, 7] - tr[st, 7]), med(tr[st, 9] - tr[st, 7]), med(tr[st, 8] - tr[st, 9]), med(tr[st, 9] - tr[st, 11]),
+         med(tr[st, 4] - tr[st, 10])))
