@@ -540,6 +540,14 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     L.k_slot_block = k->slot_block;
     L.k_meta = k->meta_pool;
     L.v_meta = v->meta_pool;
+    {
+        const size_t kb = static_cast<size_t>(k->n_units) * k->sparse_count * 1024;
+        const size_t vb = static_cast<size_t>(v->n_units) * v->sparse_count * 2048;
+        uint8_t* ws = static_cast<uint8_t*>(workspace(s, kb + vb + 256, kWsPrefill, &st));
+        if (st) return st;
+        L.k_meta_hw = reinterpret_cast<uint16_t*>(ws);
+        L.v_meta_hw = reinterpret_cast<uint16_t*>(ws + kb);
+    }
     L.out = out;
     static long long* trace = nullptr;
     if (getenv("HS_PREFILL_TRACE")) {
@@ -566,6 +574,7 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     if (!ok) return fail(HS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     cudaError_t e = hs::launch_prefill(L, s);
     count_launch();
+    count_launch();  // metadata atom-order pass + the attention kernel
     if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
     if (L.trace) {
         static std::vector<long long> host(4096 * 16);

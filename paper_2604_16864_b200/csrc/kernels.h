@@ -92,6 +92,8 @@ struct PrefillLaunch {
     const int32_t* k_slot_block;
     const uint16_t* k_meta;
     const uint16_t* v_meta;
+    uint16_t* k_meta_hw;     // workspace: K metadata in the tcgen05 TMEM atom order, 1 KB / block
+    uint16_t* v_meta_hw;     // workspace: V metadata atom rows (8 of 16 bytes used), 2 KB / block
     const void* k_tail;
     const void* v_tail;
     float* out;

@@ -34,7 +34,16 @@
 namespace hs {
 namespace {
 
-constexpr int kThreads = 352;  // 2 softmax warpgroups + TMA + MMA + metadata warps
+#ifndef HS_PREFILL_WG
+#define HS_PREFILL_WG 4
+#endif
+constexpr int kSoftWG = HS_PREFILL_WG;     // softmax warpgroups (each owns kCols query columns); 4 + 4 role warps = 20 warps
+constexpr int kCols = 128 / kSoftWG;       // query columns per softmax thread
+constexpr int kSoftWarps = 4 * kSoftWG;
+constexpr int kWarpK = kSoftWarps;         // TMA producer (tile list, Q, K and V tiles)
+constexpr int kWarpMma = kSoftWarps + 1;   // tcgen05 issuer of GEMM1 (S^T = K Q^T), TMEM owner
+constexpr int kWarpMma2 = kSoftWarps + 2;  // tcgen05 issuer of GEMM2 (O^T += V^T P^T)
+constexpr int kThreads = 32 * (kSoftWarps + 3);
 
 constexpr float kTau = 8.0f;      // lazy-rescale threshold (log2 units): P <= 2^8
 
@@ -68,6 +77,24 @@ struct PrefillLayout {
 __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// TMEM -> registers: this warp's 32 lanes x N consecutive 32-bit columns.
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
+    if constexpr (N == 16) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+    } else {
+#pragma unroll
+        for (int c = 0; c < N; c += 32) tmem_ld32(taddr + c, *reinterpret_cast<uint32_t(*)[32]>(&r[c]));
+    }
+}
 
 // Barrier over `n` threads of named barrier `id` that also ORs a predicate.
 __device__ __forceinline__ bool bar_red_or(int id, bool v) {
@@ -100,12 +127,45 @@ __device__ __forceinline__ void trace(const PrefillLaunch& L, int t, int ev) {
         L.trace[t * 16 + ev] = clock64();
 }
 
+// Canonical 2-bit metadata (nm_metadata.hpp:42-46: row m of a stored block has
+// 8 (K) or 4 (V) u16 words) -> the tcgen05 TMEM metadata atom, so the prefill
+// kernel copies it smem -> TMEM with tcgen05.cp and no per-tile shuffling.
+// Atom u16 index of (row m, word w): 8(m&7) + ((m>>3)&1) + 128(m>>4) + 64(w&1)
+// + 2(w>>1) (pinned by tools/probes/umma_probe.cu).  K: 1 KB per block (a pair
+// of consecutive slots is the 2 KB atom of a 128-row tile).  V: 2 KB per block,
+// 16-byte lane rows of which the first 8 bytes are used (one tcgen05.cp per
+// block into its own 4-column group).
+__global__ void __launch_bounds__(128) meta_atom_kernel(const uint16_t* __restrict__ k_meta, int k_blocks,
+                                                        const uint16_t* __restrict__ v_meta, int v_blocks,
+                                                        uint16_t* __restrict__ k_hw, uint16_t* __restrict__ v_hw) {
+    const int b = blockIdx.x, m = threadIdx.x;  // one CTA per block, one thread per stored row
+    auto idx = [](int m, int w) { return 8 * (m & 7) + ((m >> 3) & 1) + 128 * (m >> 4) + 64 * (w & 1) + 2 * (w >> 1); };
+    if (b < k_blocks) {
+        if (m < 64) {
+            const uint4 row = *reinterpret_cast<const uint4*>(k_meta + static_cast<int64_t>(b) * 512 + m * 8);
+            const uint32_t wd[4] = {row.x, row.y, row.z, row.w};
+            uint16_t* dst = k_hw + static_cast<int64_t>(b) * 512;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) dst[idx(m, w)] = static_cast<uint16_t>(wd[w >> 1] >> (16 * (w & 1)));
+        }
+    } else {
+        const int vb = b - k_blocks;
+        const uint2 row = *reinterpret_cast<const uint2*>(v_meta + static_cast<int64_t>(vb) * 512 + m * 4);
+        const uint32_t wd[2] = {row.x, row.y};
+        uint16_t* dst = v_hw + static_cast<int64_t>(vb) * 1024;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) dst[idx(m, w)] = static_cast<uint16_t>(wd[w >> 1] >> (16 * (w & 1)));
+        if (m < 64) *reinterpret_cast<uint2*>(dst + 16 * m + 4) = make_uint2(0u, 0u);  // unused halves of
+        if (m < 64) *reinterpret_cast<uint2*>(dst + 16 * m + 12) = make_uint2(0u, 0u); // the 16-byte rows
+    }
+}
+
 template <typename T, bool HILO>
 __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_constant__ PrefillLaunch L,
                                                                PrefillLayout lay) {
     extern __shared__ uint8_t smem_raw[];
-    __shared__ __align__(8) uint64_t bar_q, bar_kfull[4], bar_kmeta[4], bar_kempty[4];
-    __shared__ __align__(8) uint64_t bar_vfull[4], bar_vmeta[4], bar_vempty[4];
+    __shared__ __align__(8) uint64_t bar_q, bar_kfull[4], bar_kempty[4];
+    __shared__ __align__(8) uint64_t bar_vfull[4], bar_vempty[4];
     __shared__ __align__(8) uint64_t bar_sfull[2], bar_sempty[2], bar_pfull[2], bar_pempty[2];
     __shared__ uint32_t s_tmem;
     __shared__ int s_ntiles;
@@ -130,28 +190,26 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     const int nk = static_cast<int>(lay.nk), nv = static_cast<int>(lay.nv);
 
     // ------------------------------------------------------------ setup ----
-    if (warp == 9) tmem_alloc(&s_tmem, 512);
+    if (warp == kWarpMma) tmem_alloc(&s_tmem, 512);
     if (tid == 0) {
         mbar_init(&bar_q, 1);
         for (int s = 0; s < nk; ++s) {
             mbar_init(&bar_kfull[s], 1);
-            mbar_init(&bar_kmeta[s], 1);
             mbar_init(&bar_kempty[s], 1);
         }
         for (int s = 0; s < nv; ++s) {
             mbar_init(&bar_vfull[s], 1);
-            mbar_init(&bar_vmeta[s], 1);
             mbar_init(&bar_vempty[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bar_sfull[i], 1);
-            mbar_init(&bar_sempty[i], 8);
-            mbar_init(&bar_pfull[i], 8);
+            mbar_init(&bar_sempty[i], kSoftWarps);
+            mbar_init(&bar_pfull[i], kSoftWarps);
             mbar_init(&bar_pempty[i], 1);
         }
         fence_barrier_init();
     }
-    if (warp == 8) {
+    if (warp == kWarpK) {
         // Key-tile list (see header).  Block b is fully visible iff its last key
         // <= the tile's first query position; visible iff its first key <= the last.
         // The kind-grouped pairs are index arithmetic over the slot lists, so the
@@ -215,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     auto pbuf_of = [npb](int t) { return npb == 2 ? (t & 1) : 0; };
     auto pphase = [npb](int t) { return static_cast<uint32_t>((npb == 2 ? (t >> 1) : t) & 1); };
     const int ntiles = s_ntiles;
-    // TMEM columns: S[0] 0..127, S[1] 128..255, O 256..383, E_K[2] 384.., E_V[2] 392..
+    // TMEM columns: S[0] 0..127, S[1] 128..255, O 256..383, E_K[2] 384..391, E_V[2] 392..407
     const uint32_t tS0 = tmem, tO = tmem + 256, tEK = tmem + 384, tEV = tmem + 392;
 
     const int warp_u = warp_id_uniform();
@@ -224,50 +282,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     // arithmetic below stays in uniform registers and the single-thread
     // tcgen05 / TMA instructions issue without R2UR waterfall loops.
     auto uni = [](int v) { return __shfl_sync(0xffffffffu, v, 0); };
-    // Canonical 2-bit metadata rows -> tcgen05 TMEM metadata atom.  E atom u16
-    // index for (row m, word w): 8(m&7) + ((m>>3)&1) + 128(m>>4) + 64(w&1) +
-    // 2(w>>1) (+4 for the second V block); rows m and m+8 are adjacent u16s, so
-    // each store writes a (row m, row m+8) pair.
-    auto permute_k_meta = [&](const uint8_t* meta, uint8_t* e, bool single) {
-        for (int pidx = lane; pidx < 64; pidx += 32) {  // row pairs (m, m+8)
-            const int m = (pidx & 7) + 16 * (pidx >> 3);
-            uint4 lo4 = make_uint4(0x44444444u, 0x44444444u, 0x44444444u, 0x44444444u);
-            uint4 hi4 = lo4;
-            if (!(single && m >= 64)) {
-                lo4 = *reinterpret_cast<const uint4*>(meta + m * 16);
-                hi4 = *reinterpret_cast<const uint4*>(meta + (m + 8) * 16);
-            }
-            const uint32_t lw[4] = {lo4.x, lo4.y, lo4.z, lo4.w}, hw[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
-#pragma unroll
-            for (int w = 0; w < 8; ++w) {
-                const uint32_t a = (lw[w >> 1] >> (16 * (w & 1))) & 0xFFFF;
-                const uint32_t b = (hw[w >> 1] >> (16 * (w & 1))) & 0xFFFF;
-                const int idx = 8 * (m & 7) + 128 * (m >> 4) + 64 * (w & 1) + 2 * (w >> 1);
-                *reinterpret_cast<uint32_t*>(reinterpret_cast<uint16_t*>(e) + idx) = a | (b << 16);
-            }
-        }
-    };
-    auto permute_v_meta = [&](const uint8_t* meta, uint8_t* e, int i) {
-        for (int pidx = lane; pidx < 64; pidx += 32) {
-            const int m = (pidx & 7) + 16 * (pidx >> 3);
-            const uint2 lo2 = *reinterpret_cast<const uint2*>(meta + 1024 * i + m * 8);
-            const uint2 hi2 = *reinterpret_cast<const uint2*>(meta + 1024 * i + (m + 8) * 8);
-            const uint32_t lw[2] = {lo2.x, lo2.y}, hw[2] = {hi2.x, hi2.y};
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                const uint32_t a = (lw[w >> 1] >> (16 * (w & 1))) & 0xFFFF;
-                const uint32_t b = (hw[w >> 1] >> (16 * (w & 1))) & 0xFFFF;
-                const int idx = 8 * (m & 7) + 128 * (m >> 4) + 64 * (w & 1) + 2 * (w >> 1) + 4 * i;
-                *reinterpret_cast<uint32_t*>(reinterpret_cast<uint16_t*>(e) + idx) = a | (b << 16);
-            }
-        }
-    };
-    if (warp_u == 8) {
-        // ------------------------------------------- K producer + K metadata
-        // Issue K(t), then permute the metadata of K(t-1) (one tile behind, so the
-        // TMA of the next tile is in flight while this warp waits for a landing;
-        // with a single stage K(t+1) needs K(t) consumed, so no lag).
-        const int lag = nk >= 2 ? 1 : 0;
+    if (warp_u == kWarpK) {
+        // --------------------------------------------------------- producer
         if (elect_one()) {
             prefetch_tmap(&L.tm_q);
             prefetch_tmap(&L.tm_knnz);
@@ -278,22 +294,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             tma_tile_g2s(base_ptr + lay.off_q + 16384, &L.tm_q, 64, qrow, &bar_q);
         }
         __syncwarp();
-        auto meta_of = [&](int t) {
-            const int s = t % nk;
-            mbar_wait_dbg(&bar_kfull[s], (t / nk) & 1, L.dbg, 2);
-            const TileInfo ti = s_tiles[t];
-            if (ti.ke0 < 0) {
-                uint8_t* st = base_ptr + lay.off_k + s * lay.k_stage;
-                permute_k_meta(st + lay.k_meta, st + lay.k_e, ti.ve1 == 0);
-                fence_async_smem();
-            }
-            __syncwarp();
-            if (lane == 0) {
-                trace(L, t, 8);
-                mbar_arrive(&bar_kmeta[s]);
-            }
-        };
-        for (int t = 0; t < ntiles; ++t) {
+        if (elect_one()) {
+            prefetch_tmap(&L.tm_vnnz);
+            prefetch_tmap(&L.tm_vden);
+        }
+        __syncwarp();
+        auto issue_k = [&](int t) {
             const int s = t % nk;
             const TileInfo ti = s_tiles[t];
             const int ke0 = uni(ti.ke0), two = uni(ti.ve1 != 0);
@@ -311,35 +317,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     mbar_arrive_expect_tx(&bar_kfull[s], 16384u + 1024u * (1 + two));
                     const int sbk = u * L.k_sparse_count + (-ke0 - 1);
                     tma_tile_g2s(st, &L.tm_knnz, 0, sbk * kBlock, &bar_kfull[s]);
-                    tma_bulk_g2s(st + lay.k_meta, L.k_meta + static_cast<int64_t>(sbk) * 512, 1024 * (1 + two),
+                    tma_bulk_g2s(st + lay.k_e, L.k_meta_hw + static_cast<int64_t>(sbk) * 512, 1024 * (1 + two),
                                  &bar_kfull[s]);
                 }
             }
             __syncwarp();
-            if (t >= lag) meta_of(t - lag);
-        }
-        for (int t = max(0, ntiles - lag); t < ntiles; ++t) meta_of(t);
-    } else if (warp_u == 10) {
-        // ------------------------------------------- V producer + V metadata
-        const int lag = nv >= 2 ? 1 : 0;
-        if (elect_one()) {
-            prefetch_tmap(&L.tm_vnnz);
-            prefetch_tmap(&L.tm_vden);
-        }
-        __syncwarp();
-        auto meta_of = [&](int t) {
-            const int s = t % nv;
-            mbar_wait_dbg(&bar_vfull[s], (t / nv) & 1, L.dbg, 2);
-            const TileInfo ti = s_tiles[t];
-            uint8_t* st = base_ptr + lay.off_v + s * lay.v_stage;
-            bool any = false;
-            if (ti.ve0 < 0) { permute_v_meta(st + lay.v_meta, st + lay.v_e, 0); any = true; }
-            if (ti.ve1 < 0) { permute_v_meta(st + lay.v_meta, st + lay.v_e, 1); any = true; }
-            if (any) fence_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_vmeta[s]);
         };
-        for (int t = 0; t < ntiles; ++t) {
+        auto issue_v = [&](int t) {
             const int s = t % nv;
             const TileInfo ti = s_tiles[t];
             const int ve0 = uni(ti.ve0), ve1 = uni(ti.ve1);
@@ -347,8 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             if (elect_one()) {
                 uint8_t* st = base_ptr + lay.off_v + s * lay.v_stage;
                 const int nb_t = ve1 != 0 ? 2 : 1;
-                uint32_t bytes = ve0 > 0 ? 16384u : 9216u;
-                if (nb_t == 2) bytes += ve1 > 0 ? 16384u : 9216u;
+                uint32_t bytes = ve0 > 0 ? 16384u : 8192u + 2048u;
+                if (nb_t == 2) bytes += ve1 > 0 ? 16384u : 8192u + 2048u;
                 mbar_arrive_expect_tx(&bar_vfull[s], bytes);
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
@@ -360,17 +344,25 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     } else {
                         const int sbv = u * L.v_sparse_count + (-ve - 1);
                         tma_tile_g2s(st + lay.vblk * i, &L.tm_vnnz, 0, sbv * kHeadDim, &bar_vfull[s]);
-                        tma_bulk_g2s(st + lay.v_meta + 1024 * i, L.v_meta + static_cast<int64_t>(sbv) * 512, 1024,
+                        tma_bulk_g2s(st + lay.v_e + 2048 * i, L.v_meta_hw + static_cast<int64_t>(sbv) * 1024, 2048,
                                      &bar_vfull[s]);
                     }
                 }
             }
             __syncwarp();
-            if (t >= lag) meta_of(t - lag);
+        };
+        // K(t) is consumed a tile earlier than V(t): issue K one tile ahead.
+        for (int t = 0; t < ntiles; ++t) {
+            issue_k(t);
+            if (t >= 1) issue_v(t - 1);
         }
-        for (int t = max(0, ntiles - lag); t < ntiles; ++t) meta_of(t);
-    } else if (warp_u == 9) {
-        // ------------------------------------------------------- MMA issuer
+        if (ntiles > 0) issue_v(ntiles - 1);
+    } else if (warp_u == kWarpMma || warp_u == kWarpMma2) {
+        // ------------------------------------------------------ MMA issuers
+        // kWarpMma issues GEMM1 (S^T = K Q^T) per tile, kWarpMma2 GEMM2
+        // (O^T += V^T P^T): the two chains wait on different barriers (K / S
+        // buffer vs V / P^T), so neither stalls the other's issue.  Each
+        // tcgen05.commit tracks the MMAs of its own thread only.
         const bool bf = std::is_same<T, __nv_bfloat16>::value;
         const uint32_t id_g1_sp = umma_idesc_f16(bf, 128, 128, false, false, true);
         const uint32_t id_g1_de = umma_idesc_f16(bf, 128, 128, false, false, false);
@@ -394,14 +386,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             const int s = tp % nv;
             const TileInfo ti = s_tiles[tp];
             const int ve0 = uni(ti.ve0), ve1 = uni(ti.ve1);
-            mbar_wait_dbg(&bar_vmeta[s], (tp / nv) & 1, L.dbg, 3);
+            mbar_wait_dbg(&bar_vfull[s], (tp / nv) & 1, L.dbg, 3);
             mbar_wait_dbg(&bar_pfull[pbuf_of(tp)], pphase(tp), L.dbg, 7);
             tc_fence_after();
             if (lane == 0) trace(L, tp, 5);
             if (elect_one()) {
                 const int nb_t = (L.mode & 2) ? 0 : ve1 != 0 ? 2 : 1;
                 const uint64_t so = static_cast<uint64_t>(s) * vst16;
-                if (ve0 < 0 || ve1 < 0) tmem_cp_128x128b(tEV + 4 * (tp & 1), dEV + so);
+                if (ve0 < 0) tmem_cp_128x128b(tEV + 8 * (tp & 1), dEV + so);
+                if (ve1 < 0) tmem_cp_128x128b(tEV + 8 * (tp & 1) + 4, dEV + so + 128);
 #pragma unroll
                 for (int pass = 0; pass < (HILO ? 2 : 1); ++pass) {
                     for (int i = 0; i < nb_t; ++i) {
@@ -417,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
 #pragma unroll
                             for (int j = 0; j < 2; ++j) {
                                 umma_sp_f16(tO, dVsp + so + i * vblk16 + 2 * j, pb + 256 * j,
-                                            tEV + 4 * (tp & 1) + 2 * i + j, id_g2_sp, o_started);
+                                            tEV + 8 * (tp & 1) + 4 * i + j, id_g2_sp, o_started);
                                 o_started = true;
                             }
                         }
@@ -430,12 +423,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             o_started = true;
             if (lane == 0) trace(L, tp, 6);
         };
+        if (warp_u == kWarpMma2) {
+            for (int tp = 0; tp < ntiles; ++tp) gemm2(tp);
+        } else
         for (int t = 0; t < ntiles; ++t) {
             const int s = t % nk, sb = t & 1;
             const TileInfo ti = s_tiles[t];
             const int ke0 = uni(ti.ke0);
             if (lane == 0) trace(L, t, 11);
-            mbar_wait_dbg(&bar_kmeta[s], (t / nk) & 1, L.dbg, 3);  // K landed (+ metadata permuted)
+            mbar_wait_dbg(&bar_kfull[s], (t / nk) & 1, L.dbg, 3);  // K tile + metadata atom landed
             if (lane == 0) trace(L, t, 10);
             if (t >= 2) mbar_wait_dbg(&bar_sempty[sb], ((t >> 1) - 1) & 1, L.dbg, 6);
             tc_fence_after();
@@ -462,27 +458,27 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 umma_commit(&bar_kempty[s]);  // K stage can be refilled once GEMM1(t) read it
             }
             __syncwarp();
-            if (t >= 1) gemm2(t - 1);
         }
-        if (ntiles > 0) gemm2(ntiles - 1);
     } else {
         // ------------------------------------------------------- softmax WGs
-        // S^T is read from TMEM once per tile and released at once (GEMM1(t+2) may
-        // reuse the buffer).  The running column max m lives in smem; in steady
-        // state a tile needs no cross-lane reduction at all: every thread checks
-        // x = s*scale*log2e - m <= tau for its own values, and one bar.red.or per
-        // warpgroup confirms it (P <= 2^tau fits fp16).  Only when some column grows
-        // past m + tau (first visible tile, rare later) the slow path computes the
-        // exact column max (redux.f32 + smem), updates m and rescales O^T and l.
+        // kSoftWG warpgroups; WG g owns query columns [kCols*g, kCols*(g+1)); warp
+        // w reads TMEM lanes 32(w%4).. (key row r of the tile = d row of O^T).
+        // S^T is read from TMEM once per tile and released at once.  The running
+        // column max m lives in smem; in steady state a tile needs no cross-lane
+        // reduction: every thread checks x = s*scale*log2e - m <= tau for its own
+        // values, one bar.red.or per warpgroup confirms it (P <= 2^tau fits fp16).
+        // Only when a column grows past m + tau (first visible tile, rare later)
+        // the slow path computes the exact column max (redux.f32 + smem), updates
+        // m and rescales O^T and the partial sums.
         const int wg = warp >> 2, wq = warp & 3;
         const int r = 32 * wq + lane;  // TMEM lane = key row of the tile = d row of O^T
-        const int cbase = 64 * wg;     // this warpgroup's query columns
+        const int c0 = kCols * wg;     // this warpgroup's first query column
         const int bar_id = 1 + wg;
         const uint32_t lane_off = static_cast<uint32_t>(32 * wq) << 16;
-        float l_part[64];
+        float l_part[kCols];
 #pragma unroll
-        for (int c = 0; c < 64; ++c) l_part[c] = 0.f;
-        if (r < 64) s_mrun[cbase + r] = -INFINITY;
+        for (int c = 0; c < kCols; ++c) l_part[c] = 0.f;
+        if (r < kCols) s_mrun[c0 + r] = -INFINITY;
         named_bar(bar_id, 128);
         uint8_t* const pbuf0 = base_ptr + lay.off_p;
         const float sl2 = L.scale_log2;
@@ -501,141 +497,131 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 }
                 continue;
             }
+            const uint32_t tS = tS0 + 128 * sb + lane_off + c0;
+            float x[kCols];
+            auto load_s = [&]() {
+                uint32_t v[kCols];
+                tmem_ld_cols<kCols>(tS, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int k = 0; k < kCols; ++k) x[k] = __uint_as_float(v[k]);
+            };
+            load_s();
             // masks: invalid rows of single-block tiles; causal (attention.hpp:181-190)
             const bool row_valid = r < 64 || ti.ve1 != 0;
             const int key_pos = ti.dblk * kBlock + r;  // diagonal pairs are consecutive blocks
             // column c (query q0 + c at position off + q0 + c) sees this key iff c >= c_first
             const int c_first = row_valid ? (ti.dblk >= 0 ? key_pos - off - q0 : 0) : 1 << 30;
-            // The warpgroup's 64 columns are processed as two 32-column halves
-            // (32 score registers live at a time next to the 64 partial sums).
+            // warp-uniform fast path: every (row, column) of this warp visible
+            const bool fast = __all_sync(0xffffffffu, c_first <= c0);
+            // x <- s*scale*log2e - m (masked: -inf); does any value exceed m + tau?
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                const int c0 = cbase + 32 * hf;  // first column of this half
-                const uint32_t tS = tS0 + 128 * sb + lane_off + c0;
-                // warp-uniform fast path: every (row, column) of this warp visible
-                const bool fast = __all_sync(0xffffffffu, c_first <= c0);
-                float x[32];
-                auto load_s = [&]() {
-                    uint32_t v[32];
-                    tmem_ld32(tS, v);
-                    tmem_ld_wait();
+            for (int k = 0; k < kCols; k += 4) {
+                const float4 m4 = *reinterpret_cast<const float4*>(&s_mrun[c0 + k]);
+                x[k] = fmaf(x[k], sl2, -m4.x);
+                x[k + 1] = fmaf(x[k + 1], sl2, -m4.y);
+                x[k + 2] = fmaf(x[k + 2], sl2, -m4.z);
+                x[k + 3] = fmaf(x[k + 3], sl2, -m4.w);
+            }
+            if (!fast) {
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) x[k] = __uint_as_float(v[k]);
-                };
+                for (int k = 0; k < kCols; ++k)
+                    if (c0 + k < c_first) x[k] = -INFINITY;
+            }
+            float xmax = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < kCols; k += 4)
+                xmax = fmaxf(fmaxf(xmax, fmaxf(x[k], x[k + 1])), fmaxf(x[k + 2], x[k + 3]));
+            if (bar_red_or(bar_id, !(xmax <= kTau))) {
+                // ---- slow path (!(xmax <= tau) also catches a NaN from m = -inf)
                 load_s();
-                // x <- s*scale*log2e - m (masked: -inf); does any value exceed m + tau?
 #pragma unroll
-                for (int k = 0; k < 32; k += 4) {
-                    const float4 m4 = *reinterpret_cast<const float4*>(&s_mrun[c0 + k]);
-                    x[k] = fmaf(x[k], sl2, -m4.x);
-                    x[k + 1] = fmaf(x[k + 1], sl2, -m4.y);
-                    x[k + 2] = fmaf(x[k + 2], sl2, -m4.z);
-                    x[k + 3] = fmaf(x[k + 3], sl2, -m4.w);
+                for (int k = 0; k < kCols; ++k) {
+                    const bool vis = fast || c0 + k >= c_first;
+                    x[k] = vis ? x[k] * sl2 : -INFINITY;  // s*scale*log2e (scale > 0 commutes with max)
+                    s_red[wq][c0 + k] = redux_max(x[k]);
                 }
-                if (!fast) {
-#pragma unroll
-                    for (int k = 0; k < 32; ++k)
-                        if (c0 + k < c_first) x[k] = -INFINITY;
-                }
-                float xmax = -INFINITY;
-#pragma unroll
-                for (int k = 0; k < 32; k += 4)
-                    xmax = fmaxf(fmaxf(xmax, fmaxf(x[k], x[k + 1])), fmaxf(x[k + 2], x[k + 3]));
-                if (bar_red_or(bar_id, !(xmax <= kTau))) {
-                    // ---- slow path: exact column max of this half-tile, update m (lazy
-                    // rule).  (!(xmax <= tau) also catches a NaN from m = -inf.)
-                    load_s();
-#pragma unroll
-                    for (int k = 0; k < 32; ++k) {
-                        const bool vis = fast || c0 + k >= c_first;
-                        x[k] = vis ? x[k] * sl2 : -INFINITY;  // s*scale*log2e (scale > 0 commutes with max)
-                        s_red[wq][c0 + k] = redux_max(x[k]);
-                    }
-                    named_bar(bar_id, 128);
-                    bool resc = false;
-                    if (r < 32) {
-                        const int c = c0 + r;
-                        const float tm = fmaxf(fmaxf(s_red[0][c], s_red[1][c]), fmaxf(s_red[2][c], s_red[3][c]));
-                        const float mo = s_mrun[c];
-                        float mnew = mo, alpha = 1.f;
-                        if (tm > -INFINITY && (mo == -INFINITY || tm > mo + kTau)) {
-                            mnew = tm;
-                            if (mo != -INFINITY) {
-                                alpha = fast_exp2(mo - mnew);
-                                resc = true;
-                            }
-                        }
-                        s_mnew[c] = mnew;
-                        s_alpha[c] = alpha;
-                    }
-                    resc = bar_red_or(bar_id, resc);
-                    if (r < 32) s_mrun[c0 + r] = s_mnew[c0 + r];
-                    // x <- x - m_new (masked stay -inf; columns with no visible key yet stay -inf)
-#pragma unroll
-                    for (int k = 0; k < 32; ++k) {
-                        const float mn = s_mnew[c0 + k];
-                        x[k] = mn == -INFINITY ? -INFINITY : x[k] - mn;
-                    }
-                    if (resc) {
-                        // O^T (GEMM2(t-1) complete) and l rescale for the grown columns
-                        if (t >= 1) mbar_wait_dbg(&bar_pempty[pbuf_of(t - 1)], pphase(t - 1), L.dbg, 8);
-                        tc_fence_after();
-#pragma unroll
-                        for (int k = 0; k < 32; ++k) l_part[32 * hf + k] *= s_alpha[c0 + k];
-                        if (t >= 1) {
-                            uint32_t v[32];
-                            tmem_ld32(tO + lane_off + c0, v);
-                            tmem_ld_wait();
-#pragma unroll
-                            for (int k = 0; k < 32; ++k)
-                                v[k] = __float_as_uint(__uint_as_float(v[k]) * s_alpha[c0 + k]);
-#pragma unroll
-                            for (int k = 0; k < 32; k += 4)
-                                tmem_st4(tO + lane_off + c0 + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
-                            tmem_st_wait();
+                named_bar(bar_id, 128);
+                bool resc = false;
+                if (r < kCols) {
+                    const int c = c0 + r;
+                    const float tm = fmaxf(fmaxf(s_red[0][c], s_red[1][c]), fmaxf(s_red[2][c], s_red[3][c]));
+                    const float mo = s_mrun[c];
+                    float mnew = mo, alpha = 1.f;
+                    if (tm > -INFINITY && (mo == -INFINITY || tm > mo + kTau)) {
+                        mnew = tm;
+                        if (mo != -INFINITY) {
+                            alpha = fast_exp2(mo - mnew);
+                            resc = true;
                         }
                     }
-                    named_bar(bar_id, 128);  // s_mnew / s_alpha reads done before the next slow path
+                    s_mnew[c] = mnew;
+                    s_alpha[c] = alpha;
                 }
-                if (hf == 1) {
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&bar_sempty[sb]);  // this warp is done with S^T[sb]
+                resc = bar_red_or(bar_id, resc);
+                if (r < kCols) s_mrun[c0 + r] = s_mnew[c0 + r];
+                // x <- x - m_new (masked stay -inf; columns with no visible key yet stay -inf)
+#pragma unroll
+                for (int k = 0; k < kCols; ++k) {
+                    const float mn = s_mnew[c0 + k];
+                    x[k] = mn == -INFINITY ? -INFINITY : x[k] - mn;
                 }
-                if (tid == 0) trace(L, t, 1);
-                // P^T buffer free + O^T stable (GEMM2(t-1) complete)
-                if (hf == 0 && t >= npb) mbar_wait_dbg(&bar_pempty[pbuf_of(t)], pphase(t - npb), L.dbg, 8);
-                if (tid == 0) trace(L, t, 2);
-                // probabilities, partial column sums, P^T (+ residual for bf16)
+                if (resc) {
+                    // O^T (GEMM2(t-1) complete) and l rescale for the grown columns
+                    if (t >= 1) mbar_wait_dbg(&bar_pempty[pbuf_of(t - 1)], pphase(t - 1), L.dbg, 8);
+                    tc_fence_after();
 #pragma unroll
-                for (int g8 = 0; g8 < 4; ++g8) {
-                    const int q8 = (c0 >> 3) + g8;  // 8-query chunk index in 0..15
-                    float p[8];
+                    for (int k = 0; k < kCols; ++k) l_part[k] *= s_alpha[c0 + k];
+                    if (t >= 1) {
+                        uint32_t v[kCols];
+                        tmem_ld_cols<kCols>(tO + lane_off + c0, v);
+                        tmem_ld_wait();
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        p[k] = fast_exp2(x[8 * g8 + k]);  // exp2(-inf) = 0
-                        l_part[32 * hf + 8 * g8 + k] += p[k];
+                        for (int k = 0; k < kCols; ++k)
+                            v[k] = __float_as_uint(__uint_as_float(v[k]) * s_alpha[c0 + k]);
+#pragma unroll
+                        for (int k = 0; k < kCols; k += 4)
+                            tmem_st4(tO + lane_off + c0 + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
+                        tmem_st_wait();
                     }
-                    const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
-                                                F16Traits<T>::pack(p[4], p[5]), F16Traits<T>::pack(p[6], p[7]));
-                    uint8_t* const pbuf = pbuf0 + pbuf_of(t) * lay.p_bytes;
-                    *reinterpret_cast<uint4*>(pbuf + pt_chunk_off(r, q8)) = hi;
-                    if (HILO) {
-                        float rr[8];
+                }
+                named_bar(bar_id, 128);  // s_mnew / s_alpha reads done before the next slow path
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_sempty[sb]);  // this warp is done with S^T[sb]
+            if (tid == 0) trace(L, t, 1);
+            // P^T buffer free (GEMM2 of its previous tile complete)
+            if (t >= npb) mbar_wait_dbg(&bar_pempty[pbuf_of(t)], pphase(t - npb), L.dbg, 8);
+            if (tid == 0) trace(L, t, 2);
+            // probabilities, partial column sums, P^T (+ residual for bf16)
+            uint8_t* const pbuf = pbuf0 + pbuf_of(t) * lay.p_bytes;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const uint32_t w = (&hi.x)[k];
-                            rr[2 * k] = p[2 * k] - F16Traits<T>::to_float(static_cast<uint16_t>(w & 0xFFFF));
-                            rr[2 * k + 1] = p[2 * k + 1] - F16Traits<T>::to_float(static_cast<uint16_t>(w >> 16));
-                        }
-                        const uint4 lo = make_uint4(F16Traits<T>::pack(rr[0], rr[1]), F16Traits<T>::pack(rr[2], rr[3]),
-                                                    F16Traits<T>::pack(rr[4], rr[5]), F16Traits<T>::pack(rr[6], rr[7]));
-                        *reinterpret_cast<uint4*>(pbuf + 32768 + pt_chunk_off(r, q8)) = lo;
+            for (int g8 = 0; g8 < kCols / 8; ++g8) {
+                const int q8 = (c0 >> 3) + g8;  // 8-query chunk index in 0..15
+                float p[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    p[k] = fast_exp2(x[8 * g8 + k]);  // exp2(-inf) = 0
+                    l_part[8 * g8 + k] += p[k];
+                }
+                const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
+                                            F16Traits<T>::pack(p[4], p[5]), F16Traits<T>::pack(p[6], p[7]));
+                *reinterpret_cast<uint4*>(pbuf + pt_chunk_off(r, q8)) = hi;
+                if (HILO) {
+                    float rr[8];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t w = (&hi.x)[k];
+                        rr[2 * k] = p[2 * k] - F16Traits<T>::to_float(static_cast<uint16_t>(w & 0xFFFF));
+                        rr[2 * k + 1] = p[2 * k + 1] - F16Traits<T>::to_float(static_cast<uint16_t>(w >> 16));
                     }
+                    const uint4 lo = make_uint4(F16Traits<T>::pack(rr[0], rr[1]), F16Traits<T>::pack(rr[2], rr[3]),
+                                                F16Traits<T>::pack(rr[4], rr[5]), F16Traits<T>::pack(rr[6], rr[7]));
+                    *reinterpret_cast<uint4*>(pbuf + 32768 + pt_chunk_off(r, q8)) = lo;
                 }
             }
             if (tid == 0) trace(L, t, 3);
-            tc_fence_before();
             fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_pfull[pbuf_of(t)]);
@@ -644,33 +630,32 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         if (ntiles > 0) mbar_wait_dbg(&bar_pempty[pbuf_of(ntiles - 1)], pphase(ntiles - 1), L.dbg, 8);
         tc_fence_after();
         // l[c] = sum over the 128 key lanes of l_part[c]: transpose through smem
-        float* s_l = reinterpret_cast<float*>(base_ptr + lay.off_k) + wg * (128 * 65);
-        named_bar(bar_id, 128);
+        // (the K ring is free: every GEMM has completed)
+        float* s_l = reinterpret_cast<float*>(base_ptr + lay.off_k) + wg * (128 * (kCols + 1));
 #pragma unroll
-        for (int c = 0; c < 64; ++c) s_l[r * 65 + c] = l_part[c];
+        for (int c = 0; c < kCols; ++c) s_l[r * (kCols + 1) + c] = l_part[c];
         named_bar(bar_id, 128);
-        if (r < 64) {
+        if (r < kCols) {
             float lsum = 0.f;
-            for (int k = 0; k < 128; ++k) lsum += s_l[k * 65 + r];
-            s_alpha[cbase + r] = lsum > 0.f ? 1.f / lsum : 0.f;
+            for (int k = 0; k < 128; ++k) lsum += s_l[k * (kCols + 1) + r];
+            s_alpha[c0 + r] = lsum > 0.f ? 1.f / lsum : 0.f;
         }
         named_bar(bar_id, 128);
         float* out = L.out + (static_cast<int64_t>(u * L.gqa + h) * L.n_q + q0) * kHeadDim;
-#pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-            uint32_t v[32];
-            tmem_ld32(tO + lane_off + cbase + 32 * ch, v);
+        {
+            uint32_t v[kCols];
+            tmem_ld_cols<kCols>(tO + lane_off + c0, v);
             tmem_ld_wait();
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                const int c = cbase + 32 * ch + k;
+            for (int k = 0; k < kCols; ++k) {
+                const int c = c0 + k;
                 if (c < rows_q) out[c * kHeadDim + r] = __uint_as_float(v[k]) * s_alpha[c];
             }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 9) tmem_dealloc(tmem, 512);
+    if (warp == kWarpMma) tmem_dealloc(tmem, 512);
 }
 
 }  // namespace
@@ -682,14 +667,14 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     const bool hilo = L.bf16;
     // K stage: dense 128x128 tile, or 128x64 nnz + 2 KB metadata + 2 KB E atom.
     const bool kden = L.k_dense_count > 0, vden = L.v_dense_count > 0;
-    lay.k_meta = 16384u;
-    lay.k_e = 18432u;
-    lay.k_stage = kden ? 32768u : 20480u;
+    lay.k_meta = 0;  // unused: the metadata atoms come prepared (meta_atom_kernel)
+    lay.k_e = 16384u;
+    lay.k_stage = kden ? 32768u : 18432u;
     // V stage: two V^T blocks (dense 128x64 or nnz 128x32) + 2 KB metadata + 2 KB E.
-    lay.vblk = vden ? 16384u : 9216u;
-    lay.v_meta = 2 * lay.vblk;
-    lay.v_e = lay.v_meta + 2048u;
-    lay.v_stage = lay.v_e + 2048u;
+    lay.vblk = vden ? 16384u : 8192u;
+    lay.v_meta = 0;  // unused: the metadata atoms come prepared (meta_atom_kernel)
+    lay.v_e = 2 * lay.vblk;
+    lay.v_stage = lay.v_e + 4096u;
     lay.tile_cap = static_cast<uint32_t>(prefill_tile_cap(L.nb));
     const uint32_t tiles_bytes = (lay.tile_cap * sizeof(TileInfo) + 1023u) & ~1023u;
     lay.off_q = 0;
@@ -724,8 +709,16 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     lay.off_v = lay.off_k + lay.nk * lay.k_stage;
     lay.off_tiles = lay.off_v + lay.nv * lay.v_stage;
     size_t smem = lay.off_tiles + tiles_bytes + 1024;
-    const size_t epi = lay.off_k + 2 * 128 * 65 * 4 + 1024;
+    const size_t epi = lay.off_k + kSoftWG * 128 * (kCols + 1) * 4 + 1024;
     if (smem < epi) smem = epi;
+    {
+        const int kb = L.n_units * L.k_sparse_count, vb = L.n_units * L.v_sparse_count;
+        if (kb + vb > 0) {
+            meta_atom_kernel<<<kb + vb, 128, 0, s>>>(L.k_meta, kb, L.v_meta, vb, L.k_meta_hw, L.v_meta_hw);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+        }
+    }
     const dim3 grid((L.n_q + 127) / 128, L.gqa, L.n_units);
     if (L.bf16) {
         auto k = prefill_kernel<__nv_bfloat16, true>;

@@ -22,7 +22,7 @@ d = np.where(tr[:n] > 0, tr[:n] - t0, -1)
 print(f"L={L} s={s} mode={os.environ.get('HS_PREFILL_MODE', '0')} tiles {n} cycles {tr[n - 1, 6] - t0} "
       f"per tile {(tr[n - 1, 4] - tr[n // 2, 4]) / (n - 1 - n // 2):.0f}")
 for t in list(range(3)) + list(range(n // 2, n // 2 + 4)):
-    print(t, " ".join(f"e{e}={d[t, e]}" for e in range(12)))
+    print(t, " ".join(f"e{e}={d[t, e]}" for e in range(13)))
 st = slice(n // 4, 3 * n // 4)
 nx = slice(n // 4 + 1, 3 * n // 4 + 1)
 med = lambda a: float(np.median(a))
@@ -33,6 +33,7 @@ if tr[st, 3].min() > 0:
     print("softmax: e1-e0 %.0f | e2-e1 %.0f | e3-e2 %.0f | e0(t+1)-e3(t) %.0f | e5(t)-e3(t) %.0f"
           % (med(tr[st, 1] - tr[st, 0]), med(tr[st, 2] - tr[st, 1]), med(tr[st, 3] - tr[st, 2]),
              med(tr[nx, 0] - tr[st, 3]), med(tr[st, 5] - tr[st, 3])))
-print("producer/meta: e7(t+1)-e7(t) %.0f | e9-e7 (TMA landed after issue) %.0f | e8-e9 (meta) %.0f | e9-e11 (MMA waited full) %.0f | e4-e10 (sempty wait) %.0f"
-      % (med(tr[nx, 7] - tr[st, 7]), med(tr[st, 9] - tr[st, 7]), med(tr[st, 8] - tr[st, 9]), med(tr[st, 9] - tr[st, 11]),
-         med(tr[st, 4] - tr[st, 10])))
+print("K producer: issue period e7 %.0f | meta start after issue e9-e7 %.0f | kfull wait e12-e9 %.0f | permute e8-e12 %.0f"
+      " | MMA kmeta wait e10-e11 %.0f | sempty wait e4-e10 %.0f"
+      % (med(tr[nx, 7] - tr[st, 7]), med(tr[st, 9] - tr[st, 7]), med(tr[st, 12] - tr[st, 9]), med(tr[st, 8] - tr[st, 12]),
+         med(tr[st, 10] - tr[st, 11]), med(tr[st, 4] - tr[st, 10])))
