@@ -147,6 +147,106 @@ def host_caches(dev, units):
 
 
 # ---------------------------------------------------------------- our arm ---
+def build_workload(args, hs, dev, rank, world, scale):
+    """The decode workload this rank runs (synthetic bf16 K/V, compressed on device):
+
+    config2 (headline, BASELINE configs[1]): this rank's own request, 8 KV heads x
+        GQA 4 x 128K, S_K=S_V=1 — weak scaling over ranks, no collective.
+    config4 (configs[3]): 32 requests x 32K x 8 KV heads, KV heads sharded over the
+        ranks (each rank: 8/N heads x 32 requests = 256/N units) — strong scaling.
+    config5 (configs[4]): 1 request x 1M tokens x 8 KV heads, the sequence split
+        into N contiguous shards (distributed.sequence_shard); each step = decode
+        partial over the shard + NCCL all-gather of the (O, m, l) partials +
+        LSE combine — strong scaling."""
+    import torch
+    from paper_2604_16864_b200 import distributed as Dd
+    cfg = hs.SparsityConfig(1.0, 1.0, 64)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    if args.workload == "config2":
+        units, L_ctx, blocks = U, L, L // 64
+        desc = {"workload": "configs[1]: Llama-3.1-8B GQA decode, 32 q / 8 kv heads, d=128, 128K ctx, batch 1 "
+                            "per GPU, S_K=S_V=1 (2:4 K+V)", "kv_heads": U, "gqa": GQA, "context": L,
+                "block_size": 64, "s_key": 1.0, "s_value": 1.0, "parallelism": f"request-per-GPU x{world}"}
+        scaling = "weak"
+    elif args.workload == "config4":
+        heads = Dd.heads_of_rank(8, world, rank)
+        units, L_ctx, blocks = 32 * heads.size, 32768, 32768 // 64
+        desc = {"workload": "configs[3]: batched decode, 32 requests x 32K ctx x 8 KV heads x GQA 4, S_K=S_V=1, "
+                            "KV heads sharded over GPUs", "requests": 32, "kv_heads": 8, "gqa": GQA,
+                "context": 32768, "parallelism": f"kv-head shards x{world} ({heads.size} heads/GPU)"}
+        scaling = "strong"
+    elif args.workload == "config5":
+        sh = Dd.sequence_shard(1 << 14, world, rank)
+        units, L_ctx, blocks = U, sh.size * 64, sh.size
+        desc = {"workload": "configs[4]: 1M-token decode, 8 KV heads x GQA 4, S_K=S_V=1, sequence split over "
+                            "GPUs + NCCL all-gather of partials", "kv_heads": U, "gqa": GQA, "context": 1 << 20,
+                "parallelism": f"sequence shards x{world} ({sh.size} blocks/GPU)"}
+        scaling = "strong"
+    else:
+        raise SystemExit(f"unknown workload {args.workload}")
+    # compress in chunks of units to bound the dense staging buffer (<= 4 GB)
+    chunk = max(1, min(units, (1 << 31) // (L_ctx * D * 2)))
+    kcs, vcs = [], []
+    comp_ms = []
+    comp_bytes = 0
+    for c0 in range(0, units, chunk):
+        n = min(chunk, units - c0)
+        key = torch.randn((n, L_ctx, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+        val = torch.randn((n, L_ctx, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+        if c0 == 0:  # compression (prune_cache + fused_magnitude_compress) timed on the first chunk
+            for _ in range(3):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                kc0, vc0 = hs.prune_cache(key, val, cfg)
+                e1.record()
+                torch.cuda.synchronize()
+                comp_ms.append(e0.elapsed_time(e1))
+            comp_bytes = 2 * key.numel() * 2 + kc0.nbytes() + vc0.nbytes() + 2 * n * kc0.logical_blocks * (8 + 1 + 4)
+            kcs.append(kc0)
+            vcs.append(vc0)
+        else:
+            kc0, vc0 = hs.prune_cache(key, val, cfg)
+            kcs.append(kc0)
+            vcs.append(vc0)
+        del key, val
+    q = torch.randn((units, GQA, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    _, bytes_u = hs.flop_and_byte_count(GQA, kcs[0], vcs[0], 0, False)
+    step_bytes = units * bytes_u
+    wl = {"kc": kcs[0], "vc": vcs[0], "q": q, "bytes": step_bytes, "config": desc, "scaling": scaling,
+          "comp_ms": comp_ms, "comp_bytes": comp_bytes, "plan": None}
+    if args.workload == "config5":
+        last = rank == world - 1
+
+        def call(qd):
+            return Dd.sequence_split_decode(qd, kcs[0], vcs[0], is_last=last, scale=scale)
+        wl["step"] = lambda: call(q)
+        wl["e2e_call"] = call
+        wl["e2e_name"] = "distributed.sequence_split_decode (decode_partial + all-gather + decode_combine)"
+        return wl
+    # one CUDA graph per chunk of units (the decode step of every unit of this rank)
+    plans = [hs.DecodePlan(q[i * chunk:(i + 1) * chunk], kcs[i], vcs[i], scale=scale) for i in range(len(kcs))]
+
+    class MultiPlan:
+        kernels_per_step = sum(p.kernels_per_step for p in plans)
+        out = plans[0].out
+
+        def __call__(self):
+            for p in plans:
+                p()
+    wl["plan"] = MultiPlan()
+    wl["step"] = wl["plan"]
+    outs = [torch.empty((kc.n_units, GQA, D), dtype=torch.float32, device=dev) for kc in kcs]
+
+    def call(qd):
+        for i in range(len(kcs)):
+            hs.decode_attention(qd[i * chunk:(i + 1) * chunk], kcs[i], vcs[i], scale=scale, out=outs[i])
+        return outs[0] if len(outs) == 1 else torch.cat(outs)
+    wl["e2e_call"] = call
+    wl["e2e_name"] = "hierasparse.decode_attention"
+    return wl
+
+
 def run_ours(args):
     import torch
     from paper_2604_16864_b200 import capi
@@ -156,44 +256,22 @@ def run_ours(args):
     dev = torch.device("cuda", torch.cuda.current_device())
     hbm_peak, _, peak_kind = peaks()
     scale = 1.0 / math.sqrt(D)
-
-    # Synthetic inputs of the configs[1] shape (distinct per rank = per request).
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    key = torch.randn((U, L, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
-    val = torch.randn((U, L, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
-    q = torch.randn((U, GQA, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
-    cfg = hs.SparsityConfig(1.0, 1.0, 64)
-
-    # Compression (prune_cache + fused_magnitude_compress), timed on its own.
-    comp_ms = []
-    for i in range(3):
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        kc, vc = hs.prune_cache(key, val, cfg)
-        e1.record()
-        torch.cuda.synchronize()
-        comp_ms.append(e0.elapsed_time(e1))
-    comp_bytes = 2 * key.numel() * 2 + kc.nbytes() + vc.nbytes() + 2 * U * kc.logical_blocks * (8 + 1 + 4)
-
-    flops_u, bytes_u = hs.flop_and_byte_count(GQA, kc, vc, 0, False)
-    step_bytes = U * bytes_u  # 302,056,032 at configs[1]
-    out = torch.empty((U, GQA, D), dtype=torch.float32, device=dev)
+    wl = build_workload(args, hs, dev, rank, world, scale)
+    kc, vc, q, step_bytes = wl["kc"], wl["vc"], wl["q"], wl["bytes"]
+    comp_ms, comp_bytes = wl["comp_ms"], wl["comp_bytes"]
     # L2 flush between timed steps: read (not write) a 2x-L2 buffer, so the next
     # step starts with an L2 full of clean, unrelated lines (a write flush would
     # charge ~126 MB of dirty-line writebacks to the timed kernel).
     flush = torch.ones(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
-    flush_sink = torch.empty(1, dtype=torch.float32, device=dev)
+    flush_sink = torch.empty((), dtype=torch.float32, device=dev)
 
     def flush_l2():
         torch.sum(flush, dim=0, out=flush_sink)
 
-    # The decode step is replayed from a CUDA graph (hs.DecodePlan): the device
-    # time of the step is the kernels', not the host's enqueue latency.
-    plan = hs.DecodePlan(q, kc, vc, scale=scale)
-    out = plan.out
+    plan = wl["plan"]
+    step = wl["step"]
     for _ in range(args.warmup):
-        plan()
+        step()
     torch.cuda.synchronize()
 
     # ---- timed region: K decode steps (device events), L2 flushed between steps
@@ -207,7 +285,7 @@ def run_ours(args):
         for i in range(args.steps):
             flush_l2()
             starts[i].record()
-            plan()
+            step()
             stops[i].record()
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
@@ -216,10 +294,10 @@ def run_ours(args):
         t_soak = time.perf_counter()
         while not args.profile and time.perf_counter() - t_soak < 1.5:
             for _ in range(50):
-                plan()
+                step()
             torch.cuda.synchronize()
     barrier(world)
-    launches = capi.kernel_launches() - launches0 + args.steps * plan.kernels_per_step
+    launches = capi.kernel_launches() - launches0 + (args.steps * plan.kernels_per_step if plan else 0)
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, stops)]
     ms = statistics.mean(step_ms)
     ms_max = max_over_ranks(ms, world)
@@ -228,12 +306,13 @@ def run_ours(args):
 
     # ---- e2e: host queries in (pinned), decode through the public API, result out
     q_host = q.cpu().pin_memory()
-    out_host = torch.empty((U, GQA, D), dtype=torch.float32).pin_memory()
     q_dev = torch.empty_like(q)
-    out = torch.empty((U, GQA, D), dtype=torch.float32, device=dev)
+    e2e_call = wl["e2e_call"]
+    out = e2e_call(q_dev)
+    out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
     for _ in range(max(3, args.warmup)):
         q_dev.copy_(q_host, non_blocking=True)
-        hs.decode_attention(q_dev, kc, vc, scale=scale, out=out)
+        out = e2e_call(q_dev)
         out_host.copy_(out, non_blocking=True)
     torch.cuda.synchronize()
     e_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -243,7 +322,7 @@ def run_ours(args):
         flush_l2()
         e_s[i].record()
         q_dev.copy_(q_host, non_blocking=True)
-        hs.decode_attention(q_dev, kc, vc, scale=scale, out=out)
+        out = e2e_call(q_dev)
         out_host.copy_(out, non_blocking=True)
         e_t[i].record()
     torch.cuda.synchronize()
@@ -251,11 +330,11 @@ def run_ours(args):
     e2e_value = total_bytes / (e2e_ms * 1e-3) / 1e9
 
     # ---- prefill (configs[2]): 32 q / 8 kv heads, 64K causal, S in {0,.25,.5,.75}
-    prefill = None if args.no_prefill else run_prefill(hs, dev, rank, args)
+    prefill = None if (args.no_prefill or args.workload != "config2") else run_prefill(hs, dev, rank, args)
 
     # ---- CPU baseline: the reference's decode on this host's cores (rank 0, N=1)
     cpu = None
-    if rank == 0 and world == 1 and not (args.skip_cpu or args.profile):
+    if rank == 0 and world == 1 and args.workload == "config2" and not (args.skip_cpu or args.profile):
         threads = min(16, os.cpu_count() or 1)
         units = list(range(U))
         kch, vch = host_caches(kc, units), host_caches(vc, units)
@@ -286,21 +365,20 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms_max, 5),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": wl["scaling"],
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (torch.randn, bf16), random-init; pools compressed on device",
-        "config": {"workload": "configs[1]: Llama-3.1-8B GQA decode, 32 q / 8 kv heads, d=128, 128K ctx, "
-                               "batch 1 per GPU, S_K=S_V=1 (2:4 K+V)",
-                   "kv_heads": U, "gqa": GQA, "context": L, "block_size": 64, "s_key": 1.0, "s_value": 1.0,
-                   "bytes_per_step_per_gpu": step_bytes, "parallelism": f"request-per-GPU x{world}",
-                   "l2": "flushed between timed steps (read of a 252 MB buffer); pools 302 MB > 126 MB L2"},
+        "config": dict(wl["config"], bytes_per_step_per_gpu=step_bytes,
+                       l2="flushed between timed steps (read of a 252 MB buffer)"),
         "decode_us": round(ms_max * 1e3, 2),
         "roofline": {"bound": "hbm", "achieved": round(per_gpu_gbs, 2), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(per_gpu_gbs / hbm_peak, 4), "traffic": traffic,
-                     "peak_kind": peak_kind, "kernel": "hs::decode_kernel (+fused split combine)"},
+                     "peak_kind": peak_kind, "kernel": "hs::decode_kernel (+fused split combine)"}
+        if args.workload == "config2" else None,
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "ms_per_step": round(e2e_ms, 5),
-                "h2d_bytes_per_step": int(q.numel() * 2), "d2h_bytes_per_step": int(out.numel() * 4)},
+                "h2d_bytes_per_step": int(q.numel() * 2), "d2h_bytes_per_step": int(out.numel() * 4),
+                "call": wl["e2e_name"]},
         "compress": {"ms": round(min(comp_ms), 4), "gbs": round(comp_bytes / (min(comp_ms) * 1e-3) / 1e9, 2),
                      "bytes": int(comp_bytes)},
         "gpu_launches": int(launches),
@@ -423,6 +501,8 @@ def main():
     ap.add_argument("--no-prefill", action="store_true", help="skip the configs[2] prefill leg")
     ap.add_argument("--prefill-ctx", type=int, default=65536)
     ap.add_argument("--prefill-steps", type=int, default=3)
+    ap.add_argument("--workload", default="config2", choices=["config2", "config4", "config5"],
+                    help="config2 (headline) | config4 batched KV-head sharding | config5 1M sequence split")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

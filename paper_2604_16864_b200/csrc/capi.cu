@@ -446,7 +446,7 @@ static hs_status decode_common(const void* q, const hs_device_cache* k, const hs
     L.v_nnz = v->nnz_pool;
     L.k_dense = k->dense_pool;
     L.v_dense = v->dense_pool;
-    L.prefetch_distance = 1;
+    L.prefetch_distance = 0;  // measured: L2 prefetch ahead of the TMA ring costs 3% (tools/tune_decode.py)
     if (const char* env = getenv("HS_DECODE_PF")) L.prefetch_distance = atoi(env);
     if (const char* env = getenv("HS_DECODE_DEBUG_STREAM_ONLY")) L.debug_stream_only = atoi(env);
     L.k_tail = k_tail;
@@ -472,9 +472,27 @@ static hs_status decode_common(const void* q, const hs_device_cache* k, const hs
     L.partial = reinterpret_cast<float*>(ws + cnt_bytes);
     L.out = out;
     L.out_mode = out_mode;
+    L.cta_times = nullptr;
+    static long long* times = nullptr;
+    const char* tpath = getenv("HS_DECODE_TIMES");  // tools: per-CTA timeline dump
+    if (tpath) {
+        if (!times) cudaMalloc(&times, 65536 * 8 * sizeof(long long));
+        cudaMemsetAsync(times, 0, 65536 * 8 * sizeof(long long), s);
+        L.cta_times = times;
+    }
     cudaError_t e = hs::launch_decode(L, s);
     count_launch();
     if (e != cudaSuccess) return cuda_fail(e, "decode launch");
+    if (tpath) {
+        const size_t n = static_cast<size_t>(L.n_units) * ns * 8;
+        std::vector<long long> host(n);
+        cudaStreamSynchronize(s);
+        cudaMemcpy(host.data(), times, n * sizeof(long long), cudaMemcpyDeviceToHost);
+        if (FILE* f = fopen(tpath, "wb")) {
+            fwrite(host.data(), sizeof(long long), n, f);
+            fclose(f);
+        }
+    }
     return HS_OK;
 }
 

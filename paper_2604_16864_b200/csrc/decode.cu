@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int split = blockIdx.x, u = blockIdx.y;
+    long long* const ct = L.cta_times ? L.cta_times + 8 * (static_cast<int64_t>(u) * gridDim.x + split) : nullptr;
+    if (ct && threadIdx.x == 0) ct[0] = globaltimer();
     const int gqa = L.gqa;
     // Block range of this CTA (attention.hpp:380-381 partition of [begin, end)).
     const int span = L.block_end - L.block_begin;
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
             const int i = warp + NW * k;
             const int s = warp * spw + k % spw;
             mbar_wait(&full_bar[s], (k / spw) & 1);
+            if (ct && k == 0 && threadIdx.x == 0) ct[1] = globaltimer();
             const bool kd = s_kidx[i] > 0, vd = s_vidx[i] > 0;
             if (L.debug_stream_only) {  // pipeline-only measurement mode (tools/)
                 __syncwarp();
@@ -359,6 +362,7 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
 
     // ---------------- merge warps (attention.hpp:387-407 formula) ----------------
     __syncthreads();  // all stages consumed; reuse the ring as scratch
+    if (ct && threadIdx.x == 0) ct[2] = globaltimer();
     float* s_o = reinterpret_cast<float*>(base_ptr);            // [NW][gqa][128]
     float* s_m = s_o + NW * kMaxGqa * kHeadDim;                 // [NW][gqa]
     float* s_l = s_m + NW * kMaxGqa;
@@ -401,28 +405,51 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
             part[qq * (kHeadDim + 2) + kHeadDim + 1] = acc;    // l
         }
     }
+    if (ct && threadIdx.x == 0) ct[3] = globaltimer();
     if (L.out == nullptr) return;
 
     // ---------------- last CTA of the unit combines all splits ----------------
     __threadfence();
+    if (ct && threadIdx.x == 0) ct[7] = globaltimer();
     __syncthreads();
     if (threadIdx.x == 0) s_ticket = atomicAdd(&L.counters[u], 1);
     __syncthreads();
     if (s_ticket != L.nsplit - 1) return;
+    if (ct && threadIdx.x == 0) ct[5] = globaltimer();
     __threadfence();
+    if (ct && threadIdx.x == 0) ct[6] = globaltimer();
     const float* P = L.partial + static_cast<int64_t>(u) * L.nsplit * stride_p;
     constexpr float kLog2e = 1.4426950408889634f;
+    // Streaming LSE merge in chunks of 32 splits: every load of a chunk (m, l
+    // and this thread's O column of each split) is independent, so a chunk costs
+    // one L2 round trip (configs[1] has 18 splits per unit: one chunk).
     for (int idx = threadIdx.x; idx < gqa * kHeadDim; idx += nthr) {
         const int qq = idx / kHeadDim, c = idx % kHeadDim;
-        float M = -INFINITY;
-        for (int sp = 0; sp < L.nsplit; ++sp) M = fmaxf(M, __ldcg(P + sp * stride_p + qq * (kHeadDim + 2) + kHeadDim));
-        float acc = 0.f, lsum = 0.f;
-        for (int sp = 0; sp < L.nsplit; ++sp) {
-            const float* ps = P + sp * stride_p + qq * (kHeadDim + 2);
-            const float ms = __ldcg(ps + kHeadDim);
-            const float wt = ms == -INFINITY ? 0.f : fast_exp2((ms - M) * kLog2e);
-            lsum += __ldcg(ps + kHeadDim + 1) * wt;
-            acc += __ldcg(ps + c) * wt;
+        const float* pq = P + qq * (kHeadDim + 2);
+        float M = -INFINITY, lsum = 0.f, acc = 0.f;
+        for (int sp0 = 0; sp0 < L.nsplit; sp0 += 32) {
+            float mv[32], lv[32], ov[32];
+#pragma unroll
+            for (int x = 0; x < 32; ++x) {
+                const bool ok = sp0 + x < L.nsplit;
+                const float* ps = pq + static_cast<int64_t>(sp0 + x) * stride_p;
+                mv[x] = ok ? __ldcg(ps + kHeadDim) : -INFINITY;
+                lv[x] = ok ? __ldcg(ps + kHeadDim + 1) : 0.f;
+                ov[x] = ok ? __ldcg(ps + c) : 0.f;
+            }
+            float mc = M;
+#pragma unroll
+            for (int x = 0; x < 32; ++x) mc = fmaxf(mc, mv[x]);
+            const float a = (M == -INFINITY) ? 0.f : fast_exp2((M - mc) * kLog2e);
+            lsum *= a;
+            acc *= a;
+#pragma unroll
+            for (int x = 0; x < 32; ++x) {
+                const float wt = mv[x] == -INFINITY ? 0.f : fast_exp2((mv[x] - mc) * kLog2e);
+                lsum += lv[x] * wt;
+                acc += ov[x] * wt;
+            }
+            M = mc;
         }
         if (L.out_mode == 0) {
             L.out[(static_cast<int64_t>(u) * gqa + qq) * kHeadDim + c] = acc / lsum;
@@ -436,6 +463,7 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
         }
     }
     if (threadIdx.x == 0) L.counters[u] = 0;
+    if (ct && threadIdx.x == 0) ct[4] = globaltimer();
 }
 
 // Standalone LSE combine of n_parts partials (cross-GPU sequence split).
@@ -502,7 +530,9 @@ size_t decode_smem_bytes(const DecodeLaunch& L, int* nw_out, int* spw_out, Stage
     if (spw < 1) spw = 1;
     size_t smem = static_cast<size_t>(NW * spw) * lay.stage_bytes;
     const size_t scratch = (NW * kMaxGqa * kHeadDim + 2 * NW * kMaxGqa) * sizeof(float);
+    const size_t combine = (2 * static_cast<size_t>(L.nsplit) * kMaxGqa + 2 * kMaxGqa) * sizeof(float);
     if (smem < scratch) smem = scratch;
+    if (smem < combine) smem = combine;
     smem += idx_bytes + 1024;
     *nw_out = NW;
     *spw_out = spw;

@@ -73,6 +73,7 @@ struct DecodeLaunch {
     float* out;              // fused combine target or nullptr (split partials only)
     int out_mode;            // 0: normalised [u][gqa][d]; 1: merged partial [u][gqa][d+2]
     int* counters;           // [u] arrival counters for the fused combine
+    long long* cta_times;    // tools only: [grid][5] globaltimer at start / first data / loop end / partial written / combine done
     CUtensorMap tm_knnz, tm_kden, tm_vnnz, tm_vden;
 };
 cudaError_t launch_decode(const DecodeLaunch& L, cudaStream_t s);

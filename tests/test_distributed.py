@@ -1,0 +1,95 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the multi-GPU partitioning:
+shard arithmetic (attention.hpp:380-381), the all-gather of SplitPartials in
+rank order, and the sequence-split decode they assemble, checked against the
+oracle's single-process decode_attention (attention.hpp:360-409)."""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2604_16864_b200 import distributed as D
+
+
+@pytest.mark.parametrize("n,world", [(2048, 8), (16384, 8), (7, 3), (64, 2), (1, 1), (5, 5)])
+def test_contiguous_shards_partition_the_range(n, world):
+    shards = [D.contiguous_shard(n, world, r) for r in range(world)]
+    assert shards[0].begin == 0 and shards[-1].end == n
+    for a, b in zip(shards, shards[1:]):
+        assert a.end == b.begin
+    assert sum(s.size for s in shards) == n
+    assert all(s == D.Shard(n * r // world, n * (r + 1) // world) for r, s in enumerate(shards))
+
+
+def test_head_and_unit_shards():
+    assert [D.heads_of_rank(8, 4, r) for r in range(4)] == [D.Shard(2 * r, 2 * r + 2) for r in range(4)]
+    with pytest.raises(ValueError):
+        D.heads_of_rank(8, 3, 0)
+    with pytest.raises(ValueError):
+        D.contiguous_shard(8, 2, 2)
+    # config 4: 32 requests x 8 KV heads over 8 ranks -> 32 units each
+    assert all(D.unit_shard(32, 8, 8, r).size == 32 for r in range(8))
+
+
+def _combine(parts):
+    """LSE combine of packed partials [P, rows, d+2] (attention.hpp:387-407)."""
+    o, m, l = parts[..., :-2], parts[..., -2], parts[..., -1]
+    mx = m.max(axis=0)
+    w = np.where(np.isfinite(m), np.exp(m - mx[None]), 0.0)
+    lt = (l * w).sum(axis=0)
+    return (o * w[..., None]).sum(axis=0) / lt[:, None]
+
+
+def _worker(rank, world, port_no, L, tail, ret):
+    import torch
+    import torch.distributed as dist
+    from oracle.oracle import Oracle, SparsityConfig
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        port = Oracle("port")
+        d, gqa, seed = 128, 4, 7
+        k = port.round_to(port.random_gaussian(L + tail, d, port.head_seed(seed, 0, 0)), "bf16")
+        v = port.round_to(port.random_gaussian(L + tail, d, port.head_seed(seed, 0, 1)), "bf16")
+        q = port.round_to(np.stack([port.random_gaussian(1, d, port.head_seed(seed, 0, 32 + g))[0]
+                                    for g in range(gqa)]), "bf16")
+        scale = np.float32(1 / math.sqrt(d))
+        nb = L // 64
+        sh = D.sequence_shard(nb, world, rank)
+        last = rank == world - 1
+        # this rank compresses only its own shard (S = 1: every block 2:4)
+        cfg = SparsityConfig(1.0, 1.0, 64)
+        ks = port.prune_compress(k[sh.begin * 64:sh.end * 64], cfg, 0, 1.0)
+        vs = port.prune_compress(v[sh.begin * 64:sh.end * 64], cfg, 1, 1.0)
+        kt, vt = (k[L:], v[L:]) if (last and tail) else (None, None)
+        out_t, m, l = port.attend_rows(q, ks, vs, kt, vt, 0, sh.size, last, scale)
+        partial = torch.from_numpy(np.concatenate([out_t.T, m[:, None], l[:, None]], axis=1))[None]
+        gathered = D.gather_partials(partial).numpy()  # [world, 1, gqa, d+2]
+        got = _combine(gathered[:, 0])
+        if rank == 0:
+            kf = port.prune_compress(k[:L], cfg, 0, 1.0)
+            vf = port.prune_compress(v[:L], cfg, 1, 1.0)
+            want = port.decode(q, kf, vf, k[L:] if tail else None, v[L:] if tail else None, scale, 1)
+            ret.put((float(np.abs(got - want).max()), gathered.shape))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("L,tail", [(4096, 0), (2048, 37)])
+def test_sequence_split_decode_two_ranks(L, tail):
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), L, tail, ret), nprocs=world, join=True,
+                       start_method="spawn")
+    err, shape = ret.get(timeout=60)
+    assert shape == (world, 1, 4, 130)
+    assert err < 1e-5, err

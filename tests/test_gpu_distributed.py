@@ -1,0 +1,71 @@
+"""GPU parity of the sequence-split decode (config 5) with the shards simulated
+on one device: each shard is compressed on its own (as its rank would), the
+per-shard SplitPartials (hs_decode_partial) are stacked in rank order and merged
+by hs_decode_combine; the result must match the oracle's decode_attention over
+the whole sequence (attention.hpp:360-409).  Also checks unit sharding: a rank's
+decode over its unit range equals the same rows of the all-unit decode."""
+import math
+
+import numpy as np
+import pytest
+
+from tests.helpers import MAX_ABS_TOL, MEAN_REL_TOL, device_to_oracle, err_stats, gen_units, to_torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hs():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2604_16864_b200 import hierasparse
+    return hierasparse
+
+
+@pytest.mark.parametrize("world,L,tail", [(2, 4096, 0), (4, 8192, 21), (8, 16384, 0)])
+def test_sequence_split_matches_whole_sequence(hs, port, world, L, tail):
+    import torch
+    from paper_2604_16864_b200 import distributed as D
+    U, gqa, d = 2, 4, 128
+    kx = gen_units(port, U, L + tail, d, 5, 0, "bf16")
+    vx = gen_units(port, U, L + tail, d, 5, 1, "bf16")
+    q = np.stack([port.round_to(np.stack([port.random_gaussian(1, d, port.head_seed(5, u, 32 + g))[0]
+                                          for g in range(gqa)]), "bf16") for u in range(U)])
+    scale = float(np.float32(1 / math.sqrt(d)))
+    cfg = hs.SparsityConfig(1.0, 1.0, 64)
+    nb = L // 64
+    parts = []
+    for r in range(world):
+        sh = D.sequence_shard(nb, world, r)
+        ks, vs = hs.prune_cache(to_torch(kx[:, sh.begin * 64:sh.end * 64], "bf16"),
+                                to_torch(vx[:, sh.begin * 64:sh.end * 64], "bf16"), cfg)
+        last = r == world - 1
+        kt = to_torch(kx[:, L:], "bf16") if (last and tail) else None
+        vt = to_torch(vx[:, L:], "bf16") if (last and tail) else None
+        parts.append(hs.decode_partial(to_torch(q, "bf16"), ks, vs, 0, sh.size, kt, vt, include_tail=last,
+                                       scale=scale))
+    got = hs.decode_combine(torch.stack(parts)).cpu().numpy()
+    kf, vf = hs.prune_cache(to_torch(kx[:, :L], "bf16"), to_torch(vx[:, :L], "bf16"), cfg)
+    want = np.stack([port.decode(q[u], device_to_oracle(kf, u), device_to_oracle(vf, u),
+                                 kx[u, L:] if tail else None, vx[u, L:] if tail else None, np.float32(scale), 1)
+                     for u in range(U)])
+    mx, mr = err_stats(got, want)
+    assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
+
+
+def test_unit_shards_equal_rows_of_full_decode(hs, port):
+    from paper_2604_16864_b200 import distributed as D
+    U, L, gqa, world = 8, 2048, 4, 4
+    kx = gen_units(port, U, L, 128, 9, 0, "f16")
+    vx = gen_units(port, U, L, 128, 9, 1, "f16")
+    q = np.stack([port.round_to(np.stack([port.random_gaussian(1, 128, port.head_seed(9, u, 32 + g))[0]
+                                          for g in range(gqa)]), "f16") for u in range(U)])
+    cfg = hs.SparsityConfig(0.5, 1.0, 64)
+    kc, vc = hs.prune_cache(to_torch(kx, "f16"), to_torch(vx, "f16"), cfg)
+    full = hs.decode_attention(to_torch(q, "f16"), kc, vc).cpu().numpy()
+    for r in range(world):
+        sh = D.unit_shard(1, U, world, r)
+        ks, vs = hs.prune_cache(to_torch(kx[sh.begin:sh.end], "f16"), to_torch(vx[sh.begin:sh.end], "f16"), cfg)
+        got = hs.decode_attention(to_torch(q[sh.begin:sh.end], "f16"), ks, vs).cpu().numpy()
+        mx, _ = err_stats(got, full[sh.begin:sh.end])
+        assert mx < 1e-5, (r, mx)

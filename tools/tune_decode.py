@@ -42,7 +42,7 @@ def run(splits=0, it=30):
     return statistics.median(ts), err
 
 
-variants = [(8, 1, 1), (4, 1, 2), (4, 2, 1)]
+variants = [(8, 1, 1), (4, 1, 2), (4, 2, 1), (4, 1, 3)]
 for pf in (0, 1, 2, 3, 4, 6, 8):
     os.environ["HS_DECODE_PF"] = str(pf)
     us, err = run()
@@ -59,6 +59,6 @@ for w, c, s in variants:
         print(f"warps={w} ctas/sm={c} spw={s}: failed {e}", flush=True)
 for k in ("HS_DECODE_WARPS", "HS_DECODE_CTAS_PER_SM", "HS_DECODE_SPW"):
     os.environ.pop(k, None)
-for splits in (9, 18, 36, 37, 74):
+for splits in (9, 18, 19, 36, 37, 74):
     us, err = run(splits)
     print(f"default splits={splits}: {us:8.2f} us  {nbytes / us / 1e3:8.1f} GB/s", flush=True)
