@@ -119,3 +119,17 @@ def test_closed_form_flop_count_matches_oracle(port):
         kd = kf if (kc.sparse_count and kc.dense_count) else [int(kc.sparse_count == 0)] * nb
         vd = vf if (vc.sparse_count and vc.dense_count) else [int(vc.sparse_count == 0)] * nb
         assert flop_count(kd, vd, B, d, n_q, tail, causal) == want, it
+
+
+def test_cpp_header_is_standalone():
+    """include/hierasparse_b200.hpp compiles on its own (no reference headers)."""
+    import shutil
+    import subprocess
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("no g++")
+    inc = os.path.join(ROOT, "include")
+    src = '#include "hierasparse_b200.hpp"\nint main() { hierasparse::b200::SparsityConfig c; return (int)c.block_size - 64; }\n'
+    out = subprocess.run([gxx, "-std=c++17", "-fsyntax-only", "-I", inc, "-I", "/usr/local/cuda/include", "-x", "c++",
+                          "-"], input=src, capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
