@@ -40,6 +40,35 @@ __device__ __forceinline__ uint32_t group_code(uint32_t keep, uint32_t& p0, uint
     return p0 | (p1 << 2);
 }
 
+// Top-2-of-4 of one group given as two packed words (lo = g0 | g1 << 16,
+// hi = g2 | g3 << 16), branch-free.  Keys (|g_i| << 2) | (3 - i) are distinct
+// and order exactly like the reference's stable descending sort (larger
+// magnitude first, ties to the lower index, pruner.hpp:63-66), so a 4-element
+// min/max network yields the two kept positions (canonical code, first kept
+// index in the low 2 bits, nm_metadata.hpp:42-46), the kept pair packed by one
+// byte permute, and the two pruned magnitudes straight from the low keys.
+struct Sel2of4 {
+    uint32_t code;   // p0 | p1 << 2, p0 < p1
+    uint32_t kept;   // g[p0] | g[p1] << 16
+    uint32_t pr_lo;  // magnitude bits of the smaller pruned element
+    uint32_t pr_hi;  // magnitude bits of the larger pruned element
+};
+__device__ __forceinline__ Sel2of4 select2of4(uint32_t lo, uint32_t hi) {
+    const uint32_t k0 = ((lo & 0x7FFFu) << 2) | 3u, k1 = ((lo >> 14) & 0x1FFFCu) | 2u;
+    const uint32_t k2 = ((hi & 0x7FFFu) << 2) | 1u, k3 = (hi >> 14) & 0x1FFFCu;
+    const uint32_t a = max(k0, k1), b = min(k0, k1), c = max(k2, k3), d = min(k2, k3);
+    const uint32_t t1 = max(a, c), t2 = max(min(a, c), max(b, d));
+    const uint32_t b1 = min(b, d), b2 = min(max(b, d), min(a, c));
+    const uint32_t pa = 3u - (t1 & 3u), pb = 3u - (t2 & 3u);
+    const uint32_t p0 = min(pa, pb), p1 = max(pa, pb);
+    Sel2of4 r;
+    r.code = p0 | (p1 << 2);
+    r.kept = __byte_perm(lo, hi, 0x1010u + p0 * 0x22u + p1 * 0x2200u);
+    r.pr_lo = b1 >> 2;
+    r.pr_hi = b2 >> 2;
+    return r;
+}
+
 // Exact-loss bookkeeping.  Every 16-bit float is M * 2^e with integer M below
 // 2^(mant+1); a double sum of such terms is exact in any order while the total
 // stays below 2^(53 + e_min), and then equals the reference's sequential double
@@ -66,6 +95,19 @@ __device__ __forceinline__ void loss_add(LossAcc& a, uint16_t bits) {
     a.emin = min(a.emin, e);
     a.emax = max(a.emax, e);
     a.sum += fabs(static_cast<double>(F16Traits<T>::to_float(bits)));
+}
+
+// Both pruned elements of a group (magnitude bits, lo <= hi): exponents tracked
+// as max(E, 1) of the nonzero terms (same differences as the unit exponents).
+template <typename T>
+__device__ __forceinline__ void loss_add_pair(LossAcc& a, uint32_t lo, uint32_t hi) {
+    constexpr int mant = F16Traits<T>::kMantBits;
+    const int eh = hi ? max(static_cast<int>(hi >> mant), 1) : -(1 << 20);
+    const int el = lo ? max(static_cast<int>(lo >> mant), 1) : (hi ? eh : (1 << 20));
+    a.emin = min(a.emin, el);
+    a.emax = max(a.emax, eh);
+    a.sum += static_cast<double>(F16Traits<T>::to_float(static_cast<uint16_t>(lo))) +
+             static_cast<double>(F16Traits<T>::to_float(static_cast<uint16_t>(hi)));
 }
 
 // Reduce LossAcc across the CTA; thread 0 gets the totals.  Returns true on
@@ -181,30 +223,16 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
                 *reinterpret_cast<uint4*>(dst + r * kHeadDim + c * 8) = v;
             }
             if (MODE == 1 && dense) continue;
-            const uint16_t x[8] = {
-                (uint16_t)(v.x & 0xFFFF), (uint16_t)(v.x >> 16), (uint16_t)(v.y & 0xFFFF), (uint16_t)(v.y >> 16),
-                (uint16_t)(v.z & 0xFFFF), (uint16_t)(v.z >> 16), (uint16_t)(v.w & 0xFFFF), (uint16_t)(v.w >> 16)};
-            uint32_t kept_vals[4];
-            uint32_t meta_byte = 0;
-#pragma unroll
-            for (int gi = 0; gi < 2; ++gi) {
-                const uint16_t* g = x + 4 * gi;
-                const uint32_t keep = keep_mask4(mag16(g[0]), mag16(g[1]), mag16(g[2]), mag16(g[3]));
-                uint32_t p0, p1;
-                meta_byte |= group_code(keep, p0, p1) << (4 * gi);
-                kept_vals[2 * gi] = pick4(g[0], g[1], g[2], g[3], p0);
-                kept_vals[2 * gi + 1] = pick4(g[0], g[1], g[2], g[3], p1);
-                if (kLoss) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (!((keep >> i) & 1u)) loss_add<T>(acc, g[i]);
-                }
+            const Sel2of4 s0 = select2of4(v.x, v.y), s1 = select2of4(v.z, v.w);
+            const uint32_t meta_byte = s0.code | (s1.code << 4);
+            if (kLoss) {
+                loss_add_pair<T>(acc, s0.pr_lo, s0.pr_hi);
+                loss_add_pair<T>(acc, s1.pr_lo, s1.pr_hi);
             }
             if (MODE != 0 && !dense) {
                 const uint64_t sb = static_cast<uint64_t>(u) * a.sparse_count + slot;
                 uint16_t* nnz = a.nnz_pool + sb * (kBlock * kHeadDim / 2);
-                *reinterpret_cast<uint2*>(nnz + r * (kHeadDim / 2) + c * 4) =
-                    make_uint2(kept_vals[0] | (kept_vals[1] << 16), kept_vals[2] | (kept_vals[3] << 16));
+                *reinterpret_cast<uint2*>(nnz + r * (kHeadDim / 2) + c * 4) = make_uint2(s0.kept, s1.kept);
                 uint8_t* meta = reinterpret_cast<uint8_t*>(a.meta_pool + sb * (kBlock * kHeadDim / 16));
                 meta[r * (kHeadDim / 8) + c] = static_cast<uint8_t>(meta_byte);
             }
@@ -240,18 +268,12 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
 #pragma unroll
             for (int gi = 0; gi < 8; ++gi) {
                 const int r0 = 32 * h + 4 * gi;
-                uint16_t g[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) g[i] = tile[(r0 + i) * kHeadDim + c];
-                const uint32_t keep = keep_mask4(mag16(g[0]), mag16(g[1]), mag16(g[2]), mag16(g[3]));
-                uint32_t p0, p1;
-                meta |= group_code(keep, p0, p1) << (4 * gi);
-                vals[gi] = pick4(g[0], g[1], g[2], g[3], p0) | (pick4(g[0], g[1], g[2], g[3], p1) << 16);
-                if (kLoss) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (!((keep >> i) & 1u)) loss_add<T>(acc, g[i]);
-                }
+                const uint32_t lo = tile[r0 * kHeadDim + c] | (static_cast<uint32_t>(tile[(r0 + 1) * kHeadDim + c]) << 16);
+                const uint32_t hi = tile[(r0 + 2) * kHeadDim + c] | (static_cast<uint32_t>(tile[(r0 + 3) * kHeadDim + c]) << 16);
+                const Sel2of4 sg = select2of4(lo, hi);
+                meta |= sg.code << (4 * gi);
+                vals[gi] = sg.kept;
+                if (kLoss) loss_add_pair<T>(acc, sg.pr_lo, sg.pr_hi);
             }
             if (MODE != 0 && !dense) {
                 const uint64_t sb = static_cast<uint64_t>(u) * a.sparse_count + slot;
