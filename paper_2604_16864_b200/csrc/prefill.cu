@@ -84,7 +84,11 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
 // TMEM -> registers: this warp's 32 lanes x N consecutive 32-bit columns.
 template <int N>
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
-    if constexpr (N == 16) {
+    if constexpr (N == 8) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                     : "r"(taddr));
+    } else if constexpr (N == 16) {
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
@@ -94,6 +98,21 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
 #pragma unroll
         for (int c = 0; c < N; c += 32) tmem_ld32(taddr + c, *reinterpret_cast<uint32_t(*)[32]>(&r[c]));
     }
+}
+
+#ifndef HS_PREFILL_EXP_F16X2
+#define HS_PREFILL_EXP_F16X2 0  // sm_100a splits f16x2 ex2 into two MUFU ops: no gain
+#endif
+constexpr bool kExpF16x2 = HS_PREFILL_EXP_F16X2 != 0;
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ uint32_t ex2_f16x2(uint32_t x) {
+    uint32_t r;
+    asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
 }
 
 // Barrier over `n` threads of named barrier `id` that also ORs a predicate.
@@ -160,9 +179,13 @@ __global__ void __launch_bounds__(128) meta_atom_kernel(const uint16_t* __restri
     }
 }
 
-template <typename T, bool HILO>
+template <typename T, bool HILO, bool DBG>
 __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_constant__ PrefillLaunch L,
                                                                PrefillLayout lay) {
+    // DBG: tools-only instrumentation (per-tile trace, watchdog waits, mode
+    // switches); the production instantiation compiles all of it out.
+    int* const dbgp = DBG ? L.dbg : nullptr;
+    const int mode = DBG ? L.mode : 0;
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bar_q, bar_kfull[4], bar_kempty[4];
     __shared__ __align__(8) uint64_t bar_vfull[4], bar_vempty[4];
@@ -303,8 +326,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             const int s = t % nk;
             const TileInfo ti = s_tiles[t];
             const int ke0 = uni(ti.ke0), two = uni(ti.ve1 != 0);
-            mbar_wait_dbg(&bar_kempty[s], ((t / nk) & 1) ^ 1, L.dbg, 4);
-            if (lane == 0) trace(L, t, 7);
+            mbar_wait_dbg(&bar_kempty[s], ((t / nk) & 1) ^ 1, dbgp, 4);
+            if (DBG && lane == 0) trace(L, t, 7);
             if (elect_one()) {
                 uint8_t* st = base_ptr + lay.off_k + s * lay.k_stage;
                 // both blocks (consecutive slots) in one 128-row box per column half
@@ -327,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             const int s = t % nv;
             const TileInfo ti = s_tiles[t];
             const int ve0 = uni(ti.ve0), ve1 = uni(ti.ve1);
-            mbar_wait_dbg(&bar_vempty[s], ((t / nv) & 1) ^ 1, L.dbg, 4);
+            mbar_wait_dbg(&bar_vempty[s], ((t / nv) & 1) ^ 1, dbgp, 4);
             if (elect_one()) {
                 uint8_t* st = base_ptr + lay.off_v + s * lay.v_stage;
                 const int nb_t = ve1 != 0 ? 2 : 1;
@@ -368,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         const uint32_t id_g1_de = umma_idesc_f16(bf, 128, 128, false, false, false);
         const uint32_t id_g2_sp = umma_idesc_f16(bf, 128, 128, false, true, true);
         const uint32_t id_g2_de = umma_idesc_f16(bf, 128, 128, false, true, false);
-        mbar_wait_dbg(&bar_q, 0, L.dbg, 1);
+        mbar_wait_dbg(&bar_q, 0, dbgp, 1);
         tc_fence_after();
         // Descriptor bases (start address in 16-byte units in the low 14 bits:
         // adding (bytes >> 4) advances the start address).
@@ -386,12 +409,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             const int s = tp % nv;
             const TileInfo ti = s_tiles[tp];
             const int ve0 = uni(ti.ve0), ve1 = uni(ti.ve1);
-            mbar_wait_dbg(&bar_vfull[s], (tp / nv) & 1, L.dbg, 3);
-            mbar_wait_dbg(&bar_pfull[pbuf_of(tp)], pphase(tp), L.dbg, 7);
+            mbar_wait_dbg(&bar_vfull[s], (tp / nv) & 1, dbgp, 3);
+            mbar_wait_dbg(&bar_pfull[pbuf_of(tp)], pphase(tp), dbgp, 7);
             tc_fence_after();
-            if (lane == 0) trace(L, tp, 5);
+            if (DBG && lane == 0) trace(L, tp, 5);
             if (elect_one()) {
-                const int nb_t = (L.mode & 2) ? 0 : ve1 != 0 ? 2 : 1;
+                const int nb_t = (mode & 2) ? 0 : ve1 != 0 ? 2 : 1;
                 const uint64_t so = static_cast<uint64_t>(s) * vst16;
                 if (ve0 < 0) tmem_cp_128x128b(tEV + 8 * (tp & 1), dEV + so);
                 if (ve1 < 0) tmem_cp_128x128b(tEV + 8 * (tp & 1) + 4, dEV + so + 128);
@@ -421,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             }
             __syncwarp();
             o_started = true;
-            if (lane == 0) trace(L, tp, 6);
+            if (DBG && lane == 0) trace(L, tp, 6);
         };
         if (warp_u == kWarpMma2) {
             for (int tp = 0; tp < ntiles; ++tp) gemm2(tp);
@@ -430,19 +453,19 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             const int s = t % nk, sb = t & 1;
             const TileInfo ti = s_tiles[t];
             const int ke0 = uni(ti.ke0);
-            if (lane == 0) trace(L, t, 11);
-            mbar_wait_dbg(&bar_kfull[s], (t / nk) & 1, L.dbg, 3);  // K tile + metadata atom landed
-            if (lane == 0) trace(L, t, 10);
-            if (t >= 2) mbar_wait_dbg(&bar_sempty[sb], ((t >> 1) - 1) & 1, L.dbg, 6);
+            if (DBG && lane == 0) trace(L, t, 11);
+            mbar_wait_dbg(&bar_kfull[s], (t / nk) & 1, dbgp, 3);  // K tile + metadata atom landed
+            if (DBG && lane == 0) trace(L, t, 10);
+            if (t >= 2) mbar_wait_dbg(&bar_sempty[sb], ((t >> 1) - 1) & 1, dbgp, 6);
             tc_fence_after();
-            if (lane == 0) trace(L, t, 4);
+            if (DBG && lane == 0) trace(L, t, 4);
             if (elect_one()) {
                 const uint64_t so = static_cast<uint64_t>(s) * kst16;
                 // metadata -> TMEM (ordered before the MMAs that read it)
                 if (ke0 < 0) tmem_cp_128x128b(tEK + 4 * sb, dEK + so);
                 // GEMM1: S^T[sb] = K_tile * Q^T
                 const uint32_t tS = tS0 + 128 * sb;
-                if (L.mode & 2) {
+                if (mode & 2) {
                 } else if (ke0 > 0) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
@@ -485,11 +508,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         for (int t = 0; t < ntiles; ++t) {
             const int sb = t & 1;
             const TileInfo ti = s_tiles[t];
-            mbar_wait_dbg(&bar_sfull[sb], (t >> 1) & 1, L.dbg, 5);
+            mbar_wait_dbg(&bar_sfull[sb], (t >> 1) & 1, dbgp, 5);
             tc_fence_after();
-            if (tid == 0) trace(L, t, 0);
-            if (L.mode & 1) {  // tools: pipeline without the softmax
-                if (t >= npb) mbar_wait_dbg(&bar_pempty[pbuf_of(t)], pphase(t - npb), L.dbg, 8);
+            if (DBG && tid == 0) trace(L, t, 0);
+            if (mode & 1) {  // tools: pipeline without the softmax
+                if (t >= npb) mbar_wait_dbg(&bar_pempty[pbuf_of(t)], pphase(t - npb), dbgp, 8);
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&bar_sempty[sb]);
@@ -568,20 +591,22 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 }
                 if (resc) {
                     // O^T (GEMM2(t-1) complete) and l rescale for the grown columns
-                    if (t >= 1) mbar_wait_dbg(&bar_pempty[pbuf_of(t - 1)], pphase(t - 1), L.dbg, 8);
+                    if (t >= 1) mbar_wait_dbg(&bar_pempty[pbuf_of(t - 1)], pphase(t - 1), dbgp, 8);
                     tc_fence_after();
 #pragma unroll
                     for (int k = 0; k < kCols; ++k) l_part[k] *= s_alpha[c0 + k];
                     if (t >= 1) {
-                        uint32_t v[kCols];
-                        tmem_ld_cols<kCols>(tO + lane_off + c0, v);
-                        tmem_ld_wait();
+#pragma unroll 1
+                        for (int k8 = 0; k8 < kCols; k8 += 8) {  // 8 columns at a time: low register pressure
+                            uint32_t v[8];
+                            tmem_ld_cols<8>(tO + lane_off + c0 + k8, v);
+                            tmem_ld_wait();
 #pragma unroll
-                        for (int k = 0; k < kCols; ++k)
-                            v[k] = __float_as_uint(__uint_as_float(v[k]) * s_alpha[c0 + k]);
-#pragma unroll
-                        for (int k = 0; k < kCols; k += 4)
-                            tmem_st4(tO + lane_off + c0 + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
+                            for (int k = 0; k < 8; ++k)
+                                v[k] = __float_as_uint(__uint_as_float(v[k]) * s_alpha[c0 + k8 + k]);
+                            tmem_st4(tO + lane_off + c0 + k8, v[0], v[1], v[2], v[3]);
+                            tmem_st4(tO + lane_off + c0 + k8 + 4, v[4], v[5], v[6], v[7]);
+                        }
                         tmem_st_wait();
                     }
                 }
@@ -590,15 +615,30 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_sempty[sb]);  // this warp is done with S^T[sb]
-            if (tid == 0) trace(L, t, 1);
+            if (DBG && tid == 0) trace(L, t, 1);
             // P^T buffer free (GEMM2 of its previous tile complete)
-            if (t >= npb) mbar_wait_dbg(&bar_pempty[pbuf_of(t)], pphase(t - npb), L.dbg, 8);
-            if (tid == 0) trace(L, t, 2);
+            if (t >= npb) mbar_wait_dbg(&bar_pempty[pbuf_of(t)], pphase(t - npb), dbgp, 8);
+            if (DBG && tid == 0) trace(L, t, 2);
             // probabilities, partial column sums, P^T (+ residual for bf16)
             uint8_t* const pbuf = pbuf0 + pbuf_of(t) * lay.p_bytes;
 #pragma unroll
             for (int g8 = 0; g8 < kCols / 8; ++g8) {
                 const int q8 = (c0 >> 3) + g8;  // 8-query chunk index in 0..15
+                if constexpr (!HILO && kExpF16x2) {
+                    // fp16 P: two exponentials per MUFU op (ex2.approx.f16x2 on x
+                    // rounded to fp16; x <= tau keeps the argument error small where
+                    // P is large), the packed result is the stored P^T chunk.
+                    uint32_t ph[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        ph[k] = ex2_f16x2(pack_f16x2(x[8 * g8 + 2 * k], x[8 * g8 + 2 * k + 1]));
+                        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&ph[k]));
+                        l_part[8 * g8 + 2 * k] += f.x;
+                        l_part[8 * g8 + 2 * k + 1] += f.y;
+                    }
+                    *reinterpret_cast<uint4*>(pbuf + pt_chunk_off(r, q8)) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+                    continue;
+                }
                 float p[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
@@ -621,17 +661,17 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     *reinterpret_cast<uint4*>(pbuf + 32768 + pt_chunk_off(r, q8)) = lo;
                 }
             }
-            if (tid == 0) trace(L, t, 3);
+            if (DBG && tid == 0) trace(L, t, 3);
             fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_pfull[pbuf_of(t)]);
         }
         // ---------------------------------------------------- epilogue ----
-        if (ntiles > 0) mbar_wait_dbg(&bar_pempty[pbuf_of(ntiles - 1)], pphase(ntiles - 1), L.dbg, 8);
+        if (ntiles > 0) mbar_wait_dbg(&bar_pempty[pbuf_of(ntiles - 1)], pphase(ntiles - 1), dbgp, 8);
         tc_fence_after();
         // l[c] = sum over the 128 key lanes of l_part[c]: transpose through smem
-        // (the K ring is free: every GEMM has completed)
-        float* s_l = reinterpret_cast<float*>(base_ptr + lay.off_k) + wg * (128 * (kCols + 1));
+        // (P^T buffers and the K ring are free: every GEMM has completed)
+        float* s_l = reinterpret_cast<float*>(base_ptr + lay.off_p) + wg * (128 * (kCols + 1));
 #pragma unroll
         for (int c = 0; c < kCols; ++c) s_l[r * (kCols + 1) + c] = l_part[c];
         named_bar(bar_id, 128);
@@ -683,8 +723,11 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     const uint32_t budget = 227u * 1024u - 8192u /*static smem*/ - 1024u /*align*/ - tiles_bytes;
     // Preference order: 2 K + 2 V stages with two P^T buffers, then fewer P^T
     // buffers, then shallower rings.
-    const uint32_t plans[][3] = {{2, 3, 3}, {2, 2, 3}, {2, 3, 2}, {2, 2, 2}, {1, 2, 2}, {2, 2, 1}, {2, 1, 2},
-                                 {1, 2, 1}, {1, 1, 2}, {1, 1, 1}};
+    // V(t) is consumed a softmax period after K(t), so one V stage is enough to
+    // keep two P^T buffers (softmax(t+1) never waits for GEMM2(t)) when dense
+    // tiles leave no room for both.
+    const uint32_t plans[][3] = {{2, 3, 3}, {2, 2, 3}, {2, 3, 2}, {2, 2, 2}, {2, 3, 1}, {2, 2, 1}, {1, 2, 2},
+                                 {2, 1, 2}, {1, 2, 1}, {1, 1, 2}, {1, 1, 1}};
     bool ok = false;
     for (const auto& pl : plans) {
         const uint32_t need = 32768u + pl[0] * lay.p_bytes + pl[1] * lay.k_stage + pl[2] * lay.v_stage;
@@ -709,7 +752,7 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     lay.off_v = lay.off_k + lay.nk * lay.k_stage;
     lay.off_tiles = lay.off_v + lay.nv * lay.v_stage;
     size_t smem = lay.off_tiles + tiles_bytes + 1024;
-    const size_t epi = lay.off_k + kSoftWG * 128 * (kCols + 1) * 4 + 1024;
+    const size_t epi = lay.off_p + kSoftWG * 128 * (kCols + 1) * 4 + 1024;
     if (smem < epi) smem = epi;
     {
         const int kb = L.n_units * L.k_sparse_count, vb = L.n_units * L.v_sparse_count;
@@ -720,17 +763,17 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
         }
     }
     const dim3 grid((L.n_q + 127) / 128, L.gqa, L.n_units);
-    if (L.bf16) {
-        auto k = prefill_kernel<__nv_bfloat16, true>;
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool dbg = L.trace != nullptr || L.dbg != nullptr || L.mode != 0;
+    auto launch = [&](auto kern) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e) return e;
-        k<<<grid, kThreads, smem, s>>>(L, lay);
-    } else {
-        auto k = prefill_kernel<__half, false>;
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e) return e;
-        k<<<grid, kThreads, smem, s>>>(L, lay);
-    }
+        kern<<<grid, kThreads, smem, s>>>(L, lay);
+        return cudaSuccess;
+    };
+    cudaError_t e;
+    if (L.bf16) e = dbg ? launch(prefill_kernel<__nv_bfloat16, true, true>) : launch(prefill_kernel<__nv_bfloat16, true, false>);
+    else e = dbg ? launch(prefill_kernel<__half, false, true>) : launch(prefill_kernel<__half, false, false>);
+    if (e) return e;
     return cudaGetLastError();
 }
 
