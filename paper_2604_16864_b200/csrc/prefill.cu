@@ -100,6 +100,26 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
     }
 }
 
+// Blackwell packed fp32: (x0, x1) <- (x0, x1) * b + (c0, c1) in one FFMA2.
+__device__ __forceinline__ void ffma2(float& x0, float& x1, float b, float c0, float c1) {
+    asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%0, %1};\n\tmov.b64 rb, {%2, %2};\n\t"
+        "mov.b64 rc, {%3, %4};\n\tfma.rn.f32x2 ra, ra, rb, rc;\n\tmov.b64 {%0, %1}, ra;\n\t}"
+        : "+f"(x0), "+f"(x1)
+        : "f"(b), "f"(c0), "f"(c1));
+}
+// (a0, a1) += (b0, b1) in one FADD2.
+__device__ __forceinline__ void fadd2(float& a0, float& a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb;\n\tmov.b64 ra, {%0, %1};\n\tmov.b64 rb, {%2, %3};\n\t"
+        "add.rn.f32x2 ra, ra, rb;\n\tmov.b64 {%0, %1}, ra;\n\t}"
+        : "+f"(a0), "+f"(a1)
+        : "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
 #ifndef HS_PREFILL_EXP_F16X2
 #define HS_PREFILL_EXP_F16X2 0  // sm_100a splits f16x2 ex2 into two MUFU ops: no gain
 #endif
@@ -193,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     __shared__ uint32_t s_tmem;
     __shared__ int s_ntiles;
     __shared__ float s_red[4][128];
-    __shared__ float s_mnew[128], s_alpha[128], s_mrun[128];
+    __shared__ float s_mnew[128], s_alpha[128], s_mrun[128], s_mneg[128];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     const int n_tiles_q = (L.n_q + 127) / 128;
@@ -501,7 +521,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         float l_part[kCols];
 #pragma unroll
         for (int c = 0; c < kCols; ++c) l_part[c] = 0.f;
-        if (r < kCols) s_mrun[c0 + r] = -INFINITY;
+        if (r < kCols) {
+            s_mrun[c0 + r] = -INFINITY;
+            s_mneg[c0 + r] = INFINITY;  // -m, the FMA addend of the fast path
+        }
         named_bar(bar_id, 128);
         uint8_t* const pbuf0 = base_ptr + lay.off_p;
         const float sl2 = L.scale_log2;
@@ -538,23 +561,22 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             // warp-uniform fast path: every (row, column) of this warp visible
             const bool fast = __all_sync(0xffffffffu, c_first <= c0);
             // x <- s*scale*log2e - m (masked: -inf); does any value exceed m + tau?
+            // (packed f32x2 FMA against -m, 3-input max: half the instructions)
 #pragma unroll
             for (int k = 0; k < kCols; k += 4) {
-                const float4 m4 = *reinterpret_cast<const float4*>(&s_mrun[c0 + k]);
-                x[k] = fmaf(x[k], sl2, -m4.x);
-                x[k + 1] = fmaf(x[k + 1], sl2, -m4.y);
-                x[k + 2] = fmaf(x[k + 2], sl2, -m4.z);
-                x[k + 3] = fmaf(x[k + 3], sl2, -m4.w);
+                const float4 n4 = *reinterpret_cast<const float4*>(&s_mneg[c0 + k]);
+                ffma2(x[k], x[k + 1], sl2, n4.x, n4.y);
+                ffma2(x[k + 2], x[k + 3], sl2, n4.z, n4.w);
             }
             if (!fast) {
 #pragma unroll
                 for (int k = 0; k < kCols; ++k)
                     if (c0 + k < c_first) x[k] = -INFINITY;
             }
-            float xmax = -INFINITY;
+            float xmax = max3f(x[0], x[1], x[2]);
 #pragma unroll
-            for (int k = 0; k < kCols; k += 4)
-                xmax = fmaxf(fmaxf(xmax, fmaxf(x[k], x[k + 1])), fmaxf(x[k + 2], x[k + 3]));
+            for (int k = 3; k + 1 < kCols; k += 2) xmax = max3f(xmax, x[k], x[k + 1]);
+            if constexpr (kCols % 2 == 0) xmax = fmaxf(xmax, x[kCols - 1]);
             if (bar_red_or(bar_id, !(xmax <= kTau))) {
                 // ---- slow path (!(xmax <= tau) also catches a NaN from m = -inf)
                 load_s();
@@ -582,7 +604,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     s_alpha[c] = alpha;
                 }
                 resc = bar_red_or(bar_id, resc);
-                if (r < kCols) s_mrun[c0 + r] = s_mnew[c0 + r];
+                if (r < kCols) {
+                    s_mrun[c0 + r] = s_mnew[c0 + r];
+                    s_mneg[c0 + r] = -s_mnew[c0 + r];
+                }
                 // x <- x - m_new (masked stay -inf; columns with no visible key yet stay -inf)
 #pragma unroll
                 for (int k = 0; k < kCols; ++k) {
@@ -641,10 +666,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 }
                 float p[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    p[k] = fast_exp2(x[8 * g8 + k]);  // exp2(-inf) = 0
-                    l_part[8 * g8 + k] += p[k];
-                }
+                for (int k = 0; k < 8; ++k) p[k] = fast_exp2(x[8 * g8 + k]);  // exp2(-inf) = 0
+#pragma unroll
+                for (int k = 0; k < 8; k += 2) fadd2(l_part[8 * g8 + k], l_part[8 * g8 + k + 1], p[k], p[k + 1]);
                 const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
                                             F16Traits<T>::pack(p[4], p[5]), F16Traits<T>::pack(p[6], p[7]));
                 *reinterpret_cast<uint4*>(pbuf + pt_chunk_off(r, q8)) = hi;
