@@ -12,7 +12,7 @@ import os
 from .errors import ConfigError, CudaError, DataError, IoError
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libhierasparse_b200.so")
+LIB_PATH = os.environ.get("HS_LIB") or os.path.join(PKG, "lib", "libhierasparse_b200.so")  # HS_LIB: A/B tooling
 
 HS_OK, HS_ERR_CONFIG, HS_ERR_IO, HS_ERR_DATA, HS_ERR_CUDA = 0, 2, 3, 4, 5
 DTYPE_BF16, DTYPE_F16 = 0, 1
