@@ -40,7 +40,8 @@ def _stale() -> bool:
 def _compile(src: str) -> tuple[str, str]:
     obj = os.path.join(LIBDIR, "obj", os.path.basename(src) + ".o")
     os.makedirs(os.path.dirname(obj), exist_ok=True)
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    extra = os.environ.get("HS_NVCC_FLAGS", "").split()  # tools: variant builds for A/B timing
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
     out = subprocess.run(cmd, capture_output=True, text=True)
     if out.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{out.stderr}")
