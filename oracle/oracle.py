@@ -360,3 +360,28 @@ class Oracle:
 
 def available(kind: str) -> bool:
     return os.path.exists(PORT_SO if kind == "port" else REF_SO)
+
+
+def ref_serialize(c: CompressedCache) -> bytes:
+    """The reference's serialize (container.hpp:119-148) of one cache (oracle/_ref only)."""
+    ref = Oracle("reference")
+    ref.lib.ref_serialize.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
+    n = C.c_size_t()
+    cs = c._c()
+    ref._check(ref.lib.ref_serialize(C.byref(cs), None, 0, C.byref(n)))
+    buf = (C.c_uint8 * n.value)()
+    cs = c._c()
+    ref._check(ref.lib.ref_serialize(C.byref(cs), buf, n.value, C.byref(n)))
+    return bytes(buf)
+
+
+def ref_parse(data: bytes):
+    """The reference's parse (container.hpp:150-250): (rc, message, (nb, dense, sparse))."""
+    ref = Oracle("reference")
+    ref.lib.ref_parse.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                                  C.POINTER(C.c_size_t)]
+    a, b, c = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    buf = (C.c_uint8 * len(data)).from_buffer_copy(data)
+    rc = ref.lib.ref_parse(buf, len(data), C.byref(a), C.byref(b), C.byref(c))
+    msg = ref.lib.ref_last_error().decode() if rc else ""
+    return rc, msg, (a.value, b.value, c.value)

@@ -239,4 +239,27 @@ int ref_flop_and_byte_count(size_t n_q, size_t d, const hso_cache* k, const hso_
     });
 }
 
+// serialize (container.hpp:119-148): bytes of one cache; *len = size (call with
+// out = NULL to size the buffer).
+int ref_serialize(const hso_cache* c, uint8_t* out, size_t cap, size_t* len) {
+    return guarded([&] {
+        const std::vector<std::uint8_t> b = serialize(to_cache(c));
+        *len = b.size();
+        if (out != nullptr && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+    });
+}
+
+// parse (container.hpp:150-250): 0 when the bytes are a valid container, the
+// reference's error code otherwise (DataError -> 4); decoded geometry out.
+int ref_parse(const uint8_t* bytes, size_t len, size_t* logical_blocks, size_t* dense_count,
+              size_t* sparse_count) {
+    return guarded([&] {
+        const std::vector<std::uint8_t> b(bytes, bytes + len);
+        const CompressedCache c = parse(b);
+        *logical_blocks = c.logical_blocks;
+        *dense_count = c.dense_count;
+        *sparse_count = c.sparse_count;
+    });
+}
+
 }  // extern "C"
