@@ -197,6 +197,24 @@ def decompress(c: DeviceCompressedCache) -> torch.Tensor:
     return out
 
 
+def recompress(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: float) -> DeviceCompressedCache:
+    """The decode-phase re-prune (pipeline.hpp:227-240): decompress
+    (compressed_cache.hpp:271-298) -> hierarchical_mask_for at the decode sparsity
+    (pruner.hpp:121-158) -> fused_magnitude_compress, for every unit on the
+    device.  Bit-identical to the reference's chain on the same pools (the
+    decompressed cache is exact, so re-pruning sees the same values)."""
+    dense = decompress(c)
+    out = prune_compress(dense, cfg, sparsity, c.axis)
+    del dense
+    return out
+
+
+def recompress_pair(k: DeviceCompressedCache, v: DeviceCompressedCache, cfg: SparsityConfig):
+    """prune_cache at the decode sparsity (cfg.s_key / cfg.s_value) of already
+    compressed caches (pipeline.hpp:228-240, "further pruned")."""
+    return recompress(k, cfg, cfg.s_key), recompress(v, cfg, cfg.s_value)
+
+
 def _tails(k_tail, v_tail, U, d):
     if k_tail is None or k_tail.numel() == 0:
         return None, None, 0

@@ -181,3 +181,22 @@ def test_config2_full_size_compression(hs, port):
         kept = torch.where(dgrp != 0, grp.abs(), torch.zeros_like(grp)).sum(-1)
         top2 = grp.abs().topk(2, dim=-1).values.sum(-1)
         assert torch.equal(kept, top2)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("s_pre,s_dec", [(0.0, 1.0), (0.5, 1.0), (0.25, 0.75)])
+def test_decode_phase_recompress_matches_oracle(hs, port, dtype, s_pre, s_dec):
+    """Prefill-sparsity caches re-pruned at the decode sparsity (pipeline.hpp:227-240):
+    GPU recompress == oracle decompress -> prune_compress, bit for bit."""
+    from oracle.oracle import SparsityConfig as OCfg
+    U, L = 2, 1024
+    kx = gen_units(port, U, L, 128, 21, 0, dtype)
+    vx = gen_units(port, U, L, 128, 21, 1, dtype)
+    kc, vc = hs.prune_cache(to_torch(kx, dtype), to_torch(vx, dtype), hs.SparsityConfig(s_pre, s_pre, 64))
+    cfg_dec = hs.SparsityConfig(s_dec, s_dec, 64)
+    k2, v2 = hs.recompress_pair(kc, vc, cfg_dec)
+    for dev_old, dev_new, axis in ((kc, k2, 0), (vc, v2, 1)):
+        for u in range(U):
+            dense = port.decompress(device_to_oracle(dev_old, u))
+            want = port.prune_compress(dense, OCfg(s_dec, s_dec, 64), axis, s_dec)
+            assert_cache_equal(dev_new, u, want, f"recompress axis={axis} unit={u}")
