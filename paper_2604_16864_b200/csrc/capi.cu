@@ -532,8 +532,7 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     const uint64_t n_kv = static_cast<uint64_t>(k->logical_blocks) * k->block_size + tail;
     HS_CHECK_CONFIG(n_kv > 0, "prefill_attention: empty key/value cache");
     HS_CHECK_CONFIG(!causal || n_kv >= n_q, "prefill_attention: causal queries exceed key sequence");
-    HS_CHECK_CONFIG(tail == 0 && k_tail == nullptr,
-                    "prefill_attention: the tcgen05 kernel takes block-aligned caches (dense tail not supported)");
+    HS_CHECK_CONFIG(tail == 0 || (k_tail != nullptr && v_tail != nullptr), "prefill_attention: null dense tail");
     HS_CHECK_CONFIG(k->logical_blocks / 2 + 8 <= 4096,
                     "prefill_attention: %u blocks exceed the kernel's key-tile list (max 8184 blocks)",
                     k->logical_blocks);
@@ -545,7 +544,10 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     L.nb = k->logical_blocks;
     L.gqa = gqa;
     L.n_q = n_q;
-    L.tail = 0;
+    L.tail = static_cast<int>(tail);
+    L.n_tail_blocks = static_cast<int>((tail + hs::kBlock - 1) / hs::kBlock);
+    L.k_tail = k_tail;
+    L.v_tail = v_tail;
     L.causal = causal;
     L.k_dense_count = k->dense_count;
     L.k_sparse_count = k->sparse_count;
@@ -561,10 +563,13 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     {
         const size_t kb = static_cast<size_t>(k->n_units) * k->sparse_count * 1024;
         const size_t vb = static_cast<size_t>(v->n_units) * v->sparse_count * 2048;
-        uint8_t* ws = static_cast<uint8_t*>(workspace(s, kb + vb + 256, kWsPrefill, &st));
+        const size_t tb = static_cast<size_t>(k->n_units) * L.n_tail_blocks * hs::kBlock * hs::kHeadDim * 2;
+        uint8_t* ws = static_cast<uint8_t*>(workspace(s, kb + vb + 2 * tb + 256, kWsPrefill, &st));
         if (st) return st;
         L.k_meta_hw = reinterpret_cast<uint16_t*>(ws);
         L.v_meta_hw = reinterpret_cast<uint16_t*>(ws + kb);
+        L.k_tail_ws = reinterpret_cast<uint16_t*>(ws + kb + vb);
+        L.v_tail_ws = reinterpret_cast<uint16_t*>(ws + kb + vb + tb);
     }
     L.out = out;
     static long long* trace = nullptr;
@@ -589,10 +594,14 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     ok &= make_map(&L.tm_kden, k->dense_pool, 128, U * k->dense_count * 64, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     ok &= make_map(&L.tm_vnnz, v->nnz_pool, 32, U * v->sparse_count * 128, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
     ok &= make_map(&L.tm_vden, v->dense_pool, 64, U * v->dense_count * 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    const uint64_t ntb = static_cast<uint64_t>(L.n_tail_blocks);
+    ok &= make_map(&L.tm_ktail, ntb ? L.k_tail_ws : nullptr, 128, U * ntb * 64, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_map(&L.tm_vtail, ntb ? L.v_tail_ws : nullptr, 64, U * ntb * 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     if (!ok) return fail(HS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     cudaError_t e = hs::launch_prefill(L, s);
     count_launch();
     count_launch();  // metadata atom-order pass + the attention kernel
+    if (L.n_tail_blocks > 0) count_launch();  // dense-tail layout pass
     if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
     if (L.trace) {
         static std::vector<long long> host(4096 * 16);

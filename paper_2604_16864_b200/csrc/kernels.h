@@ -95,13 +95,16 @@ struct PrefillLaunch {
     const uint16_t* v_meta;
     uint16_t* k_meta_hw;     // workspace: K metadata in the tcgen05 TMEM atom order, 1 KB / block
     uint16_t* v_meta_hw;     // workspace: V metadata atom rows (8 of 16 bytes used), 2 KB / block
-    const void* k_tail;
+    const void* k_tail;      // [u][tail][d] dense tail (CacheView::dense_tail, attention.hpp:19-31)
     const void* v_tail;
+    int n_tail_blocks;       // ceil(tail / 64): the tail enters as dense blocks nb, nb+1, ...
+    uint16_t* k_tail_ws;     // workspace: [u][n_tail_blocks * 64][d], zero padded
+    uint16_t* v_tail_ws;     // workspace: [u][n_tail_blocks][d][64] (transposed, zero padded)
     float* out;
     int* dbg;                // optional pipeline watchdog record (debug)
     int mode;                // tools only: 1 = softmax skipped, 2 = MMAs skipped, 3 = both
     long long* trace;        // optional per-tile event clocks of CTA (0,0,0) (tools)
-    CUtensorMap tm_q, tm_knnz, tm_kden, tm_vnnz, tm_vden;
+    CUtensorMap tm_q, tm_knnz, tm_kden, tm_vnnz, tm_vden, tm_ktail, tm_vtail;
 };
 cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s);
 

@@ -199,6 +199,26 @@ __global__ void __launch_bounds__(128) meta_atom_kernel(const uint16_t* __restri
     }
 }
 
+// The dense tail (attention.hpp:289-297) as extra dense blocks nb, nb+1, ...:
+// K rows copied token-major ([B][d], the dense K block layout), V transposed to
+// [d][B] (the dense V^T block layout), both zero padded to whole blocks.  One CTA
+// per (tail block, unit); 128 threads = one token row (K) / one channel (V).
+__global__ void __launch_bounds__(128) tail_prep_kernel(const uint16_t* __restrict__ k_tail,
+                                                        const uint16_t* __restrict__ v_tail, int tail, int ntb,
+                                                        uint16_t* __restrict__ k_ws, uint16_t* __restrict__ v_ws) {
+    const int tb = blockIdx.x, u = blockIdx.y, c = threadIdx.x;
+    const uint16_t* kt = k_tail + static_cast<int64_t>(u) * tail * kHeadDim;
+    const uint16_t* vt = v_tail + static_cast<int64_t>(u) * tail * kHeadDim;
+    uint16_t* kw = k_ws + (static_cast<int64_t>(u) * ntb + tb) * kBlock * kHeadDim;
+    uint16_t* vw = v_ws + (static_cast<int64_t>(u) * ntb + tb) * kBlock * kHeadDim;
+    for (int i = 0; i < kBlock; ++i) {
+        const int tok = tb * kBlock + i;
+        const bool in = tok < tail;
+        kw[i * kHeadDim + c] = in ? kt[static_cast<int64_t>(tok) * kHeadDim + c] : uint16_t(0);
+        vw[c * kBlock + i] = in ? vt[static_cast<int64_t>(tok) * kHeadDim + c] : uint16_t(0);
+    }
+}
+
 template <typename T, bool HILO, bool DBG>
 __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_constant__ PrefillLaunch L,
                                                                PrefillLayout lay) {
@@ -220,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     const int qt = n_tiles_q - 1 - static_cast<int>(blockIdx.x);  // heaviest causal tiles first
     const int h = blockIdx.y, u = blockIdx.z;
     const int q0 = qt * 128;
-    const int n_kv = L.nb * kBlock;  // tail == 0 on this path
+    const int n_kv = L.nb * kBlock + L.tail;  // blocked prefix + dense tail
     const int off = n_kv - L.n_q;
     const int rows_q = min(128, L.n_q - q0);
 
@@ -304,6 +324,19 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     push(b, -1, 1);
                 }
             }
+            // dense tail blocks nb.. (dense K and V from the tail workspace; always masked)
+            const int last_q = off + q0 + rows_q - 1;
+            for (int tb = 0; tb < L.n_tail_blocks; tb += 2) {
+                if (L.causal && (L.nb + tb) * kBlock > last_q) break;
+                const bool pair = tb + 1 < L.n_tail_blocks && (!L.causal || (L.nb + tb + 1) * kBlock <= last_q);
+                TileInfo ti;
+                ti.ke0 = 1;
+                ti.ve0 = 1;
+                ti.ve1 = pair ? int16_t(1) : int16_t(0);
+                ti.dblk = static_cast<int16_t>(L.nb + tb);
+                if (n < cap) s_tiles[n] = ti;
+                ++n;
+            }
             s_ntiles = min(n, cap);
         }
     }
@@ -345,13 +378,18 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         auto issue_k = [&](int t) {
             const int s = t % nk;
             const TileInfo ti = s_tiles[t];
-            const int ke0 = uni(ti.ke0), two = uni(ti.ve1 != 0);
+            const int ke0 = uni(ti.ke0), two = uni(ti.ve1 != 0), dblk = uni(ti.dblk);
             mbar_wait_dbg(&bar_kempty[s], ((t / nk) & 1) ^ 1, dbgp, 4);
             if (DBG && lane == 0) trace(L, t, 7);
             if (elect_one()) {
                 uint8_t* st = base_ptr + lay.off_k + s * lay.k_stage;
                 // both blocks (consecutive slots) in one 128-row box per column half
-                if (ke0 > 0) {
+                if (dblk >= L.nb) {  // dense tail blocks
+                    mbar_arrive_expect_tx(&bar_kfull[s], 32768u);
+                    const int row = (u * L.n_tail_blocks + dblk - L.nb) * kBlock;
+                    tma_tile_g2s(st, &L.tm_ktail, 0, row, &bar_kfull[s]);
+                    tma_tile_g2s(st + 16384, &L.tm_ktail, 64, row, &bar_kfull[s]);
+                } else if (ke0 > 0) {
                     mbar_arrive_expect_tx(&bar_kfull[s], 32768u);
                     const int row = (u * L.k_dense_count + ke0 - 1) * kBlock;
                     tma_tile_g2s(st, &L.tm_kden, 0, row, &bar_kfull[s]);
@@ -369,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         auto issue_v = [&](int t) {
             const int s = t % nv;
             const TileInfo ti = s_tiles[t];
-            const int ve0 = uni(ti.ve0), ve1 = uni(ti.ve1);
+            const int ve0 = uni(ti.ve0), ve1 = uni(ti.ve1), vdblk = uni(ti.dblk);
             mbar_wait_dbg(&bar_vempty[s], ((t / nv) & 1) ^ 1, dbgp, 4);
             if (elect_one()) {
                 uint8_t* st = base_ptr + lay.off_v + s * lay.v_stage;
@@ -381,7 +419,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 for (int i = 0; i < 2; ++i) {
                     const int ve = i == 0 ? ve0 : ve1;
                     if (i == 1 && nb_t == 1) break;
-                    if (ve > 0) {
+                    if (vdblk >= L.nb) {  // dense tail block vdblk + i
+                        const int row = (u * L.n_tail_blocks + vdblk - L.nb + i) * kHeadDim;
+                        tma_tile_g2s(st + lay.vblk * i, &L.tm_vtail, 0, row, &bar_vfull[s]);
+                    } else if (ve > 0) {
                         const int row = (u * L.v_dense_count + ve - 1) * kHeadDim;
                         tma_tile_g2s(st + lay.vblk * i, &L.tm_vden, 0, row, &bar_vfull[s]);
                     } else {
@@ -554,10 +595,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             };
             load_s();
             // masks: invalid rows of single-block tiles; causal (attention.hpp:181-190)
-            const bool row_valid = r < 64 || ti.ve1 != 0;
-            const int key_pos = ti.dblk * kBlock + r;  // diagonal pairs are consecutive blocks
+            const int key_pos = ti.dblk * kBlock + r;  // diagonal / tail pairs are consecutive blocks
+            // rows past a single block or past the end of the tail hold no key
+            const bool row_valid = (r < 64 || ti.ve1 != 0) && (ti.dblk < 0 || key_pos < n_kv);
             // column c (query q0 + c at position off + q0 + c) sees this key iff c >= c_first
-            const int c_first = row_valid ? (ti.dblk >= 0 ? key_pos - off - q0 : 0) : 1 << 30;
+            const int c_first = row_valid ? ((L.causal && ti.dblk >= 0) ? key_pos - off - q0 : 0) : 1 << 30;
             // warp-uniform fast path: every (row, column) of this warp visible
             const bool fast = __all_sync(0xffffffffu, c_first <= c0);
             // x <- s*scale*log2e - m (masked: -inf); does any value exceed m + tau?
@@ -724,13 +766,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
 
 }  // namespace
 
-int prefill_tile_cap(int nb) { return nb / 2 + 8; }
+int prefill_tile_cap(int nb, int ntb) { return nb / 2 + ntb / 2 + 10; }
 
 cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     PrefillLayout lay;
     const bool hilo = L.bf16;
     // K stage: dense 128x128 tile, or 128x64 nnz + 2 KB metadata + 2 KB E atom.
-    const bool kden = L.k_dense_count > 0, vden = L.v_dense_count > 0;
+    const bool kden = L.k_dense_count > 0 || L.n_tail_blocks > 0, vden = L.v_dense_count > 0 || L.n_tail_blocks > 0;
     lay.k_meta = 0;  // unused: the metadata atoms come prepared (meta_atom_kernel)
     lay.k_e = 16384u;
     lay.k_stage = kden ? 32768u : 18432u;
@@ -739,7 +781,7 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     lay.v_meta = 0;  // unused: the metadata atoms come prepared (meta_atom_kernel)
     lay.v_e = 2 * lay.vblk;
     lay.v_stage = lay.v_e + 4096u;
-    lay.tile_cap = static_cast<uint32_t>(prefill_tile_cap(L.nb));
+    lay.tile_cap = static_cast<uint32_t>(prefill_tile_cap(L.nb, L.n_tail_blocks));
     const uint32_t tiles_bytes = (lay.tile_cap * sizeof(TileInfo) + 1023u) & ~1023u;
     lay.off_q = 0;
     lay.off_p = 32768;
@@ -785,6 +827,13 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
             cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) return e;
         }
+    }
+    if (L.n_tail_blocks > 0) {
+        tail_prep_kernel<<<dim3(L.n_tail_blocks, L.n_units), 128, 0, s>>>(
+            static_cast<const uint16_t*>(L.k_tail), static_cast<const uint16_t*>(L.v_tail), L.tail, L.n_tail_blocks,
+            L.k_tail_ws, L.v_tail_ws);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
     }
     const dim3 grid((L.n_q + 127) / 128, L.gqa, L.n_units);
     const bool dbg = L.trace != nullptr || L.dbg != nullptr || L.mode != 0;

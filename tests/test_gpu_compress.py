@@ -157,6 +157,33 @@ def test_golden_reference_vectors_on_gpu(hs):
                 assert (got.meta_pool == g[p + "_meta_pool"]).all()
 
 
+def test_golden_reference_attention_on_gpu(hs, port):
+    """Decode (3 splits) and causal prefill with the 17-token dense tail against the
+    reference's own committed outputs (tests/golden/make_golden.py), on the GPU box
+    where /root/reference is absent."""
+    import math
+    from tests.helpers import MAX_ABS_TOL, MEAN_REL_TOL, err_stats
+    g = np.load(GOLD)
+    to_f = lambda b: (b.astype(np.uint32) << 16).view(np.float32)  # noqa: E731
+    key = to_f(g["key"]).reshape(-1, 128)
+    val = to_f(g["val"]).reshape(-1, 128)
+    L = 256
+    scale = 1.0 / math.sqrt(128)
+    for name in ("s50", "s100w", "s25"):
+        s, sink, window = g[name + "_k_cfg"]
+        kc, vc = hs.prune_cache(to_torch(key[None, :L], "bf16"), to_torch(val[None, :L], "bf16"),
+                                hs.SparsityConfig(float(s), float(s), 64, int(sink), int(window)))
+        kt, vt = to_torch(key[None, L:], "bf16"), to_torch(val[None, L:], "bf16")
+        out = hs.decode_attention(to_torch(g[name + "_decode_q"][None], "bf16"), kc, vc, kt, vt, scale=scale, splits=3)
+        mx, mr = err_stats(out[0].cpu().numpy(), g[name + "_decode_out"])
+        assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (name, "decode", mx, mr)
+        # prefill queries: the generator stream of make_golden.py (role 2, seed 7), regenerated by the port
+        qp = port.round_to(port.random_gaussian(L + 17, 128, port.head_seed(7, 0, 2)), "bf16")
+        outp = hs.prefill_attention(to_torch(qp[None, None], "bf16"), kc, vc, kt, vt, causal=True, scale=scale)
+        mx, mr = err_stats(outp[0, 0].cpu().numpy(), g[name + "_prefill_out"])
+        assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (name, "prefill", mx, mr)
+
+
 def test_config2_full_size_compression(hs, port):
     """Config 2 geometry (8 KV heads x 128K, S=1): bit-exact on two heads,
     structural properties on all (every sparse block decodes to a 2:4 pattern

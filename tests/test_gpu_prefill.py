@@ -102,6 +102,37 @@ def test_prefill_growing_scores(hs, port, dtype, s, causal):
     assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
 
 
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("L,tail,n_q,s,causal", [
+    (512, 17, 529, 1.0, True),     # golden-vector shape: 4 blocks + 17-token tail, every query
+    (1024, 64, 300, 0.5, True),    # whole tail block, queries at the end
+    (768, 100, 868, 0.25, True),   # two tail blocks (the second one partial)
+    (512, 130, 200, 1.0, False),   # three tail blocks, non-causal
+    (0, 37, 37, 0.0, True),        # tail only (no compressed prefix)
+])
+def test_prefill_with_dense_tail(hs, port, dtype, L, tail, n_q, s, causal):
+    """prefill_attention with CacheView::dense_tail (attention.hpp:19-31, :289-297)."""
+    if L == 0:
+        pytest.skip("a cache needs at least one compressed block on the device path")
+    U, gqa = 2, 2
+    kx = gen_units(port, U, L + tail, 128, 13, 0, dtype)
+    vx = gen_units(port, U, L + tail, 128, 13, 1, dtype)
+    kc, vc = hs.prune_cache(to_torch(kx[:, :L], dtype), to_torch(vx[:, :L], dtype), hs.SparsityConfig(s, s, 64))
+    q = np.stack([np.stack([port.round_to(port.random_gaussian(n_q, 128, port.head_seed(13, u, 2 + g)), dtype)
+                            for g in range(gqa)]) for u in range(U)])
+    scale = np.float32(1.0 / math.sqrt(128))
+    got = hs.prefill_attention(to_torch(q, dtype), kc, vc, to_torch(kx[:, L:], dtype), to_torch(vx[:, L:], dtype),
+                               causal=causal, scale=float(scale)).cpu().numpy()
+
+    def one(ug):
+        u, g = divmod(ug, gqa)
+        return port.prefill(q[u, g], device_to_oracle(kc, u), device_to_oracle(vc, u), kx[u, L:], vx[u, L:], causal,
+                            scale, 64)
+    want = np.stack(parallel(one, range(U * gqa))).reshape(U, gqa, n_q, 128)
+    mx, mr = err_stats(got, want)
+    assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
+
+
 def test_prefill_rejects_invalid(hs, port):
     from paper_2604_16864_b200 import ConfigError
     kc, vc, q = setup(hs, port, 1, 256, 1.0, "f16", 1, 256)
