@@ -406,7 +406,7 @@ def run_prefill(hs, dev, rank, args):
     q = torch.randn((Up, G, Lp, D), generator=g, device=dev, dtype=torch.float32).half()
     out = torch.empty((Up, G, Lp, D), dtype=torch.float32, device=dev)
     res = {}
-    for s in (0.0, 0.25, 0.5, 0.75):
+    for s in (0.0, 0.25, 0.5, 0.75, 1.0):
         key = torch.randn((Up, Lp, D), generator=g, device=dev, dtype=torch.float32).half()
         val = torch.randn((Up, Lp, D), generator=g, device=dev, dtype=torch.float32).half()
         kc, vc = hs.prune_cache(key, val, hs.SparsityConfig(s, s, 64))
