@@ -408,22 +408,13 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     if (ct && threadIdx.x == 0) ct[3] = globaltimer();
     if (L.out == nullptr) return;
 
-    // ---------------- last CTA of the unit combines all splits ----------------
-    __threadfence();
-    if (ct && threadIdx.x == 0) ct[7] = globaltimer();
-    __syncthreads();
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&L.counters[u], 1);
-    __syncthreads();
-    if (s_ticket != L.nsplit - 1) return;
-    if (ct && threadIdx.x == 0) ct[5] = globaltimer();
-    __threadfence();
-    if (ct && threadIdx.x == 0) ct[6] = globaltimer();
+    // ---------------- combine the unit's splits (attention.hpp:387-407) ----------------
+    // Streaming LSE merge in chunks of 32 splits: every load of a chunk (m, l and
+    // the O column of each split) is independent, so a chunk costs one L2 round
+    // trip (configs[1] has 18 splits per unit: one chunk).
     const float* P = L.partial + static_cast<int64_t>(u) * L.nsplit * stride_p;
-    constexpr float kLog2e = 1.4426950408889634f;
-    // Streaming LSE merge in chunks of 32 splits: every load of a chunk (m, l
-    // and this thread's O column of each split) is independent, so a chunk costs
-    // one L2 round trip (configs[1] has 18 splits per unit: one chunk).
-    for (int idx = threadIdx.x; idx < gqa * kHeadDim; idx += nthr) {
+    auto merge = [&](int idx) {
+        constexpr float kLog2e = 1.4426950408889634f;
         const int qq = idx / kHeadDim, c = idx % kHeadDim;
         const float* pq = P + qq * (kHeadDim + 2);
         float M = -INFINITY, lsum = 0.f, acc = 0.f;
@@ -461,7 +452,42 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
                 po[kHeadDim + 1] = lsum;
             }
         }
+    };
+    __threadfence();
+    if (ct && threadIdx.x == 0) ct[7] = globaltimer();
+    __syncthreads();
+    if (L.coop_combine) {
+        // Whole grid resident (host-checked): every CTA of the unit waits for the
+        // unit's last partial, then merges its own slice of the gqa x d outputs, so
+        // the combine is one parallel round instead of one CTA's serial pass.
+        int* arrive = &L.counters[u];
+        int* done = &L.counters[L.n_units + u];
+        if (threadIdx.x == 0) {
+            atomicAdd(arrive, 1);
+            while (ld_acquire(arrive) < L.nsplit) __nanosleep(64);
+        }
+        __syncthreads();
+        if (ct && threadIdx.x == 0) ct[5] = globaltimer();
+        const int n = gqa * kHeadDim;
+        const int lo = static_cast<int>(static_cast<int64_t>(n) * split / L.nsplit);
+        const int hi = static_cast<int>(static_cast<int64_t>(n) * (split + 1) / L.nsplit);
+        for (int idx = lo + threadIdx.x; idx < hi; idx += nthr) merge(idx);
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(done, 1) == L.nsplit - 1) {
+            *arrive = 0;  // every CTA of the unit is past its spin: safe to re-arm
+            *done = 0;
+        }
+        if (ct && threadIdx.x == 0) ct[4] = globaltimer();
+        return;
     }
+    // Otherwise the last CTA of the unit to arrive merges everything.
+    if (threadIdx.x == 0) s_ticket = atomicAdd(&L.counters[u], 1);
+    __syncthreads();
+    if (s_ticket != L.nsplit - 1) return;
+    if (ct && threadIdx.x == 0) ct[5] = globaltimer();
+    __threadfence();
+    if (ct && threadIdx.x == 0) ct[6] = globaltimer();
+    for (int idx = threadIdx.x; idx < gqa * kHeadDim; idx += nthr) merge(idx);
     if (threadIdx.x == 0) L.counters[u] = 0;
     if (ct && threadIdx.x == 0) ct[4] = globaltimer();
 }

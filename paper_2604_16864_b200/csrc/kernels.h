@@ -72,7 +72,8 @@ struct DecodeLaunch {
     float* partial;          // [u][nsplit][gqa][d+2] (O, m, l)
     float* out;              // fused combine target or nullptr (split partials only)
     int out_mode;            // 0: normalised [u][gqa][d]; 1: merged partial [u][gqa][d+2]
-    int* counters;           // [u] arrival counters for the fused combine
+    int* counters;           // [2u] arrival / done counters for the fused combine
+    int coop_combine;        // every CTA resident: all CTAs of a unit merge in parallel
     long long* cta_times;    // tools only: [grid][5] globaltimer at start / first data / loop end / partial written / combine done
     CUtensorMap tm_knnz, tm_kden, tm_vnnz, tm_vden;
 };
