@@ -144,7 +144,10 @@ HS_API hs_status hs_decompress(const hs_device_cache* c, void* dst, void* stream
  *   k, v:   key cache (HS_AXIS_CHANNEL) and value cache (HS_AXIS_SEQUENCE)
  *   k_tail, v_tail: dtype [n_units][tail][d] dense tails (CacheView::dense_tail,
  *           attention.hpp:19-31) or NULL when tail == 0
- *   splits: split-KV count per unit (0 = chosen for the SM count); results
+ *   splits: split-KV count per unit.  0 = chosen for the SM count, with the
+ *           unit's CTAs claiming blocks dynamically (load-balanced; the fp32
+ *           summation order may differ between runs).  > 0 = the static,
+ *           run-to-run deterministic partition of attention.hpp:380-381.  Results
  *           agree across split counts to float rounding (test_attention.cpp:315-326)
  *   out:    float [n_units][gqa][d]
  * gqa must be 1..8. */

@@ -465,7 +465,7 @@ static hs_status decode_common(const void* q, const hs_device_cache* k, const hs
                     L.max_blocks_per_cta);
     if ((st = fill_decode_maps(L, k, v))) return st;
     const size_t part_bytes = static_cast<size_t>(L.n_units) * ns * gqa * (hs::kHeadDim + 2) * sizeof(float);
-    const size_t cnt_bytes = ((2 * static_cast<size_t>(L.n_units) * sizeof(int) + 255) / 256) * 256;
+    const size_t cnt_bytes = ((3 * static_cast<size_t>(L.n_units) * sizeof(int) + 255) / 256) * 256;
     uint8_t* ws = static_cast<uint8_t*>(workspace(s, cnt_bytes + part_bytes, kWsDecode, &st));
     if (st) return st;
     L.counters = reinterpret_cast<int*>(ws);
@@ -476,6 +476,12 @@ static hs_status decode_common(const void* q, const hs_device_cache* k, const hs
     // is resident at once (one wave of decode_ctas_per_sm() CTAs per SM).
     L.coop_combine = static_cast<int64_t>(ns) * L.n_units <= static_cast<int64_t>(hs::decode_ctas_per_sm()) * sm_count();
     if (const char* env = getenv("HS_DECODE_COOP")) L.coop_combine = L.coop_combine && atoi(env) != 0;
+    L.blk_ctr = L.counters + 2 * L.n_units;
+    // splits == 0 (auto): the unit's CTAs claim blocks dynamically (balanced across
+    // SMs, summation order varies run to run).  An explicit split count keeps the
+    // static, deterministic partition of attention.hpp:380-381.
+    L.dynamic = splits == 0 && L.debug_stream_only == 0 && L.prefetch_distance == 0;
+    if (const char* env = getenv("HS_DECODE_DYNAMIC")) L.dynamic = L.dynamic && atoi(env) != 0;
     L.cta_times = nullptr;
     static long long* times = nullptr;
     const char* tpath = getenv("HS_DECODE_TIMES");  // tools: per-CTA timeline dump

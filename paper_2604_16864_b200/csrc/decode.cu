@@ -67,7 +67,10 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
 
     const int16_t* kidx = L.k_index + static_cast<int64_t>(u) * L.nb;
     const int16_t* vidx = L.v_index + static_cast<int64_t>(u) * L.nb;
-    for (int i = threadIdx.x; i < nblk; i += 32 * NW) {
+    // dynamic block claiming needs the one-slot ring and the fused combine (which
+    // re-arms the counters)
+    const bool dyn = L.dynamic != 0 && spw == 1 && L.out != nullptr;
+    for (int i = threadIdx.x; i < (dyn ? 0 : nblk); i += 32 * NW) {
         s_kidx[i] = kidx[b0 + i];
         s_vidx[i] = vidx[b0 + i];
     }
@@ -80,11 +83,8 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     // Each consumer warp streams its own blocks (i = warp + NW*k) into its own
     // `spw` ring slots: it issues block k+spw right after finishing block k, so
     // no empty barriers are needed and a waiter is never a phase ahead.
-    auto issue = [&](int k) {
-        const int i = warp + NW * k;
+    auto issue_e = [&](int k, int ke, int ve) {
         const int s = warp * spw + k % spw;
-        const int b = b0 + i;
-        const int ke = s_kidx[i], ve = s_vidx[i];
         uint8_t* kreg = base_ptr + s * lay.stage_bytes;
         uint8_t* vreg = kreg + lay.k_bytes;
         const uint32_t bytes = (ke > 0 ? 16384u : 9216u) + (ve > 0 ? 16384u : 9216u);
@@ -112,7 +112,26 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
                 tma_tile_g2s(vreg, &L.tm_vnnz, 0, sb * kHeadDim, &full_bar[s]);
             tma_bulk_g2s(vreg + 8192, L.v_meta + static_cast<int64_t>(sb) * 512, 1024, &full_bar[s]);
         }
-        (void)b;
+    };
+    auto issue = [&](int k) {
+        const int i = warp + NW * k;
+        issue_e(k, s_kidx[i], s_vidx[i]);
+    };
+    // Dynamic mode: the warps of a unit's CTAs claim the unit's blocks one at a
+    // time from a per-unit counter, so CTAs on SMs that stream faster take more
+    // blocks (static ranges leave the whole unit waiting for its slowest SM).
+    // Lane 0 keeps a two-deep lookahead: the claim for block k+2 and the index
+    // entries for block k+1 are in flight while block k computes.
+    int* const ctr = L.blk_ctr + u;
+    const int16_t* const kidx_g = L.k_index + static_cast<int64_t>(u) * L.nb + L.block_begin;
+    const int16_t* const vidx_g = L.v_index + static_cast<int64_t>(u) * L.nb + L.block_begin;
+    const int span_dyn = dyn ? span : 0;
+    int d_cur = -1, d_cur_ke = 0, d_cur_ve = 0;  // block being computed (lane 0)
+    int d_nxt = -1, d_nxt_ke = 0, d_nxt_ve = 0;  // next block: entries in flight
+    int d_claim = -1;                            // block after next: claim in flight
+    auto claim = [&]() {
+        const int b = atomicAdd(ctr, 1);
+        return b < span_dyn ? b : -1;
     };
     // L2 prefetch of a future block of this warp (pools are contiguous per slot).
     auto prefetch = [&](int k) {
@@ -135,16 +154,32 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
             prefetch_l2(L.v_meta + sb * 512, 1024);
         }
     };
-    const int nk = nblk > warp ? (nblk - warp + NW - 1) / NW : 0;  // blocks of this warp
+    int nk = nblk > warp ? (nblk - warp + NW - 1) / NW : 0;  // blocks of this warp (static mode)
     const int pf = L.prefetch_distance;
     if (lane == 0) {
         if (warp == 0) {
             prefetch_tmap(&L.tm_knnz);
             prefetch_tmap(&L.tm_vnnz);
         }
-        for (int k = 0; k < spw && k < nk; ++k) issue(k);
-        for (int k = spw; k < spw + pf && k < nk; ++k) prefetch(k);
+        if (dyn) {
+            d_cur = claim();
+            if (d_cur >= 0) {
+                d_cur_ke = kidx_g[d_cur];
+                d_cur_ve = vidx_g[d_cur];
+                issue_e(0, d_cur_ke, d_cur_ve);
+                d_nxt = claim();
+                if (d_nxt >= 0) {
+                    d_nxt_ke = kidx_g[d_nxt];
+                    d_nxt_ve = vidx_g[d_nxt];
+                    d_claim = claim();
+                }
+            }
+        } else {
+            for (int k = 0; k < spw && k < nk; ++k) issue(k);
+            for (int k = spw; k < spw + pf && k < nk; ++k) prefetch(k);
+        }
     }
+    if (dyn) nk = 1 << 30;  // until the unit's counter runs out
     __syncwarp();
 
     // ------------------------------------------------------- consumers ----
@@ -168,11 +203,19 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
                 qb[j][x] = g < gqa ? ld_pair(q + g * kHeadDim + 32 * j + 8 * x + 2 * t) : 0u;
 
         for (int k = 0; k < nk; ++k) {
-            const int i = warp + NW * k;
             const int s = warp * spw + k % spw;
+            bool kd, vd;
+            if (dyn) {
+                if (__shfl_sync(0xffffffffu, d_cur, 0) < 0) break;
+                kd = __shfl_sync(0xffffffffu, d_cur_ke, 0) > 0;
+                vd = __shfl_sync(0xffffffffu, d_cur_ve, 0) > 0;
+            } else {
+                const int i = warp + NW * k;
+                kd = s_kidx[i] > 0;
+                vd = s_vidx[i] > 0;
+            }
             mbar_wait(&full_bar[s], (k / spw) & 1);
             if (ct && k == 0 && threadIdx.x == 0) ct[1] = globaltimer();
-            const bool kd = s_kidx[i] > 0, vd = s_vidx[i] > 0;
             if (L.debug_stream_only) {  // pipeline-only measurement mode (tools/)
                 __syncwarp();
                 if (lane == 0 && k + spw < nk) issue(k + spw);
@@ -310,8 +353,24 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
                     }
             }
             __syncwarp();  // every lane is done with slot s
-            if (lane == 0 && k + spw < nk) issue(k + spw);
-            if (lane == 0 && k + spw + pf < nk) prefetch(k + spw + pf);
+            if (dyn) {
+                if (lane == 0) {
+                    // next block -> TMA; block after next -> entries; new claim
+                    if (d_nxt >= 0) issue_e(k + 1, d_nxt_ke, d_nxt_ve);
+                    d_cur = d_nxt;
+                    d_cur_ke = d_nxt_ke;
+                    d_cur_ve = d_nxt_ve;
+                    d_nxt = d_claim;
+                    if (d_nxt >= 0) {
+                        d_nxt_ke = kidx_g[d_nxt];
+                        d_nxt_ve = vidx_g[d_nxt];
+                        d_claim = claim();
+                    }
+                }
+            } else {
+                if (lane == 0 && k + spw < nk) issue(k + spw);
+                if (lane == 0 && k + spw + pf < nk) prefetch(k + spw + pf);
+            }
             __syncwarp();
         }
 
@@ -476,6 +535,7 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
         if (threadIdx.x == 0 && atomicAdd(done, 1) == L.nsplit - 1) {
             *arrive = 0;  // every CTA of the unit is past its spin: safe to re-arm
             *done = 0;
+            if (dyn) *ctr = 0;  // every warp of the unit has finished claiming
         }
         if (ct && threadIdx.x == 0) ct[4] = globaltimer();
         return;
@@ -488,7 +548,10 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     __threadfence();
     if (ct && threadIdx.x == 0) ct[6] = globaltimer();
     for (int idx = threadIdx.x; idx < gqa * kHeadDim; idx += nthr) merge(idx);
-    if (threadIdx.x == 0) L.counters[u] = 0;
+    if (threadIdx.x == 0) {
+        L.counters[u] = 0;
+        if (dyn) *ctr = 0;  // last CTA of the unit: every warp has finished claiming
+    }
     if (ct && threadIdx.x == 0) ct[4] = globaltimer();
 }
 

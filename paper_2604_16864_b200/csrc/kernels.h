@@ -74,6 +74,8 @@ struct DecodeLaunch {
     int out_mode;            // 0: normalised [u][gqa][d]; 1: merged partial [u][gqa][d+2]
     int* counters;           // [2u] arrival / done counters for the fused combine
     int coop_combine;        // every CTA resident: all CTAs of a unit merge in parallel
+    int dynamic;             // warps claim the unit's blocks from blk_ctr (no static ranges)
+    int* blk_ctr;            // [u] block claim counters (dynamic mode; reset by the combine)
     long long* cta_times;    // tools only: [grid][5] globaltimer at start / first data / loop end / partial written / combine done
     CUtensorMap tm_knnz, tm_kden, tm_vnnz, tm_vden;
 };

@@ -123,3 +123,16 @@ def test_decode_rejects_invalid(hs, port):
         hs.decode_attention(q, vc, kc)          # swapped caches (test_attention.cpp:392-395)
     with pytest.raises(ConfigError):
         hs.decode_attention(q.repeat(1, 3, 1), kc, vc)  # 12 rows > 8
+
+
+def test_decode_fixed_splits_deterministic(hs, port):
+    """An explicit split count is the static partition: bitwise identical across
+    runs (acceptance.cpp:518-543 determinism); auto splits (dynamic block claims)
+    agree to float rounding."""
+    U, L = 4, 8192
+    kx, vx, kc, vc = build_caches(hs, port, U, L, 1.0, "bf16")
+    q = to_torch(decode_queries(port, U, 4, "bf16"), "bf16")
+    runs = [hs.decode_attention(q, kc, vc, splits=7).cpu().numpy() for _ in range(3)]
+    assert all((r == runs[0]).all() for r in runs[1:])
+    auto = [hs.decode_attention(q, kc, vc).cpu().numpy() for _ in range(3)]
+    assert max(np.abs(a - runs[0]).max() for a in auto) < 1e-5
