@@ -78,6 +78,8 @@ void* dummy_buffer() {
     return p;
 }
 
+bool make_map_halves(CUtensorMap* m, const void* ptr, uint64_t outer, uint32_t box_outer);
+
 // 2-D tile map over a row-major [outer][inner] 16-bit array.  Encoded maps are
 // cached by (pointer, geometry, swizzle) so steady-state calls skip the driver.
 bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
@@ -111,6 +113,43 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
     if (ok) {
         std::lock_guard<std::mutex> lk(mu);
         if (cache.size() > 4096) cache.clear();
+        cache[key] = *m;
+    }
+    return ok;
+}
+
+// 3-D view of a row-major [outer][128] 16-bit array as [2 halves][outer][64]
+// (half stride 128 B): one box {64, box_outer, 2} lands as the two SW128
+// column-half tiles [half][row][64] a K-major UMMA operand of K = 128 expects.
+bool make_map_halves(CUtensorMap* m, const void* ptr, uint64_t outer, uint32_t box_outer) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    if (ptr == nullptr || outer == 0) {
+        ptr = dummy_buffer();
+        outer = box_outer;
+        if (!ptr) return false;
+    }
+    using Key = std::tuple<const void*, uint64_t, uint32_t>;
+    static std::mutex mu;
+    static std::map<Key, CUtensorMap> cache;
+    const Key key{ptr, outer, box_outer};
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *m = it->second;
+            return true;
+        }
+    }
+    cuuint64_t dims[3] = {64, outer, 2};
+    cuuint64_t strides[2] = {256, 128};
+    cuuint32_t box[3] = {64, box_outer, 2};
+    cuuint32_t es[3] = {1, 1, 1};
+    const bool ok = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    if (ok) {
+        std::lock_guard<std::mutex> lk(mu);
         cache[key] = *m;
     }
     return ok;
@@ -601,11 +640,13 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     // K tiles are two consecutive pool slots (128 rows) per TMA; a single-block
     // tile's second half is masked in the kernel (and zero-filled past the pool).
     ok &= make_map(&L.tm_knnz, k->nnz_pool, 64, U * k->sparse_count * 64, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-    ok &= make_map(&L.tm_kden, k->dense_pool, 128, U * k->dense_count * 64, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_map_halves(&L.tm_kden, k->dense_pool, U * k->dense_count * 64, 128);
     ok &= make_map(&L.tm_vnnz, v->nnz_pool, 32, U * v->sparse_count * 128, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
     ok &= make_map(&L.tm_vden, v->dense_pool, 64, U * v->dense_count * 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_map(&L.tm_vnnz2, v->nnz_pool, 32, U * v->sparse_count * 128, 32, 256, CU_TENSOR_MAP_SWIZZLE_64B);
+    ok &= make_map(&L.tm_vden2, v->dense_pool, 64, U * v->dense_count * 128, 64, 256, CU_TENSOR_MAP_SWIZZLE_128B);
     const uint64_t ntb = static_cast<uint64_t>(L.n_tail_blocks);
-    ok &= make_map(&L.tm_ktail, ntb ? L.k_tail_ws : nullptr, 128, U * ntb * 64, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_map_halves(&L.tm_ktail, ntb ? L.k_tail_ws : nullptr, U * ntb * 64, 128);
     ok &= make_map(&L.tm_vtail, ntb ? L.v_tail_ws : nullptr, 64, U * ntb * 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     if (!ok) return fail(HS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     cudaError_t e = hs::launch_prefill(L, s);

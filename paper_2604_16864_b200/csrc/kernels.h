@@ -107,7 +107,9 @@ struct PrefillLaunch {
     int* dbg;                // optional pipeline watchdog record (debug)
     int mode;                // tools only: 1 = softmax skipped, 2 = MMAs skipped, 3 = both
     long long* trace;        // optional per-tile event clocks of CTA (0,0,0) (tools)
-    CUtensorMap tm_q, tm_knnz, tm_kden, tm_vnnz, tm_vden, tm_ktail, tm_vtail;
+    // tm_kden / tm_ktail are 3-D views ([half][row][64]: one box per 128x128 tile);
+    // tm_vnnz2 / tm_vden2 box two consecutive V pool slots (256 rows).
+    CUtensorMap tm_q, tm_knnz, tm_kden, tm_vnnz, tm_vden, tm_ktail, tm_vtail, tm_vnnz2, tm_vden2;
 };
 cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s);
 

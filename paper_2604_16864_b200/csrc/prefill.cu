@@ -40,11 +40,22 @@ namespace {
 constexpr int kSoftWG = HS_PREFILL_WG;     // softmax warpgroups (each owns kCols query columns); 4 + 4 role warps = 20 warps
 constexpr int kCols = 128 / kSoftWG;       // query columns per softmax thread
 constexpr int kSoftWarps = 4 * kSoftWG;
-constexpr int kWarpK = kSoftWarps;         // TMA producer (tile list, Q, K and V tiles)
+constexpr int kWarpK = kSoftWarps;         // TMA producer: tile list, Q and K tiles
 constexpr int kWarpMma = kSoftWarps + 1;   // tcgen05 issuer of GEMM1 (S^T = K Q^T), TMEM owner
 constexpr int kWarpMma2 = kSoftWarps + 2;  // tcgen05 issuer of GEMM2 (O^T += V^T P^T)
+constexpr int kWarpV = kSoftWarps + 3;     // TMA producer: V tiles
+// One warp issues a TMA operation every ~180 cycles at best (the mbarrier /
+// address chain, tools/probes/tma_ops.cu), so each tile's loads are as few
+// operations as the slot layout allows.  HS_PREFILL_SPLIT_PRODUCER moves the V
+// loads to a 20th warp (measured 3% slower: the softmax, not the producer,
+// bounds the full kernel, and the extra warp shares its SM sub-partition).
+#ifndef HS_PREFILL_SPLIT_PRODUCER
 constexpr int kThreads = 32 * (kSoftWarps + 3);
+#else
+constexpr int kThreads = 32 * (kSoftWarps + 4);
+#endif
 
+constexpr uint32_t kBiasBytes = 3 * 2048;  // ones + bias[2] GEMM1 operands (16-byte rows)
 constexpr float kTau = 8.0f;      // lazy-rescale threshold (log2 units): P <= 2^8
 
 // One key tile = one or two 64-token blocks of the same K kind.  8 bytes:
@@ -72,6 +83,7 @@ struct PrefillLayout {
     uint32_t off_k, k_stage, nk, k_meta, k_e;
     uint32_t off_v, v_stage, nv, vblk, v_meta, v_e;
     uint32_t off_tiles, tile_cap;
+    uint32_t off_bias;  // ones [128 x 16] + two bias operands [128 x 16] (16-byte rows, K halves aliased)
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -79,6 +91,15 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 }
 __device__ __forceinline__ void named_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// TMEM -> fp32 registers, 16 columns starting at taddr (the softmax's S^T halves).
+__device__ __forceinline__ void tmem_ld16_f(uint32_t taddr, float* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7]),
+          "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]), "=f"(r[12]), "=f"(r[13]), "=f"(r[14]), "=f"(r[15])
+        : "r"(taddr));
 }
 
 // TMEM -> registers: this warp's 32 lanes x N consecutive 32-bit columns.
@@ -233,7 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     __shared__ uint32_t s_tmem;
     __shared__ int s_ntiles;
     __shared__ float s_red[4][128];
-    __shared__ float s_mnew[128], s_alpha[128], s_mrun[128], s_mneg[128];
+    __shared__ float s_delta[128], s_alpha[128], s_mrun[128], s_mused[2][128];
+    __shared__ uint16_t s_bq[128];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     const int n_tiles_q = (L.n_q + 127) / 128;
@@ -340,6 +362,19 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             s_ntiles = min(n, cap);
         }
     }
+    if (warp < kSoftWarps) {
+        // GEMM1 operands of the stabiliser term (see the softmax header): A = ones,
+        // B[sb] row c = 8 copies of -m_c / (16 scale log2e) (m unset: 0).
+        uint4* ob = reinterpret_cast<uint4*>(base_ptr + lay.off_bias);
+        const uint32_t one = F16Traits<T>::pack(1.f, 1.f);
+        for (int i = tid; i < 3 * 128; i += 32 * kSoftWarps)
+            ob[i] = i < 128 ? make_uint4(one, one, one, one) : make_uint4(0u, 0u, 0u, 0u);
+        if (tid < 128) {
+            s_mused[0][tid] = 0.f;
+            s_mused[1][tid] = 0.f;
+        }
+        fence_async_smem();
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -358,9 +393,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     // arithmetic below stays in uniform registers and the single-thread
     // tcgen05 / TMA instructions issue without R2UR waterfall loops.
     auto uni = [](int v) { return __shfl_sync(0xffffffffu, v, 0); };
+#ifndef HS_PREFILL_SPLIT_PRODUCER
     if (warp_u == kWarpK) {
-        // --------------------------------------------------------- producer
-        if (elect_one()) {
+#else
+    if (warp_u == kWarpK || warp_u == kWarpV) {
+#endif
+        // -------------------------------------------------------- producers
+        if (warp_u == kWarpK && elect_one()) {
             prefetch_tmap(&L.tm_q);
             prefetch_tmap(&L.tm_knnz);
             prefetch_tmap(&L.tm_kden);
@@ -369,10 +408,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             tma_tile_g2s(base_ptr + lay.off_q, &L.tm_q, 0, qrow, &bar_q);
             tma_tile_g2s(base_ptr + lay.off_q + 16384, &L.tm_q, 64, qrow, &bar_q);
         }
-        __syncwarp();
+#ifndef HS_PREFILL_SPLIT_PRODUCER
         if (elect_one()) {
+#else
+        if (warp_u == kWarpV && elect_one()) {
+#endif
             prefetch_tmap(&L.tm_vnnz);
             prefetch_tmap(&L.tm_vden);
+            prefetch_tmap(&L.tm_vnnz2);
+            prefetch_tmap(&L.tm_vden2);
         }
         __syncwarp();
         auto issue_k = [&](int t) {
@@ -384,16 +428,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             if (elect_one()) {
                 uint8_t* st = base_ptr + lay.off_k + s * lay.k_stage;
                 // both blocks (consecutive slots) in one 128-row box per column half
+                // dense: both 64-column halves in one 3-D box ([half][row][64])
                 if (dblk >= L.nb) {  // dense tail blocks
                     mbar_arrive_expect_tx(&bar_kfull[s], 32768u);
                     const int row = (u * L.n_tail_blocks + dblk - L.nb) * kBlock;
-                    tma_tile_g2s(st, &L.tm_ktail, 0, row, &bar_kfull[s]);
-                    tma_tile_g2s(st + 16384, &L.tm_ktail, 64, row, &bar_kfull[s]);
+                    tma_tile3_g2s(st, &L.tm_ktail, 0, row, 0, &bar_kfull[s]);
                 } else if (ke0 > 0) {
                     mbar_arrive_expect_tx(&bar_kfull[s], 32768u);
                     const int row = (u * L.k_dense_count + ke0 - 1) * kBlock;
-                    tma_tile_g2s(st, &L.tm_kden, 0, row, &bar_kfull[s]);
-                    tma_tile_g2s(st + 16384, &L.tm_kden, 64, row, &bar_kfull[s]);
+                    tma_tile3_g2s(st, &L.tm_kden, 0, row, 0, &bar_kfull[s]);
                 } else {
                     mbar_arrive_expect_tx(&bar_kfull[s], 16384u + 1024u * (1 + two));
                     const int sbk = u * L.k_sparse_count + (-ke0 - 1);
@@ -415,6 +458,17 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 uint32_t bytes = ve0 > 0 ? 16384u : 8192u + 2048u;
                 if (nb_t == 2) bytes += ve1 > 0 ? 16384u : 8192u + 2048u;
                 mbar_arrive_expect_tx(&bar_vfull[s], bytes);
+                // two consecutive pool slots of one kind: one 256-row box (+ one 4 KB
+                // metadata copy); otherwise one operation per block
+                // (sparse pairs only when the stage holds nnz blocks back to back)
+                if (nb_t == 2 && vdblk < L.nb && ve0 > 0 && ve1 == ve0 + 1) {
+                    const int row = (u * L.v_dense_count + ve0 - 1) * kHeadDim;
+                    tma_tile_g2s(st, &L.tm_vden2, 0, row, &bar_vfull[s]);
+                } else if (nb_t == 2 && vdblk < L.nb && ve0 < 0 && ve1 == ve0 - 1 && lay.vblk == 8192u) {
+                    const int sbv = u * L.v_sparse_count + (-ve0 - 1);
+                    tma_tile_g2s(st, &L.tm_vnnz2, 0, sbv * kHeadDim, &bar_vfull[s]);
+                    tma_bulk_g2s(st + lay.v_e, L.v_meta_hw + static_cast<int64_t>(sbv) * 1024, 4096, &bar_vfull[s]);
+                } else
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
                     const int ve = i == 0 ? ve0 : ve1;
@@ -435,12 +489,19 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             }
             __syncwarp();
         };
-        // K(t) is consumed a tile earlier than V(t): issue K one tile ahead.
+#ifndef HS_PREFILL_SPLIT_PRODUCER
         for (int t = 0; t < ntiles; ++t) {
             issue_k(t);
             if (t >= 1) issue_v(t - 1);
         }
         if (ntiles > 0) issue_v(ntiles - 1);
+#else
+        if (warp_u == kWarpK) {
+            for (int t = 0; t < ntiles; ++t) issue_k(t);
+        } else {
+            for (int t = 0; t < ntiles; ++t) issue_v(t);
+        }
+#endif
     } else if (warp_u == kWarpMma || warp_u == kWarpMma2) {
         // ------------------------------------------------------ MMA issuers
         // kWarpMma issues GEMM1 (S^T = K Q^T) per tile, kWarpMma2 GEMM2
@@ -463,6 +524,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         const uint64_t dP = umma_desc(sP, 16384, 1024, kLayoutSW128);
         const uint64_t dEK = umma_desc(sK + lay.k_e, 16, 128, kLayoutNone);
         const uint64_t dEV = umma_desc(sV + lay.v_e, 16, 128, kLayoutNone);
+        // ones / bias operands: K-major, no swizzle, 16-byte rows (SBO 128 B per 8
+        // rows); LBO 0 aliases the two 8-element K halves (the rows are constant)
+        const uint32_t sBias = base + lay.off_bias;
+        const uint64_t dOnes = umma_desc(sBias, 0, 128, kLayoutNone);
+        const uint64_t dBias = umma_desc(sBias + 2048, 0, 128, kLayoutNone);
         const uint32_t kst16 = lay.k_stage >> 4, vst16 = lay.v_stage >> 4, vblk16 = lay.vblk >> 4;
         bool o_started = false;
         auto gemm2 = [&](int tp) {
@@ -526,17 +592,20 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 if (ke0 < 0) tmem_cp_128x128b(tEK + 4 * sb, dEK + so);
                 // GEMM1: S^T[sb] = K_tile * Q^T
                 const uint32_t tS = tS0 + 128 * sb;
+                // S^T = ones * bias[sb]^T (the -m_c / (scale log2e) stabiliser of every
+                // column) + K_tile * Q^T
+                if (!(mode & 2)) umma_f16(tS, dOnes, dBias + sb * 128, id_g1_de, 0u);
                 if (mode & 2) {
                 } else if (ke0 > 0) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
                         umma_f16(tS, dK + so + (j >> 2) * 1024 + 2 * (j & 3), dQ + (j >> 2) * 1024 + 2 * (j & 3),
-                                 id_g1_de, j > 0);
+                                 id_g1_de, 1u);
                 } else {
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
                         umma_sp_f16(tS, dK + so + 2 * j, dQ + (j >> 1) * 1024 + 4 * (j & 1), tEK + 4 * sb + j,
-                                    id_g1_sp, j > 0);
+                                    id_g1_sp, 1u);
                 }
                 umma_commit(&bar_sfull[sb]);
                 umma_commit(&bar_kempty[s]);  // K stage can be refilled once GEMM1(t) read it
@@ -564,11 +633,17 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         for (int c = 0; c < kCols; ++c) l_part[c] = 0.f;
         if (r < kCols) {
             s_mrun[c0 + r] = -INFINITY;
-            s_mneg[c0 + r] = INFINITY;  // -m, the FMA addend of the fast path
+            s_bq[c0 + r] = 0;
         }
         named_bar(bar_id, 128);
         uint8_t* const pbuf0 = base_ptr + lay.off_p;
+        uint4* const bias_rows = reinterpret_cast<uint4*>(base_ptr + lay.off_bias + 2048);
         const float sl2 = L.scale_log2;
+        // Warpgroup-uniform state: `pending` while some column of this warpgroup
+        // has no running max yet; bit b of `dirty` while bias[b] (the stabiliser
+        // GEMM1 folds into S buffer b) differs from the running max.
+        bool pending = true;
+        uint32_t dirty = 0;
         for (int t = 0; t < ntiles; ++t) {
             const int sb = t & 1;
             const TileInfo ti = s_tiles[t];
@@ -584,16 +659,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 }
                 continue;
             }
-            const uint32_t tS = tS0 + 128 * sb + lane_off + c0;
             float x[kCols];
-            auto load_s = [&]() {
-                uint32_t v[kCols];
-                tmem_ld_cols<kCols>(tS, v);
-                tmem_ld_wait();
-#pragma unroll
-                for (int k = 0; k < kCols; ++k) x[k] = __uint_as_float(v[k]);
-            };
-            load_s();
+            tmem_ld16_f(tS0 + 128 * sb + lane_off + c0, x);
+            tmem_ld16_f(tS0 + 128 * sb + lane_off + c0 + 16, x + 16);
+            tmem_ld_wait();
+            if (DBG && tid == 0) trace(L, t, 12);
             // masks: invalid rows of single-block tiles; causal (attention.hpp:181-190)
             const int key_pos = ti.dblk * kBlock + r;  // diagonal / tail pairs are consecutive blocks
             // rows past a single block or past the end of the tail hold no key
@@ -602,60 +672,62 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             const int c_first = row_valid ? ((L.causal && ti.dblk >= 0) ? key_pos - off - q0 : 0) : 1 << 30;
             // warp-uniform fast path: every (row, column) of this warp visible
             const bool fast = __all_sync(0xffffffffu, c_first <= c0);
-            // x <- s*scale*log2e - m (masked: -inf); does any value exceed m + tau?
-            // (packed f32x2 FMA against -m, 3-input max: half the instructions)
+            // S^T holds s + bias[sb] = s - m_used/(scale log2e), so x = S^T * scale log2e
+            // = s*scale*log2e - m_used: no per-column operand in the steady state
 #pragma unroll
-            for (int k = 0; k < kCols; k += 4) {
-                const float4 n4 = *reinterpret_cast<const float4*>(&s_mneg[c0 + k]);
-                ffma2(x[k], x[k + 1], sl2, n4.x, n4.y);
-                ffma2(x[k + 2], x[k + 3], sl2, n4.z, n4.w);
-            }
+            for (int k = 0; k < kCols; k += 2) ffma2(x[k], x[k + 1], sl2, 0.f, 0.f);
             if (!fast) {
 #pragma unroll
                 for (int k = 0; k < kCols; ++k)
                     if (c0 + k < c_first) x[k] = -INFINITY;
             }
-            float xmax = max3f(x[0], x[1], x[2]);
+            bool slow = pending || ((dirty >> sb) & 1u);
+            if (!slow) {
+                float xmax = max3f(x[0], x[1], x[2]);
 #pragma unroll
-            for (int k = 3; k + 1 < kCols; k += 2) xmax = max3f(xmax, x[k], x[k + 1]);
-            if constexpr (kCols % 2 == 0) xmax = fmaxf(xmax, x[kCols - 1]);
-            if (bar_red_or(bar_id, !(xmax <= kTau))) {
-                // ---- slow path (!(xmax <= tau) also catches a NaN from m = -inf)
-                load_s();
+                for (int k = 3; k + 1 < kCols; k += 2) xmax = max3f(xmax, x[k], x[k + 1]);
+                if constexpr (kCols % 2 == 0) xmax = fmaxf(xmax, x[kCols - 1]);
+                if (DBG && tid == 0) trace(L, t, 13);
+                slow = bar_red_or(bar_id, !(xmax <= kTau));
+            }
+            if (DBG && tid == 0) trace(L, t, 14);
+            if (slow) {
+                // ---- slow path: a column grew past m + tau, a column has no max
+                // yet, or S[sb] was built with a stale stabiliser.  x is relative
+                // to m_used[sb]; the exact column max decides the new m.
 #pragma unroll
-                for (int k = 0; k < kCols; ++k) {
-                    const bool vis = fast || c0 + k >= c_first;
-                    x[k] = vis ? x[k] * sl2 : -INFINITY;  // s*scale*log2e (scale > 0 commutes with max)
-                    s_red[wq][c0 + k] = redux_max(x[k]);
-                }
+                for (int k = 0; k < kCols; ++k) s_red[wq][c0 + k] = redux_max(x[k]);
                 named_bar(bar_id, 128);
-                bool resc = false;
+                bool resc = false, changed = false, pend = false;
                 if (r < kCols) {
                     const int c = c0 + r;
                     const float tm = fmaxf(fmaxf(s_red[0][c], s_red[1][c]), fmaxf(s_red[2][c], s_red[3][c]));
-                    const float mo = s_mrun[c];
+                    const float mu = s_mused[sb][c], mo = s_mrun[c];
+                    const float tabs = tm + mu;  // absolute column max (log2 units)
                     float mnew = mo, alpha = 1.f;
-                    if (tm > -INFINITY && (mo == -INFINITY || tm > mo + kTau)) {
-                        mnew = tm;
+                    if (tm > -INFINITY && (mo == -INFINITY || tabs > mo + kTau)) {
+                        // the stabiliser is what the bias operand can hold exactly
+                        const float b = F16Traits<T>::round(fminf(fmaxf(-tabs / (16.f * sl2), -60000.f), 60000.f));
+                        s_bq[c] = static_cast<uint16_t>(F16Traits<T>::pack(b, b) & 0xFFFFu);
+                        mnew = -16.f * b * sl2;
                         if (mo != -INFINITY) {
                             alpha = fast_exp2(mo - mnew);
                             resc = true;
                         }
+                        changed = true;
                     }
-                    s_mnew[c] = mnew;
+                    s_delta[c] = mnew == -INFINITY ? 0.f : mnew - mu;
                     s_alpha[c] = alpha;
+                    s_mrun[c] = mnew;
+                    pend = mnew == -INFINITY;
                 }
+                changed = bar_red_or(bar_id, changed);
                 resc = bar_red_or(bar_id, resc);
-                if (r < kCols) {
-                    s_mrun[c0 + r] = s_mnew[c0 + r];
-                    s_mneg[c0 + r] = -s_mnew[c0 + r];
-                }
-                // x <- x - m_new (masked stay -inf; columns with no visible key yet stay -inf)
+                pending = bar_red_or(bar_id, pend);
+                if (changed) dirty = 3u;
+                // x <- x - (m_new - m_used): relative to the running max
 #pragma unroll
-                for (int k = 0; k < kCols; ++k) {
-                    const float mn = s_mnew[c0 + k];
-                    x[k] = mn == -INFINITY ? -INFINITY : x[k] - mn;
-                }
+                for (int k = 0; k < kCols; ++k) x[k] -= s_delta[c0 + k];
                 if (resc) {
                     // O^T (GEMM2(t-1) complete) and l rescale for the grown columns
                     if (t >= 1) mbar_wait_dbg(&bar_pempty[pbuf_of(t - 1)], pphase(t - 1), dbgp, 8);
@@ -677,7 +749,19 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                         tmem_st_wait();
                     }
                 }
-                named_bar(bar_id, 128);  // s_mnew / s_alpha reads done before the next slow path
+                named_bar(bar_id, 128);  // s_red / s_delta / s_alpha reads done before reuse
+            }
+            if ((dirty >> sb) & 1u) {
+                // GEMM1(t+2) reads bias[sb] once every warp released S[sb]: refresh it
+                if (r < kCols) {
+                    const int c = c0 + r;
+                    const uint32_t w = s_bq[c] * 0x10001u;
+                    bias_rows[sb * 128 + c] = make_uint4(w, w, w, w);
+                    const float m = s_mrun[c];
+                    s_mused[sb][c] = m == -INFINITY ? 0.f : m;  // no max yet: bias 0
+                    fence_async_smem();
+                }
+                dirty &= ~(1u << sb);
             }
             tc_fence_before();
             __syncwarp();
@@ -708,12 +792,20 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 }
                 float p[8];
 #pragma unroll
+#ifdef HS_AB_NO_EXP
+                for (int k = 0; k < 8; ++k) p[k] = x[8 * g8 + k] * 0.001f;  // A/B timing only
+#else
                 for (int k = 0; k < 8; ++k) p[k] = fast_exp2(x[8 * g8 + k]);  // exp2(-inf) = 0
+#endif
 #pragma unroll
                 for (int k = 0; k < 8; k += 2) fadd2(l_part[8 * g8 + k], l_part[8 * g8 + k + 1], p[k], p[k + 1]);
                 const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
                                             F16Traits<T>::pack(p[4], p[5]), F16Traits<T>::pack(p[6], p[7]));
+#ifdef HS_AB_NO_PST
+                if (hi.x == 0x12345u) *reinterpret_cast<uint4*>(pbuf + pt_chunk_off(r, q8)) = hi;  // A/B only
+#else
                 *reinterpret_cast<uint4*>(pbuf + pt_chunk_off(r, q8)) = hi;
+#endif
                 if (HILO) {
                     float rr[8];
 #pragma unroll
@@ -786,7 +878,7 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     lay.off_q = 0;
     lay.off_p = 32768;
     lay.p_bytes = hilo ? 65536u : 32768u;  // P^T (hi [+ lo]) per buffer
-    const uint32_t budget = 227u * 1024u - 8192u /*static smem*/ - 1024u /*align*/ - tiles_bytes;
+    const uint32_t budget = 227u * 1024u - 8192u /*static smem*/ - 1024u /*align*/ - tiles_bytes - kBiasBytes;
     // Preference order: 2 K + 2 V stages with two P^T buffers, then fewer P^T
     // buffers, then shallower rings.
     // V(t) is consumed a softmax period after K(t), so one V stage is enough to
@@ -817,7 +909,8 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     lay.off_k = lay.off_p + lay.n_pbuf * lay.p_bytes;
     lay.off_v = lay.off_k + lay.nk * lay.k_stage;
     lay.off_tiles = lay.off_v + lay.nv * lay.v_stage;
-    size_t smem = lay.off_tiles + tiles_bytes + 1024;
+    lay.off_bias = lay.off_tiles + tiles_bytes;
+    size_t smem = lay.off_bias + kBiasBytes + 1024;
     const size_t epi = lay.off_p + kSoftWG * 128 * (kCols + 1) * 4 + 1024;
     if (smem < epi) smem = epi;
     {
