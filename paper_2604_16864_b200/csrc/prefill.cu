@@ -141,6 +141,32 @@ __device__ __forceinline__ float max3f(float a, float b, float c) {
     return r;
 }
 
+// 2^x on the FMA pipe for x <= tau (+inf excluded, -inf -> 0): round-to-nearest
+// split x = j + f (magic-number add), degree-5 minimax-style polynomial for 2^f on
+// [-1/2, 1/2] (relative error ~2e-7, below fp16/bf16 P rounding), 2^j by an
+// integer add into the exponent field.  Offloads the MUFU / MIO queue, which the
+// exponentials otherwise saturate (ncu: MUFU.EX2 stalls on mio).
+__device__ __forceinline__ float exp2_fma(float x) {
+    x = fmaxf(x, -127.f);
+    const float y = x + 12582912.f;  // 1.5 * 2^23: j in the low mantissa bits
+    const float j = y - 12582912.f;
+    const float f = x - j;
+    float p = 1.3333558e-3f;
+    p = fmaf(p, f, 9.6181291e-3f);
+    p = fmaf(p, f, 5.5504109e-2f);
+    p = fmaf(p, f, 2.4022651e-1f);
+    p = fmaf(p, f, 6.9314718e-1f);
+    p = fmaf(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(y) << 23));
+}
+#ifndef HS_PREFILL_POLY
+#define HS_PREFILL_POLY 2  // of every 8 exponentials, this many run on the FMA pipe
+#endif
+constexpr int kPolyPer8 = HS_PREFILL_POLY;
+#ifndef HS_PREFILL_LAG
+#define HS_PREFILL_LAG 0  // tools: g8 step of tile 0 at which warpgroups 2-3 may start (0 = no lag)
+#endif
+
 #ifndef HS_PREFILL_EXP_F16X2
 #define HS_PREFILL_EXP_F16X2 0  // sm_100a splits f16x2 ex2 into two MUFU ops: no gain
 #endif
@@ -250,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bar_q, bar_kfull[4], bar_kempty[4];
     __shared__ __align__(8) uint64_t bar_vfull[4], bar_vempty[4];
-    __shared__ __align__(8) uint64_t bar_sfull[2], bar_sempty[2], bar_pfull[2], bar_pempty[2];
+    __shared__ __align__(8) uint64_t bar_sfull[2], bar_sempty[2], bar_pfull[2], bar_pempty[2], bar_lag;
     __shared__ uint32_t s_tmem;
     __shared__ int s_ntiles;
     __shared__ float s_red[4][128];
@@ -292,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             mbar_init(&bar_pfull[i], kSoftWarps);
             mbar_init(&bar_pempty[i], 1);
         }
+        mbar_init(&bar_lag, 8);
         fence_barrier_init();
     }
     if (warp == kWarpK) {
@@ -647,6 +674,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         for (int t = 0; t < ntiles; ++t) {
             const int sb = t & 1;
             const TileInfo ti = s_tiles[t];
+#if HS_PREFILL_LAG
+            // warpgroups 2-3 start half a tile behind 0-1 (once): the two halves
+            // of every SM sub-partition then run different phases of the tile
+            if (t == 0 && wg >= 2) mbar_wait(&bar_lag, 0);
+#endif
             mbar_wait_dbg(&bar_sfull[sb], (t >> 1) & 1, dbgp, 5);
             tc_fence_after();
             if (DBG && tid == 0) trace(L, t, 0);
@@ -774,6 +806,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             uint8_t* const pbuf = pbuf0 + pbuf_of(t) * lay.p_bytes;
 #pragma unroll
             for (int g8 = 0; g8 < kCols / 8; ++g8) {
+#if HS_PREFILL_LAG
+                if (g8 == HS_PREFILL_LAG && t == 0 && wg < 2) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bar_lag);
+                }
+#endif
                 const int q8 = (c0 >> 3) + g8;  // 8-query chunk index in 0..15
                 if constexpr (!HILO && kExpF16x2) {
                     // fp16 P: two exponentials per MUFU op (ex2.approx.f16x2 on x
@@ -795,7 +833,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
 #ifdef HS_AB_NO_EXP
                 for (int k = 0; k < 8; ++k) p[k] = x[8 * g8 + k] * 0.001f;  // A/B timing only
 #else
-                for (int k = 0; k < 8; ++k) p[k] = fast_exp2(x[8 * g8 + k]);  // exp2(-inf) = 0
+                for (int k = 0; k < 8; ++k)  // exp2(-inf) = 0
+                    p[k] = k < 8 - kPolyPer8 ? fast_exp2(x[8 * g8 + k]) : exp2_fma(x[8 * g8 + k]);
 #endif
 #pragma unroll
                 for (int k = 0; k < 8; k += 2) fadd2(l_part[8 * g8 + k], l_part[8 * g8 + k + 1], p[k], p[k + 1]);
