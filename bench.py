@@ -189,6 +189,7 @@ def build_workload(args, hs, dev, rank, world, scale):
     kcs, vcs = [], []
     comp_ms = []
     comp_bytes = 0
+    rc_ms, rc_bytes = [], 0
     for c0 in range(0, units, chunk):
         n = min(chunk, units - c0)
         key = torch.randn((n, L_ctx, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
@@ -203,6 +204,20 @@ def build_workload(args, hs, dev, rank, world, scale):
                 torch.cuda.synchronize()
                 comp_ms.append(e0.elapsed_time(e1))
             comp_bytes = 2 * key.numel() * 2 + kc0.nbytes() + vc0.nbytes() + 2 * n * kc0.logical_blocks * (8 + 1 + 4)
+            # decode-phase re-prune (pipeline.hpp:227-240) of prefill-sparsity caches
+            # (S = 0.5) to the decode sparsity, fused over the compressed pools
+            kp, vp = hs.prune_cache(key, val, hs.SparsityConfig(0.5, 0.5, 64))
+            for _ in range(3):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                k2, v2 = hs.recompress(kp, cfg, cfg.s_key), hs.recompress(vp, cfg, cfg.s_value)
+                e1.record()
+                torch.cuda.synchronize()
+                rc_ms.append(e0.elapsed_time(e1))
+            rc_bytes = (kp.nbytes() + vp.nbytes() + k2.nbytes() + v2.nbytes() +
+                        2 * n * k2.logical_blocks * (8 + 1 + 4))
+            del kp, vp, k2, v2
             kcs.append(kc0)
             vcs.append(vc0)
         else:
@@ -214,7 +229,7 @@ def build_workload(args, hs, dev, rank, world, scale):
     _, bytes_u = hs.flop_and_byte_count(GQA, kcs[0], vcs[0], 0, False)
     step_bytes = units * bytes_u
     wl = {"kc": kcs[0], "vc": vcs[0], "q": q, "bytes": step_bytes, "config": desc, "scaling": scaling,
-          "comp_ms": comp_ms, "comp_bytes": comp_bytes, "plan": None}
+          "comp_ms": comp_ms, "comp_bytes": comp_bytes, "rc_ms": rc_ms, "rc_bytes": rc_bytes, "plan": None}
     if args.workload == "config5":
         last = rank == world - 1
 
@@ -381,6 +396,10 @@ def run_ours(args):
                 "call": wl["e2e_name"]},
         "compress": {"ms": round(min(comp_ms), 4), "gbs": round(comp_bytes / (min(comp_ms) * 1e-3) / 1e9, 2),
                      "bytes": int(comp_bytes)},
+        "recompress": {"from_s": 0.5, "to_s": 1.0, "ms": round(min(wl["rc_ms"]), 4),
+                       "gbs": round(wl["rc_bytes"] / (min(wl["rc_ms"]) * 1e-3) / 1e9, 2),
+                       "bytes": int(wl["rc_bytes"]), "call": "hierasparse.recompress x2 (hs_recompress, one pass)"}
+        if wl.get("rc_ms") else None,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,

@@ -9,6 +9,7 @@
  *   prune_cache + fused_magnitude_compress   -> hs_prune_compress
  *   fused_magnitude_compress (given mask)    -> hs_compress_with_flags
  *   decompress                               -> hs_decompress
+ *   decompress -> prune_cache -> compress     -> hs_recompress (pipeline.hpp:227-240)
  *   decode_attention                         -> hs_decode
  *   attend_range over a block range / LSE combine -> hs_decode_partial / hs_decode_combine
  *   prefill_attention                        -> hs_prefill
@@ -134,6 +135,16 @@ HS_API hs_status hs_prune_compress(const void* src, uint64_t src_unit_stride, ui
  * sparse_count must equal the flag counts. */
 HS_API hs_status hs_compress_with_flags(const void* src, uint64_t src_unit_stride, uint64_t rows,
                                         const uint8_t* flags, hs_device_cache* out, void* stream);
+
+/* Decode-phase re-prune of an already compressed cache (pipeline.hpp:227-240:
+ * decompress -> prune_cache at the decode sparsity -> compress) in one pass over
+ * the input pools: blocks are expanded on the fly, never written dense to HBM.
+ * Results are bit-identical to hs_decompress followed by hs_prune_compress;
+ * a corrupt input returns HS_ERR_DATA with decompress's messages.  in and out
+ * share axis, dtype, units and shape; out's pools are sized by hs_pool_counts
+ * for rows = in->logical_blocks * block_size. */
+HS_API hs_status hs_recompress(const hs_device_cache* in, const hs_sparsity_config* cfg, double sparsity,
+                               hs_device_cache* out, double* losses, uint8_t* flags, void* stream);
 
 /* decompress (compressed_cache.hpp:271-298): dst dtype [n_units][rows][d]. */
 HS_API hs_status hs_decompress(const hs_device_cache* c, void* dst, void* stream);

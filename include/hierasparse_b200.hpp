@@ -246,6 +246,20 @@ inline void decompress(const DeviceCompressedCache& c, void* dst, cudaStream_t s
     check(hs_decompress(&c.desc(), dst, stream));
 }
 
+// Decode-phase re-prune (pipeline.hpp:227-240: decompress -> prune_cache at the
+// decode sparsity -> compress) in one pass over c's pools.
+inline DeviceCompressedCache recompress(const DeviceCompressedCache& c, const SparsityConfig& cfg, double sparsity,
+                                        cudaStream_t stream = nullptr) {
+    const hs_device_cache& in = c.desc();
+    const PoolCounts p = pool_counts(static_cast<std::size_t>(in.logical_blocks) * in.block_size, cfg, sparsity);
+    DeviceCompressedCache out(static_cast<DType>(in.dtype), static_cast<GroupAxis>(in.axis), in.n_units,
+                              p.logical_blocks, p.dense_count, p.sparse_count, in.head_dim,
+                              static_cast<uint32_t>(cfg.block_size));
+    const hs_sparsity_config cc = cfg.c();
+    check(hs_recompress(&in, &cc, sparsity, &out.desc(), out.losses(), out.flags(), stream));
+    return out;
+}
+
 // -------------------------------------------------------------- attention ---
 // decode_attention (attention.hpp:360-409): q [n_units][gqa][d] -> out fp32.
 inline void decode_attention(const void* q, const DeviceCompressedCache& k, const DeviceCompressedCache& v,

@@ -327,11 +327,11 @@ HS_API hs_status hs_cache_bytes(const hs_device_cache* c, uint64_t* index_bytes,
     return HS_OK;
 }
 
-HS_API hs_status hs_prune_compress(const void* src, uint64_t src_unit_stride, uint64_t rows,
-                                   const hs_sparsity_config* cfg, double sparsity,
-                                   hs_device_cache* out, double* losses, uint8_t* flags,
-                                   void* stream) {
-    HS_CHECK_CONFIG(out != nullptr && src != nullptr, "prune_cache: null argument");
+static hs_status prune_compress_common(const void* src, uint64_t src_unit_stride, uint64_t rows,
+                                       const hs_sparsity_config* cfg, double sparsity,
+                                       hs_device_cache* out, double* losses, uint8_t* flags,
+                                       void* stream, const hs_device_cache* in) {
+    HS_CHECK_CONFIG(out != nullptr && (src != nullptr || in != nullptr), "prune_cache: null argument");
     uint32_t nb, dc, sc, pre, suf, quota;
     hs_status st = pool_counts(rows, cfg, sparsity, &nb, &dc, &sc, &pre, &suf, &quota);
     if (st) return st;
@@ -343,7 +343,7 @@ HS_API hs_status hs_prune_compress(const void* src, uint64_t src_unit_stride, ui
                     "prune_cache: pool counts (%u, %u) do not match the selection (%u, %u)",
                     out->dense_count, out->sparse_count, dc, sc);
     if ((st = check_device_cache(out, "prune_cache"))) return st;
-    HS_CHECK_CONFIG(out->n_units == 1 || src_unit_stride >= rows * out->head_dim,
+    HS_CHECK_CONFIG(in != nullptr || out->n_units == 1 || src_unit_stride >= rows * out->head_dim,
                     "prune_cache: unit stride too small");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool static_sel = quota == 0 || quota == nb - pre - suf;
@@ -377,10 +377,51 @@ HS_API hs_status hs_prune_compress(const void* src, uint64_t src_unit_stride, ui
         if (!losses) L.losses = reinterpret_cast<double*>(ws);
         L.flags_tmp = ws + need_l;
     }
+    if (in) {
+        L.in_index = in->index_map;
+        L.in_dense_count = static_cast<int>(in->dense_count);
+        L.in_sparse_count = static_cast<int>(in->sparse_count);
+        L.in_dense = in->dense_pool;
+        L.in_nnz = in->nnz_pool;
+        L.in_meta = in->meta_pool;
+        L.bad = static_cast<int*>(workspace(s, 64, kWsMisc, &st));
+        if (st) return st;
+        cudaMemsetAsync(L.bad, 0, sizeof(int), s);
+    }
     cudaError_t e = hs::launch_prune_compress(L, s);
     count_launch(static_sel ? 2 : 4);
     if (e != cudaSuccess) return cuda_fail(e, "prune_compress launch");
+    if (in) {
+        // decompress's DataError semantics for a corrupt input cache
+        int hbad = 0;
+        e = cudaMemcpyAsync(&hbad, L.bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_fail(e, "recompress");
+        if (hbad == 1) return fail(HS_ERR_DATA, "decompress: index map holds a zero or dangling entry");
+        if (hbad == 2) return fail(HS_ERR_DATA, "unpack_metadata: corrupt metadata, codes not increasing");
+    }
     return HS_OK;
+}
+
+HS_API hs_status hs_prune_compress(const void* src, uint64_t src_unit_stride, uint64_t rows,
+                                   const hs_sparsity_config* cfg, double sparsity,
+                                   hs_device_cache* out, double* losses, uint8_t* flags,
+                                   void* stream) {
+    HS_CHECK_CONFIG(src != nullptr, "prune_cache: null argument");
+    return prune_compress_common(src, src_unit_stride, rows, cfg, sparsity, out, losses, flags, stream, nullptr);
+}
+
+HS_API hs_status hs_recompress(const hs_device_cache* in, const hs_sparsity_config* cfg, double sparsity,
+                               hs_device_cache* out, double* losses, uint8_t* flags, void* stream) {
+    HS_CHECK_CONFIG(in != nullptr && out != nullptr, "recompress: null argument");
+    hs_status st = check_device_cache(in, "recompress");
+    if (st) return st;
+    HS_CHECK_CONFIG(in != out && in->index_map != out->index_map, "recompress: output aliases the input cache");
+    HS_CHECK_CONFIG(in->axis == out->axis && in->dtype == out->dtype && in->n_units == out->n_units &&
+                        in->head_dim == out->head_dim && in->block_size == out->block_size,
+                    "recompress: input and output caches differ in axis, dtype, units or shape");
+    return prune_compress_common(nullptr, 0, static_cast<uint64_t>(in->logical_blocks) * in->block_size, cfg,
+                                 sparsity, out, losses, flags, stream, in);
 }
 
 HS_API hs_status hs_compress_with_flags(const void* src, uint64_t src_unit_stride, uint64_t rows,

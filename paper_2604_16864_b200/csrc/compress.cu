@@ -153,9 +153,10 @@ __device__ __forceinline__ const uint16_t* unit_src(const uint16_t* src, uint64_
 }
 
 // Sequential reference-order loss (pruner.hpp:85-87) for the rare blocks whose
-// exponent spread defeats the exact-sum bound.  Logical row-major order.
-template <typename T, int AXIS>
-__device__ double sequential_loss(const uint16_t* blk /*[64][128] logical*/) {
+// exponent spread defeats the exact-sum bound.  Logical row-major order;
+// at(r, c) returns the logical element.
+template <typename T, int AXIS, typename At>
+__device__ double sequential_loss_at(At at) {
     double loss = 0.0;
     for (int r = 0; r < kBlock; ++r) {
         for (int c = 0; c < kHeadDim; ++c) {
@@ -163,19 +164,23 @@ __device__ double sequential_loss(const uint16_t* blk /*[64][128] logical*/) {
             int pos;
             if (AXIS == 0) {
                 const int g0 = c & ~3;
-                for (int i = 0; i < 4; ++i) m[i] = mag16(blk[r * kHeadDim + g0 + i]);
+                for (int i = 0; i < 4; ++i) m[i] = mag16(at(r, g0 + i));
                 pos = c & 3;
             } else {
                 const int r0 = r & ~3;
-                for (int i = 0; i < 4; ++i) m[i] = mag16(blk[(r0 + i) * kHeadDim + c]);
+                for (int i = 0; i < 4; ++i) m[i] = mag16(at(r0 + i, c));
                 pos = r & 3;
             }
             const uint32_t keep = keep_mask4(m[0], m[1], m[2], m[3]);
             if (!((keep >> pos) & 1u))
-                loss += fabs(static_cast<double>(F16Traits<T>::to_float(blk[r * kHeadDim + c])));
+                loss += fabs(static_cast<double>(F16Traits<T>::to_float(at(r, c))));
         }
     }
     return loss;
+}
+template <typename T, int AXIS>
+__device__ double sequential_loss(const uint16_t* blk /*[64][128] logical*/) {
+    return sequential_loss_at<T, AXIS>([&](int r, int c) { return blk[r * kHeadDim + c]; });
 }
 
 // ---------------------------------------------------------------------------
@@ -192,14 +197,77 @@ struct PackArgs {
     uint16_t* nnz_pool;
     uint16_t* meta_pool;
     double* losses;           // [u][nb] (modes 0, 2)
+    // SRC 1: the source is itself a compressed cache of the same geometry
+    // (decode-phase re-prune, pipeline.hpp:227-240): blocks are expanded on the
+    // fly (decompress semantics, compressed_cache.hpp:271-298), never
+    // materialised dense in HBM.
+    const int16_t* in_index;
+    int in_dense_count, in_sparse_count;
+    const uint16_t* in_dense;
+    const uint16_t* in_nnz;
+    const uint16_t* in_meta;
+    int* bad;                 // 1: zero / dangling index entry, 2: codes not increasing
 };
 
-template <typename T, int AXIS, int MODE>
+// One stored 2:4 group (kept pair word, 4-bit code) back to its four logical
+// values as two packed words (expand_sparse, nm_metadata.hpp:119-143).
+__device__ __forceinline__ void expand_group(uint32_t kept, uint32_t code, uint32_t& lo, uint32_t& hi,
+                                             bool& bad) {
+    const uint32_t p0 = code & 3u, p1 = code >> 2, klo = kept & 0xFFFFu, khi = kept >> 16;
+    bad |= p1 <= p0;
+    auto at = [&](uint32_t i) { return i == p0 ? klo : (i == p1 ? khi : 0u); };
+    lo = at(0) | (at(1) << 16);
+    hi = at(2) | (at(3) << 16);
+}
+
+// Logical element (r, c) of input block b of unit u (decompress semantics,
+// compressed_cache.hpp:271-298; invalid entries read as zero).
+template <int AXIS>
+__device__ uint16_t logical_in(const PackArgs& a, int u, int b, int r, int c) {
+    const int e = a.in_index[static_cast<int64_t>(u) * a.nb + b];
+    const int slot = (e > 0 ? e : -e) - 1;
+    if (e == 0 || (e > 0 && slot >= a.in_dense_count) || (e < 0 && slot >= a.in_sparse_count)) return 0;
+    const int sr = AXIS == 0 ? r : c, sc = AXIS == 0 ? c : r;
+    const int scols = AXIS == 0 ? kHeadDim : kBlock;
+    if (e > 0) return a.in_dense[(static_cast<uint64_t>(u) * a.in_dense_count + slot) * (kBlock * kHeadDim) + sr * scols + sc];
+    const uint64_t sb = static_cast<uint64_t>(u) * a.in_sparse_count + slot;
+    const uint16_t* nnz = a.in_nnz + sb * (kBlock * kHeadDim / 2) + sr * (scols / 2);
+    const uint16_t* meta = a.in_meta + sb * (kBlock * kHeadDim / 16) + sr * (scols / 16);
+    const int g = sc >> 2, pos = sc & 3;
+    const uint32_t code = (meta[g >> 2] >> (4 * (g & 3))) & 0xF;
+    const int p0 = code & 3, p1 = code >> 2;
+    return pos == p0 ? nnz[2 * g] : (pos == p1 ? nnz[2 * g + 1] : static_cast<uint16_t>(0));
+}
+template <typename T, int AXIS>
+__device__ double sequential_loss_in(const PackArgs& a, int u, int b) {
+    return sequential_loss_at<T, AXIS>([&](int r, int c) { return logical_in<AXIS>(a, u, b, r, c); });
+}
+
+template <typename T, int AXIS, int MODE, int SRC>
 __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
     const int b = blockIdx.x, u = blockIdx.y, t = threadIdx.x;
-    const uint16_t* blk = unit_src(a.src, a.src_stride, u) + static_cast<uint64_t>(b) * kBlock * kHeadDim;
+    const uint16_t* blk = SRC == 0 ? unit_src(a.src, a.src_stride, u) + static_cast<uint64_t>(b) * kBlock * kHeadDim
+                                   : nullptr;
     __shared__ double s_sum[kThreads / 32];
     __shared__ int s_emin[kThreads / 32], s_emax[kThreads / 32];
+    // SRC 1: the input block (dense slot or nnz + metadata of a sparse slot)
+    int in_e = 0;
+    const uint16_t *in_den = nullptr, *in_nnz = nullptr, *in_meta = nullptr;
+    bool in_bad = false;
+    if (SRC == 1) {
+        in_e = a.in_index[static_cast<int64_t>(u) * a.nb + b];
+        const int slot = (in_e > 0 ? in_e : -in_e) - 1;
+        if (in_e == 0 || (in_e > 0 && slot >= a.in_dense_count) || (in_e < 0 && slot >= a.in_sparse_count)) {
+            if (t == 0) atomicExch(a.bad, 1);
+            in_e = 0;  // read as zeros
+        } else if (in_e > 0) {
+            in_den = a.in_dense + (static_cast<uint64_t>(u) * a.in_dense_count + slot) * (kBlock * kHeadDim);
+        } else {
+            const uint64_t sb = static_cast<uint64_t>(u) * a.in_sparse_count + slot;
+            in_nnz = a.in_nnz + sb * (kBlock * kHeadDim / 2);
+            in_meta = a.in_meta + sb * (kBlock * kHeadDim / 16);
+        }
+    }
 
     bool dense = false;
     int slot = 0;
@@ -217,7 +285,20 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
             const int r = p * 16 + (t >> 4);
-            const uint4 v = *reinterpret_cast<const uint4*>(blk + r * kHeadDim + c * 8);
+            uint4 v;
+            if (SRC == 0) {
+                v = *reinterpret_cast<const uint4*>(blk + r * kHeadDim + c * 8);
+            } else if (in_e > 0) {
+                v = *reinterpret_cast<const uint4*>(in_den + r * kHeadDim + c * 8);
+            } else if (in_e < 0) {
+                // stored K row r: groups 2c, 2c+1 at nnz[4c..4c+3], codes in metadata byte c
+                const uint2 kp = *reinterpret_cast<const uint2*>(in_nnz + r * (kHeadDim / 2) + c * 4);
+                const uint32_t mb = reinterpret_cast<const uint8_t*>(in_meta + r * (kHeadDim / 16))[c];
+                expand_group(kp.x, mb & 0xFu, v.x, v.y, in_bad);
+                expand_group(kp.y, mb >> 4, v.z, v.w, in_bad);
+            } else {
+                v = make_uint4(0u, 0u, 0u, 0u);
+            }
             if (MODE != 0 && dense) {
                 uint16_t* dst = a.dense_pool + (static_cast<uint64_t>(u) * a.dense_count + slot) * (kBlock * kHeadDim);
                 *reinterpret_cast<uint4*>(dst + r * kHeadDim + c * 8) = v;
@@ -240,14 +321,46 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
     } else {
         // Value cache: groups of 4 tokens down a channel; stored transposed [d][B].
         __shared__ __align__(16) uint16_t tile[kBlock * kHeadDim];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int chunk = t + i * kThreads;  // 1024 chunks of 8 elements
-            reinterpret_cast<uint4*>(tile)[chunk] = reinterpret_cast<const uint4*>(blk)[chunk];
-        }
-        __syncthreads();
         const int c = t & 127;  // channel
         const int h = t >> 7;   // token half: groups 8h..8h+7
+        if (SRC == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int chunk = t + i * kThreads;  // 1024 chunks of 8 elements
+                reinterpret_cast<uint4*>(tile)[chunk] = reinterpret_cast<const uint4*>(blk)[chunk];
+            }
+        } else if (in_e > 0) {
+            // stored V^T [d][B]: channel c, tokens 32h..32h+31
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 w = *reinterpret_cast<const uint4*>(in_den + c * kBlock + 32 * h + 8 * q);
+                const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    tile[(32 * h + 8 * q + 2 * j) * kHeadDim + c] = static_cast<uint16_t>(ws[j] & 0xFFFFu);
+                    tile[(32 * h + 8 * q + 2 * j + 1) * kHeadDim + c] = static_cast<uint16_t>(ws[j] >> 16);
+                }
+            }
+        } else {
+            // stored channel c: token groups 8h..8h+7 at nnz[16h..16h+15], codes in 2 words
+            uint32_t kv[8];
+            const uint4 k0 = *reinterpret_cast<const uint4*>(in_nnz + c * (kBlock / 2) + 16 * h);
+            const uint4 k1 = *reinterpret_cast<const uint4*>(in_nnz + c * (kBlock / 2) + 16 * h + 8);
+            kv[0] = k0.x; kv[1] = k0.y; kv[2] = k0.z; kv[3] = k0.w;
+            kv[4] = k1.x; kv[5] = k1.y; kv[6] = k1.z; kv[7] = k1.w;
+            const uint32_t codes = in_e < 0 ? *reinterpret_cast<const uint32_t*>(in_meta + c * (kBlock / 16) + 2 * h) : 0u;
+#pragma unroll
+            for (int gi = 0; gi < 8; ++gi) {
+                uint32_t lo = 0u, hi = 0u;
+                if (in_e < 0) expand_group(kv[gi], (codes >> (4 * gi)) & 0xFu, lo, hi, in_bad);
+                const int r0 = 32 * h + 4 * gi;
+                tile[r0 * kHeadDim + c] = static_cast<uint16_t>(lo & 0xFFFFu);
+                tile[(r0 + 1) * kHeadDim + c] = static_cast<uint16_t>(lo >> 16);
+                tile[(r0 + 2) * kHeadDim + c] = static_cast<uint16_t>(hi & 0xFFFFu);
+                tile[(r0 + 3) * kHeadDim + c] = static_cast<uint16_t>(hi >> 16);
+            }
+        }
+        __syncthreads();
         if (MODE != 0 && dense) {
             uint16_t* dst = a.dense_pool + (static_cast<uint64_t>(u) * a.dense_count + slot) * (kBlock * kHeadDim) +
                             c * kBlock + 32 * h;
@@ -286,11 +399,15 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
         }
     }
 
+    if (SRC == 1 && in_bad) atomicExch(a.bad, 2);
     if (kLoss) {
         const bool exact = loss_reduce<T>(acc, s_sum, s_emin, s_emax);
         if (t == 0) {
             double loss = acc.sum;
-            if (!exact) loss = sequential_loss<T, AXIS>(blk);
+            // (SRC 1: every stored 2:4 group keeps its two largest magnitudes and
+            // zeros elsewhere, so the pruned terms of the re-prune are those of a
+            // decompressed block; the rare inexact case re-expands it)
+            if (!exact) loss = SRC == 0 ? sequential_loss<T, AXIS>(blk) : sequential_loss_in<T, AXIS>(a, u, b);
             a.losses[static_cast<int64_t>(u) * a.nb + b] = loss;
         }
     }
@@ -419,17 +536,22 @@ __global__ void __launch_bounds__(kThreads) decompress_kernel(const int16_t* ind
 }  // namespace
 
 // ----------------------------------------------------------------- launchers
-template <typename T>
-static cudaError_t launch_block_kernel(int axis, int mode, const PackArgs& a, int n_units,
-                                       cudaStream_t s) {
+template <typename T, int SRC>
+static void launch_block_kernel_src(int axis, int mode, const PackArgs& a, int n_units, cudaStream_t s) {
     const dim3 grid(a.nb, n_units);
-#define HS_LAUNCH(AX, MD) block_kernel<T, AX, MD><<<grid, kThreads, 0, s>>>(a)
+#define HS_LAUNCH(AX, MD) block_kernel<T, AX, MD, SRC><<<grid, kThreads, 0, s>>>(a)
     if (axis == 0) {
         if (mode == 0) HS_LAUNCH(0, 0); else if (mode == 1) HS_LAUNCH(0, 1); else HS_LAUNCH(0, 2);
     } else {
         if (mode == 0) HS_LAUNCH(1, 0); else if (mode == 1) HS_LAUNCH(1, 1); else HS_LAUNCH(1, 2);
     }
 #undef HS_LAUNCH
+}
+template <typename T>
+static cudaError_t launch_block_kernel(int axis, int mode, const PackArgs& a, int n_units,
+                                       cudaStream_t s) {
+    if (a.in_index) launch_block_kernel_src<T, 1>(axis, mode, a, n_units, s);
+    else launch_block_kernel_src<T, 0>(axis, mode, a, n_units, s);
     return cudaGetLastError();
 }
 
@@ -445,6 +567,13 @@ cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
     a.nnz_pool = static_cast<uint16_t*>(L.nnz_pool);
     a.meta_pool = L.meta_pool;
     a.losses = L.losses;
+    a.in_index = L.in_index;
+    a.in_dense_count = L.in_dense_count;
+    a.in_sparse_count = L.in_sparse_count;
+    a.in_dense = static_cast<const uint16_t*>(L.in_dense);
+    a.in_nnz = static_cast<const uint16_t*>(L.in_nnz);
+    a.in_meta = L.in_meta;
+    a.bad = L.bad;
     auto blocks = [&](int mode) {
         return L.bf16 ? launch_block_kernel<__nv_bfloat16>(L.axis, mode, a, L.n_units, s)
                       : launch_block_kernel<__half>(L.axis, mode, a, L.n_units, s);

@@ -30,6 +30,13 @@ struct CompressLaunch {
     void* dense_pool;
     void* nnz_pool;
     uint16_t* meta_pool;
+    // compressed source (decode-phase re-prune); in_index == nullptr: dense src
+    const int16_t* in_index;
+    int in_dense_count, in_sparse_count;
+    const void* in_dense;
+    const void* in_nnz;
+    const uint16_t* in_meta;
+    int* bad;
 };
 cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s);
 

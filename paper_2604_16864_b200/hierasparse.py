@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import torch
 
 from . import capi
-from .errors import ConfigError
+from .errors import ConfigError, DataError  # noqa: F401  (re-exported for callers)
 
 BLOCK = 64
 HEAD_DIM = 128
@@ -201,8 +201,22 @@ def recompress(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: float) -
     """The decode-phase re-prune (pipeline.hpp:227-240): decompress
     (compressed_cache.hpp:271-298) -> hierarchical_mask_for at the decode sparsity
     (pruner.hpp:121-158) -> fused_magnitude_compress, for every unit on the
-    device.  Bit-identical to the reference's chain on the same pools (the
-    decompressed cache is exact, so re-pruning sees the same values)."""
+    device, in one pass over the input pools (hs_recompress: blocks are expanded
+    on the fly, the dense cache is never materialised).  Bit-identical to the
+    reference's chain on the same pools."""
+    rows = c.logical_blocks * c.block_size
+    nb, dc, sc, _, _ = pool_counts(rows, cfg, sparsity)
+    out = DeviceCompressedCache(c.dtype, c.axis, c.n_units, nb, dc, sc, c.index_map.device, c.head_dim,
+                                 cfg.block_size, cfg)
+    cin, cout, cc = c.c(), out.c(), cfg.c()
+    capi.check(capi.load().hs_recompress(C.byref(cin), C.byref(cc), sparsity, C.byref(cout),
+                                         out.losses.data_ptr(), out.flags.data_ptr(), _stream()))
+    return out
+
+
+def recompress_unfused(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: float) -> DeviceCompressedCache:
+    """recompress as the reference composes it: decompress to a dense device
+    cache, then prune_compress (the parity check for the fused path)."""
     dense = decompress(c)
     out = prune_compress(dense, cfg, sparsity, c.axis)
     del dense

@@ -9,6 +9,7 @@
 //   2. decode_attention within max-abs 2e-2 / mean-rel 1e-3 (attention.hpp:360)
 //   3. prefill_attention (causal) within the same bar (attention.hpp:323)
 //   4. errors map to the reference taxonomy (errors.hpp:10-25)
+//   5. the fused decode-phase recompress equals decompress -> prune_cache -> compress
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -98,6 +99,25 @@ int main() {
         report(ms.size_idx == gs.size_idx && ms.size_den == gs.size_den && ms.size_nnz == gs.size_nnz &&
                    ms.size_e == gs.size_e,
                "measure_size " + tag);
+
+        // decode-phase re-prune (pipeline.hpp:227-240): decompress -> prune_cache at
+        // S_dec -> compress, against the fused one-pass recompress
+        {
+            ref::SparsityConfig dcfg = rcfg;
+            dcfg.s_key = dcfg.s_value = c.s < 1.0 ? 1.0 : 0.5;
+            const ref::Tensor2D dk = ref::decompress(rk), dv = ref::decompress(rv);
+            const auto dm = ref::prune_cache(dk, dv, dcfg);
+            const ref::CompressedCache rk2 = ref::fused_magnitude_compress(dk, dm.first.block, dcfg,
+                                                                           ref::GroupAxis::kChannel);
+            const ref::CompressedCache rv2 = ref::fused_magnitude_compress(dv, dm.second.block, dcfg,
+                                                                           ref::GroupAxis::kSequence);
+            gpu::SparsityConfig gdec{dcfg.s_key, dcfg.s_value, 64, c.sink, c.window};
+            const auto gk2 = gpu::recompress(gk, gdec, dcfg.s_key);
+            const auto gv2 = gpu::recompress(gv, gdec, dcfg.s_value);
+            gpu::check_cuda(cudaDeviceSynchronize(), "recompress");
+            report(pools_equal(rk2, gk2, c.dt) && pools_equal(rv2, gv2, c.dt),
+                   "decode-phase recompress bit-exact " + tag);
+        }
 
         // decode: 4 GQA rows (pipeline.hpp:247-251)
         ref::Tensor2D q(4, d);

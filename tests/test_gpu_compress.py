@@ -227,3 +227,43 @@ def test_decode_phase_recompress_matches_oracle(hs, port, dtype, s_pre, s_dec):
             dense = port.decompress(device_to_oracle(dev_old, u))
             want = port.prune_compress(dense, OCfg(s_dec, s_dec, 64), axis, s_dec)
             assert_cache_equal(dev_new, u, want, f"recompress axis={axis} unit={u}")
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("s_pre,s_dec", [(0.0, 0.5), (0.5, 0.25), (1.0, 1.0), (0.75, 0.0)])
+def test_fused_recompress_equals_decompress_then_compress(hs, port, dtype, s_pre, s_dec):
+    """hs_recompress (one pass over the input pools) == hs_decompress followed by
+    hs_prune_compress on the device: pools, index map, flags and losses bit for
+    bit, with sink / window protection in play."""
+    import torch
+    U, L = 3, 2048
+    kx = gen_units(port, U, L, 128, 33, 0, dtype)
+    vx = gen_units(port, U, L, 128, 33, 1, dtype)
+    pre = hs.SparsityConfig(s_pre, s_pre, 64, sink_tokens=64, local_window=128)
+    kc, vc = hs.prune_cache(to_torch(kx, dtype), to_torch(vx, dtype), pre)
+    dec = hs.SparsityConfig(s_dec, s_dec, 64, sink_tokens=128, local_window=64)
+    for c in (kc, vc):
+        a = hs.recompress(c, dec, s_dec)
+        b = hs.recompress_unfused(c, dec, s_dec)
+        for name in ("index_map", "dense_pool", "nnz_pool", "meta_pool", "flags"):
+            x, y = getattr(a, name), getattr(b, name)
+            if x.is_floating_point():
+                x, y = x.view(torch.int16), y.view(torch.int16)
+            assert torch.equal(x, y), name
+        if 0.0 < s_dec < 1.0:  # loss-driven selection computes every block's loss
+            assert torch.equal(a.losses, b.losses)
+
+
+def test_recompress_rejects_corrupt_input(hs, port):
+    """A zero index entry or non-increasing codes in the input: decompress's DataError."""
+    U, L = 1, 512
+    kx = gen_units(port, U, L, 128, 5, 0, "bf16")
+    kc = hs.prune_compress(to_torch(kx, "bf16"), hs.SparsityConfig(1.0, 1.0, 64), 1.0, 0)
+    bad = hs.recompress(kc, hs.SparsityConfig(1.0, 1.0, 64), 1.0)
+    bad.index_map[0, 3] = 0
+    with pytest.raises(hs.DataError, match="zero or dangling"):
+        hs.recompress(bad, hs.SparsityConfig(0.5, 0.5, 64), 0.5)
+    bad2 = hs.recompress(kc, hs.SparsityConfig(1.0, 1.0, 64), 1.0)
+    bad2.meta_pool[0, 0, 0] = 0x0003  # first group codes (3, 0): not increasing
+    with pytest.raises(hs.DataError, match="not increasing"):
+        hs.recompress(bad2, hs.SparsityConfig(1.0, 1.0, 64), 1.0)
