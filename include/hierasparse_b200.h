@@ -146,6 +146,19 @@ HS_API hs_status hs_compress_with_flags(const void* src, uint64_t src_unit_strid
 HS_API hs_status hs_recompress(const hs_device_cache* in, const hs_sparsity_config* cfg, double sparsity,
                                hs_device_cache* out, double* losses, uint8_t* flags, void* stream);
 
+/* Dense-tail growth (CacheView::dense_tail attention.hpp:19-31):
+ * the cache re-pruned over its blocks followed by tail_rows (a multiple of
+ * block_size) tail tokens, i.e. prune_cache + compress of
+ * [decompress(in); tail] (pipeline.hpp:227-240 semantics over the longer
+ * sequence), in one pass: input blocks are expanded from the pools, the new
+ * blocks read from tail (dtype [n_units][tail_rows][d], unit stride
+ * tail_unit_stride elements).  out sized by hs_pool_counts for
+ * rows = in->logical_blocks * block_size + tail_rows.  The caller keeps the
+ * tail's remaining (< block_size) tokens as the new dense tail. */
+HS_API hs_status hs_absorb_tail(const hs_device_cache* in, const void* tail, uint64_t tail_unit_stride,
+                                uint64_t tail_rows, const hs_sparsity_config* cfg, double sparsity,
+                                hs_device_cache* out, double* losses, uint8_t* flags, void* stream);
+
 /* decompress (compressed_cache.hpp:271-298): dst dtype [n_units][rows][d]. */
 HS_API hs_status hs_decompress(const hs_device_cache* c, void* dst, void* stream);
 

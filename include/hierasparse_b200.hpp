@@ -260,6 +260,24 @@ inline DeviceCompressedCache recompress(const DeviceCompressedCache& c, const Sp
     return out;
 }
 
+// Dense-tail growth: the cache re-pruned over its blocks followed by tail_rows
+// (whole blocks) of tail tokens tail [n_units][tail_rows][d] (device, unit
+// stride tail_unit_stride elements; 0 = tail_rows * d) in one pass.
+inline DeviceCompressedCache absorb_tail(const DeviceCompressedCache& c, const void* tail, std::size_t tail_rows,
+                                         const SparsityConfig& cfg, double sparsity, cudaStream_t stream = nullptr,
+                                         std::size_t tail_unit_stride = 0) {
+    const hs_device_cache& in = c.desc();
+    const std::size_t rows = static_cast<std::size_t>(in.logical_blocks) * in.block_size + tail_rows;
+    const PoolCounts p = pool_counts(rows, cfg, sparsity);
+    DeviceCompressedCache out(static_cast<DType>(in.dtype), static_cast<GroupAxis>(in.axis), in.n_units,
+                              p.logical_blocks, p.dense_count, p.sparse_count, in.head_dim,
+                              static_cast<uint32_t>(cfg.block_size));
+    const hs_sparsity_config cc = cfg.c();
+    check(hs_absorb_tail(&in, tail, tail_unit_stride ? tail_unit_stride : tail_rows * in.head_dim, tail_rows, &cc,
+                         sparsity, &out.desc(), out.losses(), out.flags(), stream));
+    return out;
+}
+
 // -------------------------------------------------------------- attention ---
 // decode_attention (attention.hpp:360-409): q [n_units][gqa][d] -> out fp32.
 inline void decode_attention(const void* q, const DeviceCompressedCache& k, const DeviceCompressedCache& v,

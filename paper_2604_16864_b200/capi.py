@@ -34,7 +34,7 @@ class DeviceCacheC(C.Structure):
 
 # Exported symbols (every one declared in include/hierasparse_b200.h).
 EXPORTS = ("hs_last_error", "hs_version", "hs_pool_counts", "hs_cache_bytes", "hs_prune_compress",
-           "hs_compress_with_flags", "hs_decompress", "hs_recompress", "hs_decode", "hs_decode_partial",
+           "hs_compress_with_flags", "hs_decompress", "hs_recompress", "hs_absorb_tail", "hs_decode", "hs_decode_partial",
            "hs_decode_combine", "hs_prefill", "hs_kernel_launches")
 
 _lib = None
@@ -60,6 +60,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hs_compress_with_flags": [vp, u64, u64, vp, P(DeviceCacheC), vp],
         "hs_decompress": [P(DeviceCacheC), vp, vp],
         "hs_recompress": [P(DeviceCacheC), P(SparsityConfigC), C.c_double, P(DeviceCacheC), vp, vp, vp],
+        "hs_absorb_tail": [P(DeviceCacheC), vp, u64, u64, P(SparsityConfigC), C.c_double, P(DeviceCacheC), vp, vp,
+                           vp],
         "hs_decode": [vp, P(DeviceCacheC), P(DeviceCacheC), vp, vp, u32, u32, C.c_float, u32, vp, vp],
         "hs_decode_partial": [vp, P(DeviceCacheC), P(DeviceCacheC), vp, vp, u32, u32, C.c_float, u32, u32,
                               i32, vp, vp],

@@ -379,6 +379,7 @@ static hs_status prune_compress_common(const void* src, uint64_t src_unit_stride
     }
     if (in) {
         L.in_index = in->index_map;
+        L.in_nb = static_cast<int>(in->logical_blocks);
         L.in_dense_count = static_cast<int>(in->dense_count);
         L.in_sparse_count = static_cast<int>(in->sparse_count);
         L.in_dense = in->dense_pool;
@@ -411,17 +412,37 @@ HS_API hs_status hs_prune_compress(const void* src, uint64_t src_unit_stride, ui
     return prune_compress_common(src, src_unit_stride, rows, cfg, sparsity, out, losses, flags, stream, nullptr);
 }
 
-HS_API hs_status hs_recompress(const hs_device_cache* in, const hs_sparsity_config* cfg, double sparsity,
-                               hs_device_cache* out, double* losses, uint8_t* flags, void* stream) {
-    HS_CHECK_CONFIG(in != nullptr && out != nullptr, "recompress: null argument");
-    hs_status st = check_device_cache(in, "recompress");
+static hs_status recompress_common(const hs_device_cache* in, const void* tail, uint64_t tail_unit_stride,
+                                   uint64_t tail_rows, const hs_sparsity_config* cfg, double sparsity,
+                                   hs_device_cache* out, double* losses, uint8_t* flags, void* stream,
+                                   const char* what) {
+    HS_CHECK_CONFIG(in != nullptr && out != nullptr, "%s: null argument", what);
+    hs_status st = check_device_cache(in, what);
     if (st) return st;
-    HS_CHECK_CONFIG(in != out && in->index_map != out->index_map, "recompress: output aliases the input cache");
+    HS_CHECK_CONFIG(in != out && in->index_map != out->index_map, "%s: output aliases the input cache", what);
     HS_CHECK_CONFIG(in->axis == out->axis && in->dtype == out->dtype && in->n_units == out->n_units &&
                         in->head_dim == out->head_dim && in->block_size == out->block_size,
-                    "recompress: input and output caches differ in axis, dtype, units or shape");
-    return prune_compress_common(nullptr, 0, static_cast<uint64_t>(in->logical_blocks) * in->block_size, cfg,
+                    "%s: input and output caches differ in axis, dtype, units or shape", what);
+    HS_CHECK_CONFIG(tail_rows % in->block_size == 0, "%s: tail rows %llu are not whole blocks", what,
+                    static_cast<unsigned long long>(tail_rows));
+    HS_CHECK_CONFIG(tail_rows == 0 || tail != nullptr, "%s: null tail", what);
+    HS_CHECK_CONFIG(tail_rows == 0 || in->n_units == 1 || tail_unit_stride >= tail_rows * in->head_dim,
+                    "%s: tail unit stride too small", what);
+    return prune_compress_common(tail, tail_unit_stride,
+                                 static_cast<uint64_t>(in->logical_blocks) * in->block_size + tail_rows, cfg,
                                  sparsity, out, losses, flags, stream, in);
+}
+
+HS_API hs_status hs_recompress(const hs_device_cache* in, const hs_sparsity_config* cfg, double sparsity,
+                               hs_device_cache* out, double* losses, uint8_t* flags, void* stream) {
+    return recompress_common(in, nullptr, 0, 0, cfg, sparsity, out, losses, flags, stream, "recompress");
+}
+
+HS_API hs_status hs_absorb_tail(const hs_device_cache* in, const void* tail, uint64_t tail_unit_stride,
+                                uint64_t tail_rows, const hs_sparsity_config* cfg, double sparsity,
+                                hs_device_cache* out, double* losses, uint8_t* flags, void* stream) {
+    return recompress_common(in, tail, tail_unit_stride, tail_rows, cfg, sparsity, out, losses, flags, stream,
+                             "absorb_tail");
 }
 
 HS_API hs_status hs_compress_with_flags(const void* src, uint64_t src_unit_stride, uint64_t rows,

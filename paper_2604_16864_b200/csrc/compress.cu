@@ -202,6 +202,7 @@ struct PackArgs {
     // fly (decompress semantics, compressed_cache.hpp:271-298), never
     // materialised dense in HBM.
     const int16_t* in_index;
+    int in_nb;                // blocks of the input cache; blocks >= in_nb read src
     int in_dense_count, in_sparse_count;
     const uint16_t* in_dense;
     const uint16_t* in_nnz;
@@ -224,7 +225,7 @@ __device__ __forceinline__ void expand_group(uint32_t kept, uint32_t code, uint3
 // compressed_cache.hpp:271-298; invalid entries read as zero).
 template <int AXIS>
 __device__ uint16_t logical_in(const PackArgs& a, int u, int b, int r, int c) {
-    const int e = a.in_index[static_cast<int64_t>(u) * a.nb + b];
+    const int e = a.in_index[static_cast<int64_t>(u) * a.in_nb + b];
     const int slot = (e > 0 ? e : -e) - 1;
     if (e == 0 || (e > 0 && slot >= a.in_dense_count) || (e < 0 && slot >= a.in_sparse_count)) return 0;
     const int sr = AXIS == 0 ? r : c, sc = AXIS == 0 ? c : r;
@@ -246,7 +247,11 @@ __device__ double sequential_loss_in(const PackArgs& a, int u, int b) {
 template <typename T, int AXIS, int MODE, int SRC>
 __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
     const int b = blockIdx.x, u = blockIdx.y, t = threadIdx.x;
-    const uint16_t* blk = SRC == 0 ? unit_src(a.src, a.src_stride, u) + static_cast<uint64_t>(b) * kBlock * kHeadDim
+    // SRC 1: blocks past the input cache come from the dense source (a tail's
+    // full blocks absorbed into the cache)
+    const bool from_src = SRC == 0 || b >= a.in_nb;
+    const uint16_t* blk = from_src ? unit_src(a.src, a.src_stride, u) +
+                                         static_cast<uint64_t>(b - (SRC == 0 ? 0 : a.in_nb)) * kBlock * kHeadDim
                                    : nullptr;
     __shared__ double s_sum[kThreads / 32];
     __shared__ int s_emin[kThreads / 32], s_emax[kThreads / 32];
@@ -254,8 +259,8 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
     int in_e = 0;
     const uint16_t *in_den = nullptr, *in_nnz = nullptr, *in_meta = nullptr;
     bool in_bad = false;
-    if (SRC == 1) {
-        in_e = a.in_index[static_cast<int64_t>(u) * a.nb + b];
+    if (SRC == 1 && !from_src) {
+        in_e = a.in_index[static_cast<int64_t>(u) * a.in_nb + b];
         const int slot = (in_e > 0 ? in_e : -in_e) - 1;
         if (in_e == 0 || (in_e > 0 && slot >= a.in_dense_count) || (in_e < 0 && slot >= a.in_sparse_count)) {
             if (t == 0) atomicExch(a.bad, 1);
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
         for (int p = 0; p < 4; ++p) {
             const int r = p * 16 + (t >> 4);
             uint4 v;
-            if (SRC == 0) {
+            if (from_src) {
                 v = *reinterpret_cast<const uint4*>(blk + r * kHeadDim + c * 8);
             } else if (in_e > 0) {
                 v = *reinterpret_cast<const uint4*>(in_den + r * kHeadDim + c * 8);
@@ -323,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
         __shared__ __align__(16) uint16_t tile[kBlock * kHeadDim];
         const int c = t & 127;  // channel
         const int h = t >> 7;   // token half: groups 8h..8h+7
-        if (SRC == 0) {
+        if (from_src) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int chunk = t + i * kThreads;  // 1024 chunks of 8 elements
@@ -407,7 +412,7 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
             // (SRC 1: every stored 2:4 group keeps its two largest magnitudes and
             // zeros elsewhere, so the pruned terms of the re-prune are those of a
             // decompressed block; the rare inexact case re-expands it)
-            if (!exact) loss = SRC == 0 ? sequential_loss<T, AXIS>(blk) : sequential_loss_in<T, AXIS>(a, u, b);
+            if (!exact) loss = from_src ? sequential_loss<T, AXIS>(blk) : sequential_loss_in<T, AXIS>(a, u, b);
             a.losses[static_cast<int64_t>(u) * a.nb + b] = loss;
         }
     }
@@ -568,6 +573,7 @@ cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
     a.meta_pool = L.meta_pool;
     a.losses = L.losses;
     a.in_index = L.in_index;
+    a.in_nb = L.in_nb;
     a.in_dense_count = L.in_dense_count;
     a.in_sparse_count = L.in_sparse_count;
     a.in_dense = static_cast<const uint16_t*>(L.in_dense);

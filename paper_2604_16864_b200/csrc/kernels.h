@@ -32,6 +32,7 @@ struct CompressLaunch {
     uint16_t* meta_pool;
     // compressed source (decode-phase re-prune); in_index == nullptr: dense src
     const int16_t* in_index;
+    int in_nb;  // input blocks; blocks >= in_nb come from src (absorbed tail blocks)
     int in_dense_count, in_sparse_count;
     const void* in_dense;
     const void* in_nnz;

@@ -214,6 +214,41 @@ def recompress(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: float) -
     return out
 
 
+def absorb_tail(c: DeviceCompressedCache, tail: torch.Tensor, cfg: SparsityConfig, sparsity: float):
+    """Dense-tail growth during decode: once the dense tail
+    (CacheView::dense_tail, attention.hpp:19-31) holds whole blocks, re-prune the
+    cache over its blocks followed by those tail blocks -- prune_cache + compress
+    of [decompress(c); tail blocks] -- in one pass (hs_absorb_tail).  tail:
+    [units, T, d] tokens after the cache.  Returns (cache, remaining tail of
+    T % block_size tokens); with no whole block the inputs come back unchanged."""
+    U, d, B = c.n_units, c.head_dim, c.block_size
+    tail = tail.reshape(U, -1, d)
+    full = (tail.shape[1] // B) * B
+    if full == 0:
+        return c, tail
+    if tail.dtype != c.dtype:
+        raise ConfigError("absorb_tail: tail dtype differs from the cache")
+    if tail.stride(2) != 1 or tail.stride(1) != d:
+        tail = tail.contiguous()
+    src = tail[:, :full]  # unit stride = the whole tail's; rows contiguous
+    rows = c.logical_blocks * B + full
+    nb, dc, sc, _, _ = pool_counts(rows, cfg, sparsity)
+    out = DeviceCompressedCache(c.dtype, c.axis, U, nb, dc, sc, c.index_map.device, d, cfg.block_size, cfg)
+    cin, cout, cc = c.c(), out.c(), cfg.c()
+    capi.check(capi.load().hs_absorb_tail(C.byref(cin), src.data_ptr(), _unit_stride(src), full, C.byref(cc),
+                                          sparsity, C.byref(cout), out.losses.data_ptr(), out.flags.data_ptr(),
+                                          _stream()))
+    return out, tail[:, full:]
+
+
+def absorb_tail_pair(k: DeviceCompressedCache, v: DeviceCompressedCache, k_tail: torch.Tensor,
+                     v_tail: torch.Tensor, cfg: SparsityConfig):
+    """absorb_tail for the key (S_K, channel groups) and value (S_V, sequence groups) caches."""
+    k2, kt = absorb_tail(k, k_tail, cfg, cfg.s_key)
+    v2, vt = absorb_tail(v, v_tail, cfg, cfg.s_value)
+    return k2, v2, kt, vt
+
+
 def recompress_unfused(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: float) -> DeviceCompressedCache:
     """recompress as the reference composes it: decompress to a dense device
     cache, then prune_compress (the parity check for the fused path)."""

@@ -267,3 +267,43 @@ def test_recompress_rejects_corrupt_input(hs, port):
     bad2.meta_pool[0, 0, 0] = 0x0003  # first group codes (3, 0): not increasing
     with pytest.raises(hs.DataError, match="not increasing"):
         hs.recompress(bad2, hs.SparsityConfig(1.0, 1.0, 64), 1.0)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("s_dec,tail_rows", [(1.0, 200), (0.5, 128), (0.25, 64)])
+def test_absorb_tail_matches_oracle(hs, port, dtype, s_dec, tail_rows):
+    """Dense-tail growth: the cache's blocks plus the tail's
+    whole blocks re-pruned in one pass == oracle prune_compress of
+    [decompress(cache); tail blocks], bit for bit; the partial block stays a tail."""
+    import torch
+    from oracle.oracle import SparsityConfig as OCfg
+    U, L = 2, 1024
+    kx = gen_units(port, U, L + tail_rows, 128, 41, 0, dtype)
+    vx = gen_units(port, U, L + tail_rows, 128, 41, 1, dtype)
+    kt, vt = to_torch(kx, dtype), to_torch(vx, dtype)
+    kc, vc = hs.prune_cache(kt[:, :L].contiguous(), vt[:, :L].contiguous(), hs.SparsityConfig(0.5, 0.5, 64))
+    cfg = hs.SparsityConfig(s_dec, s_dec, 64, sink_tokens=64)
+    k2, v2, krest, vrest = hs.absorb_tail_pair(kc, vc, kt[:, L:], vt[:, L:], cfg)
+    full = (tail_rows // 64) * 64
+    assert k2.logical_blocks == (L + full) // 64 and krest.shape[1] == tail_rows - full
+    assert torch.equal(krest.view(torch.int16), kt[:, L + full:].view(torch.int16))
+    for dev_old, dev_new, axis, src in ((kc, k2, 0, kx), (vc, v2, 1, vx)):
+        for u in range(U):
+            dense = port.decompress(device_to_oracle(dev_old, u))
+            grown = np.concatenate([dense, np.asarray(src[u])[L:L + full]], axis=0)
+            want = port.prune_compress(grown, OCfg(s_dec, s_dec, 64, sink_tokens=64), axis, s_dec)
+            assert_cache_equal(dev_new, u, want, f"absorb_tail axis={axis} unit={u}")
+    # the grown cache and its remaining tail decode like any other cache
+    q = torch.randn(U, 4, 128, device="cuda").to(kt.dtype)
+    out = hs.decode_attention(q, k2, v2, krest, vrest)
+    assert torch.isfinite(out).all()
+
+
+def test_absorb_tail_without_whole_block_is_a_noop(hs, port):
+    import torch
+    U, L = 1, 256
+    kx = gen_units(port, U, L + 10, 128, 3, 0, "bf16")
+    kt = to_torch(kx, "bf16")
+    kc = hs.prune_compress(kt[:, :L].contiguous(), hs.SparsityConfig(1.0, 1.0, 64), 1.0, 0)
+    k2, rest = hs.absorb_tail(kc, kt[:, L:], hs.SparsityConfig(1.0, 1.0, 64), 1.0)
+    assert k2 is kc and rest.shape[1] == 10
