@@ -83,62 +83,52 @@ __device__ __forceinline__ int unit_exp(uint32_t mag) {
 
 struct LossAcc {
     double sum = 0.0;
-    int emin = 1 << 20;
-    int emax = -(1 << 20);
+    uint32_t min_mag = 0xFFFFu;  // smallest nonzero pruned magnitude (16-bit pattern)
 };
 
 template <typename T>
 __device__ __forceinline__ void loss_add(LossAcc& a, uint16_t bits) {
     const uint32_t mag = mag16(bits);
     if (mag == 0) return;
-    const int e = unit_exp<T>(mag);
-    a.emin = min(a.emin, e);
-    a.emax = max(a.emax, e);
+    a.min_mag = min(a.min_mag, mag);
     a.sum += fabs(static_cast<double>(F16Traits<T>::to_float(bits)));
 }
 
-// Both pruned elements of a group (magnitude bits, lo <= hi): exponents tracked
-// as max(E, 1) of the nonzero terms (same differences as the unit exponents).
+// Both pruned elements of a group (magnitude bits, lo <= hi).
 template <typename T>
 __device__ __forceinline__ void loss_add_pair(LossAcc& a, uint32_t lo, uint32_t hi) {
-    constexpr int mant = F16Traits<T>::kMantBits;
-    const int eh = hi ? max(static_cast<int>(hi >> mant), 1) : -(1 << 20);
-    const int el = lo ? max(static_cast<int>(lo >> mant), 1) : (hi ? eh : (1 << 20));
-    a.emin = min(a.emin, el);
-    a.emax = max(a.emax, eh);
+    a.min_mag = min(a.min_mag, lo ? lo : (hi ? hi : 0xFFFFu));
     a.sum += static_cast<double>(F16Traits<T>::to_float(static_cast<uint16_t>(lo))) +
              static_cast<double>(F16Traits<T>::to_float(static_cast<uint16_t>(hi)));
 }
 
-// Reduce LossAcc across the CTA; thread 0 gets the totals.  Returns true on
-// thread 0 when the exactness bound holds.
+// Reduce LossAcc across the CTA; thread 0 gets the total.  Returns true on
+// thread 0 when the parallel sum is provably the reference's sequential one:
+// every term is an integer multiple of u = 2^unit_exp(min nonzero magnitude),
+// so every partial sum in any order is K * u with K <= total / u; below 2^53
+// units all of them are exact doubles, the reference's included.
 template <typename T>
-__device__ bool loss_reduce(LossAcc& a, double* s_sum, int* s_emin, int* s_emax) {
+__device__ bool loss_reduce(LossAcc& a, double* s_sum, int* s_min, int*) {
     for (int o = 16; o > 0; o >>= 1) {
         a.sum += __shfl_xor_sync(0xffffffffu, a.sum, o);
-        a.emin = min(a.emin, __shfl_xor_sync(0xffffffffu, a.emin, o));
-        a.emax = max(a.emax, __shfl_xor_sync(0xffffffffu, a.emax, o));
+        a.min_mag = min(a.min_mag, static_cast<uint32_t>(__shfl_xor_sync(0xffffffffu, a.min_mag, o)));
     }
     const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
         s_sum[w] = a.sum;
-        s_emin[w] = a.emin;
-        s_emax[w] = a.emax;
+        s_min[w] = static_cast<int>(a.min_mag);
     }
     __syncthreads();
     bool exact = false;
     if (threadIdx.x == 0) {
         double s = 0.0;
-        int lo = 1 << 20, hi = -(1 << 20);
+        uint32_t mn = 0xFFFFu;
         for (int i = 0; i < kThreads / 32; ++i) {
             s += s_sum[i];
-            lo = min(lo, s_emin[i]);
-            hi = max(hi, s_emax[i]);
+            mn = min(mn, static_cast<uint32_t>(s_min[i]));
         }
         a.sum = s;
-        // terms < 2^(mant+1) units each, at most B*d/2 = 2^12 terms.
-        constexpr int kMBits = F16Traits<T>::kMantBits + 1;
-        exact = (hi < lo) || (hi - lo) + kMBits + 12 <= 53;
+        exact = mn == 0xFFFFu || s < ldexp(1.0, 53 + unit_exp<T>(mn));
     }
     return exact;
 }
@@ -254,7 +244,7 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
                                          static_cast<uint64_t>(b - (SRC == 0 ? 0 : a.in_nb)) * kBlock * kHeadDim
                                    : nullptr;
     __shared__ double s_sum[kThreads / 32];
-    __shared__ int s_emin[kThreads / 32], s_emax[kThreads / 32];
+    __shared__ int s_min[kThreads / 32];
     // SRC 1: the input block (dense slot or nnz + metadata of a sparse slot)
     int in_e = 0;
     const uint16_t *in_den = nullptr, *in_nnz = nullptr, *in_meta = nullptr;
@@ -287,10 +277,12 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
     if (AXIS == 0) {
         // Key cache: groups of 4 channels along a token row, stored layout = logical.
         const int c = t & 15;  // 16-byte chunk: channels 8c..8c+7 (groups 2c, 2c+1)
+        // all four rows' loads first (memory-level parallelism), then the selection
+        uint4 vr[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
             const int r = p * 16 + (t >> 4);
-            uint4 v;
+            uint4& v = vr[p];
             if (from_src) {
                 v = *reinterpret_cast<const uint4*>(blk + r * kHeadDim + c * 8);
             } else if (in_e > 0) {
@@ -304,6 +296,11 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
             } else {
                 v = make_uint4(0u, 0u, 0u, 0u);
             }
+        }
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const int r = p * 16 + (t >> 4);
+            const uint4 v = vr[p];
             if (MODE != 0 && dense) {
                 uint16_t* dst = a.dense_pool + (static_cast<uint64_t>(u) * a.dense_count + slot) * (kBlock * kHeadDim);
                 *reinterpret_cast<uint4*>(dst + r * kHeadDim + c * 8) = v;
@@ -406,7 +403,7 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
 
     if (SRC == 1 && in_bad) atomicExch(a.bad, 2);
     if (kLoss) {
-        const bool exact = loss_reduce<T>(acc, s_sum, s_emin, s_emax);
+        const bool exact = loss_reduce<T>(acc, s_sum, s_min, nullptr);
         if (t == 0) {
             double loss = acc.sum;
             // (SRC 1: every stored 2:4 group keeps its two largest magnitudes and
