@@ -55,6 +55,10 @@ constexpr int kThreads = 32 * (kSoftWarps + 3);
 constexpr int kThreads = 32 * (kSoftWarps + 4);
 #endif
 
+#ifndef HS_PREFILL_G2FIRST
+#define HS_PREFILL_G2FIRST 0  // measured: +1.5% at S=1, -2% at S=0 (64K); off
+#endif
+constexpr bool kG2First = HS_PREFILL_G2FIRST != 0;  // issue GEMM2(t-2) before GEMM1(t)
 constexpr uint32_t kBiasBytes = 3 * 2048;  // ones + bias[2] GEMM1 operands (16-byte rows)
 constexpr float kTau = 8.0f;      // lazy-rescale threshold (log2 units): P <= 2^8
 
@@ -85,6 +89,16 @@ struct PrefillLayout {
     uint32_t off_tiles, tile_cap;
     uint32_t off_bias;  // ones [128 x 16] + two bias operands [128 x 16] (16-byte rows, K halves aliased)
 };
+
+// CTA-scope release / acquire on a shared-memory word (cross-warp ordering flags).
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
 
 __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -282,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     __shared__ float s_red[4][128];
     __shared__ float s_delta[128], s_alpha[128], s_mrun[128], s_mused[2][128];
     __shared__ uint16_t s_bq[128];
+    __shared__ int s_g2_issued;  // GEMM2 tiles issued (kG2First ordering)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     const int n_tiles_q = (L.n_q + 127) / 128;
@@ -303,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     // ------------------------------------------------------------ setup ----
     if (warp == kWarpMma) tmem_alloc(&s_tmem, 512);
     if (tid == 0) {
+        s_g2_issued = 0;
         mbar_init(&bar_q, 1);
         for (int s = 0; s < nk; ++s) {
             mbar_init(&bar_kfull[s], 1);
@@ -597,6 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 umma_commit(&bar_vempty[s]);            // V stage can be refilled
             }
             __syncwarp();
+            if (kG2First && lane == 0) st_release(&s_g2_issued, tp + 1);
             o_started = true;
             if (DBG && lane == 0) trace(L, tp, 6);
         };
@@ -611,6 +628,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             mbar_wait_dbg(&bar_kfull[s], (t / nk) & 1, dbgp, 3);  // K tile + metadata atom landed
             if (DBG && lane == 0) trace(L, t, 10);
             if (t >= 2) mbar_wait_dbg(&bar_sempty[sb], ((t >> 1) - 1) & 1, dbgp, 6);
+            if (kG2First && t >= 2) {
+                // GEMM2(t-2) enters the tensor pipe ahead of GEMM1(t): the P^T buffer
+                // softmax(t) writes is then free in time (GEMM1 still runs a tile ahead)
+                while (ld_acquire_cta(&s_g2_issued) < t - 1) __nanosleep(32);
+            }
             tc_fence_after();
             if (DBG && lane == 0) trace(L, t, 4);
             if (elect_one()) {
@@ -682,6 +704,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             mbar_wait_dbg(&bar_sfull[sb], (t >> 1) & 1, dbgp, 5);
             tc_fence_after();
             if (DBG && tid == 0) trace(L, t, 0);
+            if (DBG && tid == 256) trace(L, t, 15);  // warpgroup 2's view of the same tile
             if (mode & 1) {  // tools: pipeline without the softmax
                 if (t >= npb) mbar_wait_dbg(&bar_pempty[pbuf_of(t)], pphase(t - npb), dbgp, 8);
                 __syncwarp();

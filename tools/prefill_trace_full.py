@@ -36,3 +36,6 @@ if tr[st, 3].min() > 0:
     print("  check: TMEM load %.0f | scale+mask+max %.0f | bar.red.or %.0f | to S release %.0f"
           % (med(tr[st, 12] - tr[st, 0]), med(tr[st, 13] - tr[st, 12]), med(tr[st, 14] - tr[st, 13]),
              med(tr[st, 1] - tr[st, 14])))
+    print("  warpgroup 2 got S(t) after warpgroup 0 by %.0f cycles (median; p10 %.0f, p90 %.0f)"
+          % (med(tr[st, 15] - tr[st, 0]), np.percentile(tr[st, 15] - tr[st, 0], 10),
+             np.percentile(tr[st, 15] - tr[st, 0], 90)))
