@@ -177,9 +177,6 @@ __device__ __forceinline__ float exp2_fma(float x) {
 #define HS_PREFILL_POLY 2  // of every 8 exponentials, this many run on the FMA pipe
 #endif
 constexpr int kPolyPer8 = HS_PREFILL_POLY;
-#ifndef HS_PREFILL_LAG
-#define HS_PREFILL_LAG 0  // tools: g8 step of tile 0 at which warpgroups 2-3 may start (0 = no lag)
-#endif
 
 #ifndef HS_PREFILL_EXP_F16X2
 #define HS_PREFILL_EXP_F16X2 0  // sm_100a splits f16x2 ex2 into two MUFU ops: no gain
@@ -290,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bar_q, bar_kfull[4], bar_kempty[4];
     __shared__ __align__(8) uint64_t bar_vfull[4], bar_vempty[4];
-    __shared__ __align__(8) uint64_t bar_sfull[2], bar_sempty[2], bar_pfull[2], bar_pempty[2], bar_lag;
+    __shared__ __align__(8) uint64_t bar_sfull[2], bar_sempty[2], bar_pfull[2], bar_pempty[2];
     __shared__ uint32_t s_tmem;
     __shared__ int s_ntiles;
     __shared__ float s_red[4][128];
@@ -334,7 +331,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             mbar_init(&bar_pfull[i], kSoftWarps);
             mbar_init(&bar_pempty[i], 1);
         }
-        mbar_init(&bar_lag, 8);
         fence_barrier_init();
     }
     if (warp == kWarpK) {
@@ -696,11 +692,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         for (int t = 0; t < ntiles; ++t) {
             const int sb = t & 1;
             const TileInfo ti = s_tiles[t];
-#if HS_PREFILL_LAG
-            // warpgroups 2-3 start half a tile behind 0-1 (once): the two halves
-            // of every SM sub-partition then run different phases of the tile
-            if (t == 0 && wg >= 2) mbar_wait(&bar_lag, 0);
-#endif
             mbar_wait_dbg(&bar_sfull[sb], (t >> 1) & 1, dbgp, 5);
             tc_fence_after();
             if (DBG && tid == 0) trace(L, t, 0);
@@ -829,12 +820,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             uint8_t* const pbuf = pbuf0 + pbuf_of(t) * lay.p_bytes;
 #pragma unroll
             for (int g8 = 0; g8 < kCols / 8; ++g8) {
-#if HS_PREFILL_LAG
-                if (g8 == HS_PREFILL_LAG && t == 0 && wg < 2) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&bar_lag);
-                }
-#endif
                 const int q8 = (c0 >> 3) + g8;  // 8-query chunk index in 0..15
                 if constexpr (!HILO && kExpF16x2) {
                     // fp16 P: two exponentials per MUFU op (ex2.approx.f16x2 on x
@@ -853,21 +838,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 }
                 float p[8];
 #pragma unroll
-#ifdef HS_AB_NO_EXP
-                for (int k = 0; k < 8; ++k) p[k] = x[8 * g8 + k] * 0.001f;  // A/B timing only
-#else
                 for (int k = 0; k < 8; ++k)  // exp2(-inf) = 0
                     p[k] = k < 8 - kPolyPer8 ? fast_exp2(x[8 * g8 + k]) : exp2_fma(x[8 * g8 + k]);
-#endif
 #pragma unroll
                 for (int k = 0; k < 8; k += 2) fadd2(l_part[8 * g8 + k], l_part[8 * g8 + k + 1], p[k], p[k + 1]);
                 const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
                                             F16Traits<T>::pack(p[4], p[5]), F16Traits<T>::pack(p[6], p[7]));
-#ifdef HS_AB_NO_PST
-                if (hi.x == 0x12345u) *reinterpret_cast<uint4*>(pbuf + pt_chunk_off(r, q8)) = hi;  // A/B only
-#else
                 *reinterpret_cast<uint4*>(pbuf + pt_chunk_off(r, q8)) = hi;
-#endif
                 if (HILO) {
                     float rr[8];
 #pragma unroll
