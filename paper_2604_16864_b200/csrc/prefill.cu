@@ -672,6 +672,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         const int r = 32 * wq + lane;  // TMEM lane = key row of the tile = d row of O^T
         const int c0 = kCols * wg;     // this warpgroup's first query column
         const int bar_id = 1 + wg;
+        static_assert(kCols % 32 == 0, "P^T chunk offsets assume c0/8 is a multiple of 4");
+        const uint32_t pt_r3 = static_cast<uint32_t>(r & 3) << 4;
+        const uint32_t pt_base = pt_chunk_off(r, c0 >> 3) - ((static_cast<uint32_t>((c0 >> 3) & 7) ^ (r & 7)) << 4) +
+                                 ((static_cast<uint32_t>((c0 >> 3) & 4) ^ (r & 4)) << 4);
         const uint32_t lane_off = static_cast<uint32_t>(32 * wq) << 16;
         float l_part[kCols];
 #pragma unroll
@@ -820,7 +824,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             uint8_t* const pbuf = pbuf0 + pbuf_of(t) * lay.p_bytes;
 #pragma unroll
             for (int g8 = 0; g8 < kCols / 8; ++g8) {
-                const int q8 = (c0 >> 3) + g8;  // 8-query chunk index in 0..15
+                // pt_chunk_off(r, c0/8 + g8) with c0/8 a multiple of 4: only the low two
+                // chunk bits vary with g8, so one XOR + add per chunk
+                const uint32_t pto = pt_base + ((static_cast<uint32_t>(g8) << 4) ^ pt_r3);
                 if constexpr (!HILO && kExpF16x2) {
                     // fp16 P: two exponentials per MUFU op (ex2.approx.f16x2 on x
                     // rounded to fp16; x <= tau keeps the argument error small where
@@ -833,7 +839,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                         l_part[8 * g8 + 2 * k] += f.x;
                         l_part[8 * g8 + 2 * k + 1] += f.y;
                     }
-                    *reinterpret_cast<uint4*>(pbuf + pt_chunk_off(r, q8)) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+                    *reinterpret_cast<uint4*>(pbuf + pto) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
                     continue;
                 }
                 float p[8];
@@ -844,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 for (int k = 0; k < 8; k += 2) fadd2(l_part[8 * g8 + k], l_part[8 * g8 + k + 1], p[k], p[k + 1]);
                 const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
                                             F16Traits<T>::pack(p[4], p[5]), F16Traits<T>::pack(p[6], p[7]));
-                *reinterpret_cast<uint4*>(pbuf + pt_chunk_off(r, q8)) = hi;
+                *reinterpret_cast<uint4*>(pbuf + pto) = hi;
                 if (HILO) {
                     float rr[8];
 #pragma unroll
@@ -855,7 +861,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     }
                     const uint4 lo = make_uint4(F16Traits<T>::pack(rr[0], rr[1]), F16Traits<T>::pack(rr[2], rr[3]),
                                                 F16Traits<T>::pack(rr[4], rr[5]), F16Traits<T>::pack(rr[6], rr[7]));
-                    *reinterpret_cast<uint4*>(pbuf + 32768 + pt_chunk_off(r, q8)) = lo;
+                    *reinterpret_cast<uint4*>(pbuf + 32768 + pto) = lo;
                 }
             }
             if (DBG && tid == 0) trace(L, t, 3);
