@@ -733,10 +733,17 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             }
             bool slow = pending || ((dirty >> sb) & 1u);
             if (!slow) {
-                float xmax = max3f(x[0], x[1], x[2]);
+                // four independent 3-input max chains (short dependency depth), then merge
+                static_assert(kCols == 32, "max tree laid out for 32 columns");
+                float m4[4];
 #pragma unroll
-                for (int k = 3; k + 1 < kCols; k += 2) xmax = max3f(xmax, x[k], x[k + 1]);
-                if constexpr (kCols % 2 == 0) xmax = fmaxf(xmax, x[kCols - 1]);
+                for (int j = 0; j < 4; ++j) {
+                    float m = max3f(x[8 * j], x[8 * j + 1], x[8 * j + 2]);
+                    m = max3f(m, x[8 * j + 3], x[8 * j + 4]);
+                    m = max3f(m, x[8 * j + 5], x[8 * j + 6]);
+                    m4[j] = fmaxf(m, x[8 * j + 7]);
+                }
+                const float xmax = fmaxf(max3f(m4[0], m4[1], m4[2]), m4[3]);
                 if (DBG && tid == 0) trace(L, t, 13);
                 slow = bar_red_or(bar_id, !(xmax <= kTau));
             }
