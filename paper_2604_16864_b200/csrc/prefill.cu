@@ -173,10 +173,42 @@ __device__ __forceinline__ float exp2_fma(float x) {
     p = fmaf(p, f, 1.0f);
     return __int_as_float(__float_as_int(p) + (__float_as_int(y) << 23));
 }
+// exp2_fma on a pair with packed f32x2 arithmetic (FADD2 / FFMA2): half the
+// instructions of two scalar calls.
+__device__ __forceinline__ void exp2_fma2(float& x0, float& x1) {
+    x0 = fmaxf(x0, -127.f);
+    x1 = fmaxf(x1, -127.f);
+    float y0 = x0, y1 = x1;
+    fadd2(y0, y1, 12582912.f, 12582912.f);    // 1.5 * 2^23: j in the low mantissa bits
+    float j0 = y0, j1 = y1;
+    fadd2(j0, j1, -12582912.f, -12582912.f);
+    float f0 = x0, f1 = x1;
+    fadd2(f0, f1, -j0, -j1);
+    float p0 = f0, p1 = f1;
+    ffma2(p0, p1, 1.3333558e-3f, 9.6181291e-3f, 9.6181291e-3f);  // (c5 f + c4)
+    float q0 = p0, q1 = p1;
+    // Horner: p <- p * f + c (f per lane): packed multiply by the pair f
+    auto step = [&](float c) {
+        asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%0, %1};\n\tmov.b64 rb, {%2, %3};\n\t"
+            "mov.b64 rc, {%4, %4};\n\tfma.rn.f32x2 ra, ra, rb, rc;\n\tmov.b64 {%0, %1}, ra;\n\t}"
+            : "+f"(q0), "+f"(q1)
+            : "f"(f0), "f"(f1), "f"(c));
+    };
+    (void)p0;
+    (void)p1;
+    step(5.5504109e-2f);
+    step(2.4022651e-1f);
+    step(6.9314718e-1f);
+    step(1.0f);
+    x0 = __int_as_float(__float_as_int(q0) + (__float_as_int(y0) << 23));
+    x1 = __int_as_float(__float_as_int(q1) + (__float_as_int(y1) << 23));
+}
+
 #ifndef HS_PREFILL_POLY
 #define HS_PREFILL_POLY 2  // of every 8 exponentials, this many run on the FMA pipe
 #endif
 constexpr int kPolyPer8 = HS_PREFILL_POLY;
+static_assert(kPolyPer8 % 2 == 0, "polynomial exponentials run in packed pairs");
 
 #ifndef HS_PREFILL_EXP_F16X2
 #define HS_PREFILL_EXP_F16X2 0  // sm_100a splits f16x2 ex2 into two MUFU ops: no gain
@@ -851,8 +883,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 }
                 float p[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)  // exp2(-inf) = 0
-                    p[k] = k < 8 - kPolyPer8 ? fast_exp2(x[8 * g8 + k]) : exp2_fma(x[8 * g8 + k]);
+                for (int k = 0; k < 8 - kPolyPer8; ++k) p[k] = fast_exp2(x[8 * g8 + k]);  // exp2(-inf) = 0
+#pragma unroll
+                for (int k = 8 - kPolyPer8; k < 8; k += 2) {
+                    p[k] = x[8 * g8 + k];
+                    p[k + 1] = x[8 * g8 + k + 1];
+                    exp2_fma2(p[k], p[k + 1]);
+                }
 #pragma unroll
                 for (int k = 0; k < 8; k += 2) fadd2(l_part[8 * g8 + k], l_part[8 * g8 + k + 1], p[k], p[k + 1]);
                 const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
