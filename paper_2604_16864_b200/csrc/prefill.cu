@@ -747,13 +747,18 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             tmem_ld_wait();
             if (DBG && tid == 0) trace(L, t, 12);
             // masks: invalid rows of single-block tiles; causal (attention.hpp:181-190)
-            const int key_pos = ti.dblk * kBlock + r;  // diagonal / tail pairs are consecutive blocks
-            // rows past a single block or past the end of the tail hold no key
-            const bool row_valid = (r < 64 || ti.ve1 != 0) && (ti.dblk < 0 || key_pos < n_kv);
-            // column c (query q0 + c at position off + q0 + c) sees this key iff c >= c_first
-            const int c_first = row_valid ? ((L.causal && ti.dblk >= 0) ? key_pos - off - q0 : 0) : 1 << 30;
-            // warp-uniform fast path: every (row, column) of this warp visible
-            const bool fast = __all_sync(0xffffffffu, c_first <= c0);
+            // (a full off-diagonal pair -- most tiles -- is visible everywhere: no mask work)
+            int c_first = 0;
+            bool fast = true;
+            if (ti.dblk >= 0 || ti.ve1 == 0) {
+                const int key_pos = ti.dblk * kBlock + r;  // diagonal / tail pairs are consecutive blocks
+                // rows past a single block or past the end of the tail hold no key
+                const bool row_valid = (r < 64 || ti.ve1 != 0) && (ti.dblk < 0 || key_pos < n_kv);
+                // column c (query q0 + c at position off + q0 + c) sees this key iff c >= c_first
+                c_first = row_valid ? ((L.causal && ti.dblk >= 0) ? key_pos - off - q0 : 0) : 1 << 30;
+                // warp-uniform fast path: every (row, column) of this warp visible
+                fast = __all_sync(0xffffffffu, c_first <= c0);
+            }
             // S^T holds s + bias[sb] = s - m_used/(scale log2e), so x = S^T * scale log2e
             // = s*scale*log2e - m_used: no per-column operand in the steady state
 #pragma unroll
