@@ -103,6 +103,37 @@ def test_prefill_growing_scores(hs, port, dtype, s, causal):
 
 
 @pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("qscale,negative", [(24.0, False), (24.0, True), (0.01, False)])
+def test_prefill_logit_ranges(hs, port, dtype, qscale, negative):
+    """Very large logits (|s| ~ 10^3: the running max lives in the 16-bit bias
+    operand of GEMM1, rounded), all-negative large logits (every column's max far
+    below zero) and near-uniform attention (tiny logits): the stabiliser may be any
+    representable value as long as P and the rescale factors use it consistently."""
+    U, gqa, L, n_q = 1, 2, 1024, 1024
+    kx = gen_units(port, U, L, 128, 13, 0, dtype)
+    vx = gen_units(port, U, L, 128, 13, 1, dtype)
+    if negative:  # one shared direction pushed far negative for every key
+        kx = kx.copy()
+        kx[..., 0] = -40.0
+    kx = port.round_to(kx.astype(np.float32), dtype)
+    kc, vc = hs.prune_cache(to_torch(kx, dtype), to_torch(vx, dtype), hs.SparsityConfig(1.0, 1.0, 64))
+    q = np.stack([np.stack([port.random_gaussian(n_q, 128, port.head_seed(13, u, 2 + g)) * qscale
+                            for g in range(gqa)]) for u in range(U)]).astype(np.float32)
+    if negative:
+        q[..., 0] = np.abs(q[..., 0]) + 30.0
+    q = port.round_to(q, dtype)
+    scale = np.float32(1.0 / math.sqrt(128))
+    got = hs.prefill_attention(to_torch(q, dtype), kc, vc, causal=True, scale=float(scale)).cpu().numpy()
+    assert np.isfinite(got).all()
+
+    def one(g):
+        return port.prefill(q[0, g], device_to_oracle(kc, 0), device_to_oracle(vc, 0), None, None, True, scale, 64)
+    want = np.stack(parallel(one, range(gqa)))[None]
+    mx, mr = err_stats(got, want)
+    assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
 @pytest.mark.parametrize("L,tail,n_q,s,causal", [
     (512, 17, 529, 1.0, True),     # golden-vector shape: 4 blocks + 17-token tail, every query
     (1024, 64, 300, 0.5, True),    # whole tail block, queries at the end
