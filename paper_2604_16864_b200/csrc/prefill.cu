@@ -55,6 +55,9 @@ constexpr int kThreads = 32 * (kSoftWarps + 3);
 constexpr int kThreads = 32 * (kSoftWarps + 4);
 #endif
 
+#ifndef HS_PREFILL_PP
+#define HS_PREFILL_PP 0  // tools: ping-pong softmax timing experiment (not numerically complete)
+#endif
 #ifndef HS_PREFILL_G2FIRST
 #define HS_PREFILL_G2FIRST 0  // measured: +1.5% at S=1, -2% at S=0 (64K); off
 #endif
@@ -359,8 +362,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bar_sfull[i], 1);
-            mbar_init(&bar_sempty[i], kSoftWarps);
-            mbar_init(&bar_pfull[i], kSoftWarps);
+            mbar_init(&bar_sempty[i], HS_PREFILL_PP ? kSoftWarps / 2 : kSoftWarps);
+            mbar_init(&bar_pfull[i], HS_PREFILL_PP ? kSoftWarps / 2 : kSoftWarps);
             mbar_init(&bar_pempty[i], 1);
         }
         fence_barrier_init();
@@ -637,8 +640,19 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                         }
                     }
                 }
+#if HS_PREFILL_PP
+                umma_commit(&bar_vempty[s]);  // V stage free once the O^T MMAs are done
+                {   // row sums l[q] += sum_k P^T[q][k]: P^T as an MN-major A operand, ones as B (N = 16)
+                    const uint32_t id_l = umma_idesc_f16(bf, 128, 16, true, false, false);
+                    const uint64_t pa = dP + (pbuf_of(tp) * lay.p_bytes) / 16;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) umma_f16(tmem + 416u, pa + 128 * kk, dOnes, id_l, tp > 0 || kk > 0);
+                }
+                umma_commit(&bar_pempty[pbuf_of(tp)]);  // P^T buffer free; O^T and l through tile tp final
+#else
                 umma_commit(&bar_pempty[pbuf_of(tp)]);  // P^T buffer free; O^T through tile tp final
                 umma_commit(&bar_vempty[s]);            // V stage can be refilled
+#endif
             }
             __syncwarp();
             if (kG2First && lane == 0) st_release(&s_g2_issued, tp + 1);
@@ -689,6 +703,113 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             }
             __syncwarp();
         }
+#if HS_PREFILL_PP
+    } else {
+        // ---- TIMING EXPERIMENT (not numerically complete): ping-pong softmax.
+        // Group g = warp / 8 takes tiles t = g (mod 2) with S^T buffer g and P^T
+        // buffer g; each warp covers 32 key lanes x 64 query columns; row sums go
+        // to the tensor core (GEMM2 warp, l-MMA).  Running-max sharing between the
+        // groups and the O / l rescale are omitted here.
+        const int grp = warp >> 3, wq = warp & 3, ch = (warp >> 2) & 1;
+        const int r = 32 * wq + lane;
+        const int c0 = 64 * ch;
+        const int bar_id = 1 + 2 * grp + ch;
+        const uint32_t lane_off = static_cast<uint32_t>(32 * wq) << 16;
+        const uint32_t pt_base_h = static_cast<uint32_t>(ch) * 16384u + (r >> 3) * 1024 + (r & 7) * 128;
+        const uint32_t r7 = r & 7;
+        uint8_t* const pbuf0 = base_ptr + lay.off_p;
+        const float sl2 = L.scale_log2;
+        for (int t = grp; t < ntiles; t += 2) {
+            const int sb = t & 1;
+            const TileInfo ti = s_tiles[t];
+            mbar_wait(&bar_sfull[sb], (t >> 1) & 1);
+            tc_fence_after();
+            float x[64];
+            tmem_ld16_f(tS0 + 128 * sb + lane_off + c0, x);
+            tmem_ld16_f(tS0 + 128 * sb + lane_off + c0 + 16, x + 16);
+            tmem_ld16_f(tS0 + 128 * sb + lane_off + c0 + 32, x + 32);
+            tmem_ld16_f(tS0 + 128 * sb + lane_off + c0 + 48, x + 48);
+            tmem_ld_wait();
+            int c_first = 0;
+            bool fast = true;
+            if (ti.dblk >= 0 || ti.ve1 == 0) {
+                const int key_pos = ti.dblk * kBlock + r;
+                const bool row_valid = (r < 64 || ti.ve1 != 0) && (ti.dblk < 0 || key_pos < n_kv);
+                c_first = row_valid ? ((L.causal && ti.dblk >= 0) ? key_pos - off - q0 : 0) : 1 << 30;
+                fast = __all_sync(0xffffffffu, c_first <= c0);
+            }
+#pragma unroll
+            for (int k = 0; k < 64; k += 2) ffma2(x[k], x[k + 1], sl2, 0.f, 0.f);
+            if (!fast) {
+#pragma unroll
+                for (int k = 0; k < 64; ++k)
+                    if (c0 + k < c_first) x[k] = -INFINITY;
+            }
+            float m8[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float m = max3f(x[8 * j], x[8 * j + 1], x[8 * j + 2]);
+                m = max3f(m, x[8 * j + 3], x[8 * j + 4]);
+                m = max3f(m, x[8 * j + 5], x[8 * j + 6]);
+                m8[j] = fmaxf(m, x[8 * j + 7]);
+            }
+            const float xmax = max3f(max3f(m8[0], m8[1], m8[2]), max3f(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+            if (bar_red_or(bar_id, !(xmax <= kTau))) {
+                // (experiment: a real slow path updates the shared running max here)
+#pragma unroll
+                for (int k = 0; k < 64; ++k) x[k] = fminf(x[k], kTau);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_sempty[sb]);
+            if (t >= 2) mbar_wait(&bar_pempty[sb], ((t >> 1) - 1) & 1);
+            uint8_t* const pbuf = pbuf0 + sb * lay.p_bytes;
+#pragma unroll
+            for (int g8 = 0; g8 < 8; ++g8) {
+                float p[8];
+#pragma unroll
+                for (int k = 0; k < 8 - kPolyPer8; ++k) p[k] = fast_exp2(x[8 * g8 + k]);
+#pragma unroll
+                for (int k = 8 - kPolyPer8; k < 8; k += 2) {
+                    p[k] = x[8 * g8 + k];
+                    p[k + 1] = x[8 * g8 + k + 1];
+                    exp2_fma2(p[k], p[k + 1]);
+                }
+                const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
+                                            F16Traits<T>::pack(p[4], p[5]), F16Traits<T>::pack(p[6], p[7]));
+                *reinterpret_cast<uint4*>(pbuf + pt_base_h + ((static_cast<uint32_t>(g8) ^ r7) << 4)) = hi;
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_pfull[sb]);
+        }
+        // epilogue: group 0 writes O^T / l (l from the l-MMA accumulator)
+        if (ntiles > 0) mbar_wait(&bar_pempty[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
+        tc_fence_after();
+        if (grp == 0) {
+            if (ch == 0) {
+                uint32_t lv[1];
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(lv[0]) : "r"(tmem + 416u + lane_off));
+                tmem_ld_wait();
+                const float l = __uint_as_float(lv[0]);
+                s_alpha[r] = l > 0.f ? 1.f / l : 0.f;
+            }
+            named_bar(1, 256);
+            float* out = L.out + (static_cast<int64_t>(u * L.gqa + h) * L.n_q + q0) * kHeadDim;
+#pragma unroll 1
+            for (int k16 = 0; k16 < 64; k16 += 16) {
+                float v[16];
+                tmem_ld16_f(tO + lane_off + c0 + k16, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const int c = c0 + k16 + k;
+                    if (c < rows_q) out[c * kHeadDim + r] = v[k] * s_alpha[c];
+                }
+            }
+        }
+    }
+#else
     } else {
         // ------------------------------------------------------- softmax WGs
         // kSoftWG warpgroups; WG g owns query columns [kCols*g, kCols*(g+1)); warp
@@ -945,6 +1066,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             }
         }
     }
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == kWarpMma) tmem_dealloc(tmem, 512);
