@@ -731,9 +731,11 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
         }
     }
     if (L.dbg) {
-        int h[4] = {0, 0, 0, 0};
+        int h[16] = {0};
         cudaStreamSynchronize(s);
         cudaMemcpy(h, L.dbg, sizeof h, cudaMemcpyDeviceToHost);
+        if (getenv("HS_DEBUG_COUNTS"))
+            fprintf(stderr, "prefill counts: slow %d rescale %d grow %d\n", h[8], h[9], h[10]);
         if (h[0]) return fail(HS_ERR_CUDA, "prefill watchdog: barrier tag %d parity %d block %d thread %d", h[0], h[1], h[2], h[3]);
     }
     return HS_OK;

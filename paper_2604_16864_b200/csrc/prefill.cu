@@ -55,9 +55,20 @@ constexpr int kThreads = 32 * (kSoftWarps + 3);
 constexpr int kThreads = 32 * (kSoftWarps + 4);
 #endif
 
-#ifndef HS_PREFILL_PP
-#define HS_PREFILL_PP 0  // tools: ping-pong softmax timing experiment (not numerically complete)
-#endif
+// Ping-pong softmax state (static shared memory of the PP instantiation).
+struct PPShared {
+    unsigned long long s_mcur[128];  // shared running max: orderable(m) << 32 | bias bits
+    float s_red2[2][4][128];         // slow-path column maxima [group][lane quarter][column]
+    float s_dl[2][128];              // slow path: m_t - m_used [group][column]
+    float s_mt[2][2][128];           // m of a published tile [group][slot][column]
+    float s_al[2][128];              // rescale factors exp2(m_{t-1} - m_t) [group][column]
+    int s_ver[2];                    // m version per column half (bumped on growth)
+    int s_vsnap[2][2];               // [group][half] version snapshot broadcast
+    int s_tdone[2][2][2];            // last tile published per [group][slot][half]
+};
+struct PPNone {
+    int unused;
+};
 #ifndef HS_PREFILL_G2FIRST
 #define HS_PREFILL_G2FIRST 0  // measured: +1.5% at S=1, -2% at S=0 (64K); off
 #endif
@@ -92,6 +103,15 @@ struct PrefillLayout {
     uint32_t off_tiles, tile_cap;
     uint32_t off_bias;  // ones [128 x 16] + two bias operands [128 x 16] (16-byte rows, K halves aliased)
 };
+
+// Monotone float <-> uint32 map (for atomicMax on possibly negative floats).
+__device__ __forceinline__ uint32_t ord_f32(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b >> 31) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f32(uint32_t o) {
+    return __uint_as_float((o >> 31) ? (o & 0x7FFFFFFFu) : ~o);
+}
 
 // CTA-scope release / acquire on a shared-memory word (cross-warp ordering flags).
 __device__ __forceinline__ void st_release(int* p, int v) {
@@ -312,7 +332,7 @@ __global__ void __launch_bounds__(128) tail_prep_kernel(const uint16_t* __restri
     }
 }
 
-template <typename T, bool HILO, bool DBG>
+template <typename T, bool HILO, bool DBG, bool PP>
 __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_constant__ PrefillLaunch L,
                                                                PrefillLayout lay) {
     // DBG: tools-only instrumentation (per-tile trace, watchdog waits, mode
@@ -329,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     __shared__ float s_delta[128], s_alpha[128], s_mrun[128], s_mused[2][128];
     __shared__ uint16_t s_bq[128];
     __shared__ int s_g2_issued;  // GEMM2 tiles issued (kG2First ordering)
+    __shared__ typename std::conditional<PP, PPShared, PPNone>::type pps;  // ping-pong softmax state
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     const int n_tiles_q = (L.n_q + 127) / 128;
@@ -362,8 +383,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bar_sfull[i], 1);
-            mbar_init(&bar_sempty[i], HS_PREFILL_PP ? kSoftWarps / 2 : kSoftWarps);
-            mbar_init(&bar_pfull[i], HS_PREFILL_PP ? kSoftWarps / 2 : kSoftWarps);
+            mbar_init(&bar_sempty[i], PP ? kSoftWarps / 2 : kSoftWarps);  // PP: one 8-warp group per buffer
+            mbar_init(&bar_pfull[i], PP ? kSoftWarps / 2 : kSoftWarps);
             mbar_init(&bar_pempty[i], 1);
         }
         fence_barrier_init();
@@ -444,8 +465,16 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         for (int i = tid; i < 3 * 128; i += 32 * kSoftWarps)
             ob[i] = i < 128 ? make_uint4(one, one, one, one) : make_uint4(0u, 0u, 0u, 0u);
         if (tid < 128) {
-            s_mused[0][tid] = 0.f;
-            s_mused[1][tid] = 0.f;
+            s_mused[0][tid] = PP ? -INFINITY : 0.f;
+            s_mused[1][tid] = PP ? -INFINITY : 0.f;
+        }
+        if constexpr (PP) {
+            if (tid < 128) {
+                pps.s_mcur[tid] = static_cast<unsigned long long>(ord_f32(-INFINITY)) << 32;
+                pps.s_mt[0][0][tid] = pps.s_mt[0][1][tid] = pps.s_mt[1][0][tid] = pps.s_mt[1][1][tid] = -INFINITY;
+            }
+            if (tid < 8) (&pps.s_tdone[0][0][0])[tid] = -1;
+            if (tid < 2) pps.s_ver[tid] = 0;
         }
         fence_async_smem();
     }
@@ -640,19 +669,22 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                         }
                     }
                 }
-#if HS_PREFILL_PP
+                if constexpr (PP) {
                 umma_commit(&bar_vempty[s]);  // V stage free once the O^T MMAs are done
                 {   // row sums l[q] += sum_k P^T[q][k]: P^T as an MN-major A operand, ones as B (N = 16)
                     const uint32_t id_l = umma_idesc_f16(bf, 128, 16, true, false, false);
                     const uint64_t pa = dP + (pbuf_of(tp) * lay.p_bytes) / 16;
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) umma_f16(tmem + 416u, pa + 128 * kk, dOnes, id_l, tp > 0 || kk > 0);
+                    for (int pass = 0; pass < (HILO ? 2 : 1); ++pass)
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk)
+                            umma_f16(tmem + 416u, pa + pass * 2048 + 128 * kk, dOnes, id_l, tp > 0 || pass > 0 || kk > 0);
                 }
                 umma_commit(&bar_pempty[pbuf_of(tp)]);  // P^T buffer free; O^T and l through tile tp final
-#else
+                } else {
                 umma_commit(&bar_pempty[pbuf_of(tp)]);  // P^T buffer free; O^T through tile tp final
                 umma_commit(&bar_vempty[s]);            // V stage can be refilled
-#endif
+                }
             }
             __syncwarp();
             if (kG2First && lane == 0) st_release(&s_g2_issued, tp + 1);
@@ -703,26 +735,48 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             }
             __syncwarp();
         }
-#if HS_PREFILL_PP
-    } else {
-        // ---- TIMING EXPERIMENT (not numerically complete): ping-pong softmax.
-        // Group g = warp / 8 takes tiles t = g (mod 2) with S^T buffer g and P^T
-        // buffer g; each warp covers 32 key lanes x 64 query columns; row sums go
-        // to the tensor core (GEMM2 warp, l-MMA).  Running-max sharing between the
-        // groups and the O / l rescale are omitted here.
+    } else if constexpr (PP) {
+        // ------------------------------------------- ping-pong softmax ----
+        // Two groups of 8 warps take alternate tiles: group g handles t = g (mod 2)
+        // with S^T buffer g, P^T buffer g and GEMM1 bias operand g, so one group's
+        // exponentials overlap the other's TMEM load and reduction.  Warp (g, wq,
+        // ch) covers key lanes 32 wq.. and query columns 64 ch..; its 4 warps (one
+        // per lane quarter) form a "quad" with its own named barrier.  The row sums
+        // l are accumulated by the tensor core (GEMM2 warp: P^T x ones).
+        //
+        // Running max: one shared value per column (s_mcur, grown with atomicMax,
+        // version-counted per column half).  A quad's fast path needs its bias
+        // snapshot to be current (version match) and every value <= tau; otherwise
+        // its slow path grows m_cur where needed, re-reads it, corrects x and
+        // refreshes its bias.  Every tile publishes the m it used (version +
+        // values); before its P^T is released to GEMM2, the next tile's quad
+        // compares versions and, when they differ, rescales O^T and l between
+        // GEMM2(t-1) and GEMM2(t) by exp2(m_{t-1} - m_t).
+        auto& s_mcur = pps.s_mcur;
+        auto& s_red2 = pps.s_red2;
+        auto& s_dl = pps.s_dl;
+        auto& s_mt = pps.s_mt;
+        auto& s_al = pps.s_al;
+        auto& s_ver = pps.s_ver;
+        auto& s_vsnap = pps.s_vsnap;
+        auto& s_tdone = pps.s_tdone;
         const int grp = warp >> 3, wq = warp & 3, ch = (warp >> 2) & 1;
         const int r = 32 * wq + lane;
         const int c0 = 64 * ch;
         const int bar_id = 1 + 2 * grp + ch;
         const uint32_t lane_off = static_cast<uint32_t>(32 * wq) << 16;
+        const uint32_t tL = tmem + 416u;
         const uint32_t pt_base_h = static_cast<uint32_t>(ch) * 16384u + (r >> 3) * 1024 + (r & 7) * 128;
         const uint32_t r7 = r & 7;
         uint8_t* const pbuf0 = base_ptr + lay.off_p;
+        uint4* const bias_rows = reinterpret_cast<uint4*>(base_ptr + lay.off_bias + 2048);
         const float sl2 = L.scale_log2;
+        bool pending = true;        // quad-uniform: some column of the quad has no max yet
+        int bver = -1;              // version of the m values in this group's bias snapshot
         for (int t = grp; t < ntiles; t += 2) {
-            const int sb = t & 1;
+            const int sb = grp, slot = (t >> 1) & 1;
             const TileInfo ti = s_tiles[t];
-            mbar_wait(&bar_sfull[sb], (t >> 1) & 1);
+            mbar_wait_dbg(&bar_sfull[sb], (t >> 1) & 1, dbgp, 21);
             tc_fence_after();
             float x[64];
             tmem_ld16_f(tS0 + 128 * sb + lane_off + c0, x);
@@ -739,30 +793,78 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 fast = __all_sync(0xffffffffu, c_first <= c0);
             }
 #pragma unroll
-            for (int k = 0; k < 64; k += 2) ffma2(x[k], x[k + 1], sl2, 0.f, 0.f);
+            for (int k = 0; k < 64; k += 2) ffma2(x[k], x[k + 1], sl2, 0.f, 0.f);  // s*scale*log2e - m_used
             if (!fast) {
 #pragma unroll
                 for (int k = 0; k < 64; ++k)
                     if (c0 + k < c_first) x[k] = -INFINITY;
             }
-            float m8[8];
+            bool slow = pending || *reinterpret_cast<volatile int*>(&s_ver[ch]) != bver;
+            if (!slow) {
+                float m8[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                float m = max3f(x[8 * j], x[8 * j + 1], x[8 * j + 2]);
-                m = max3f(m, x[8 * j + 3], x[8 * j + 4]);
-                m = max3f(m, x[8 * j + 5], x[8 * j + 6]);
-                m8[j] = fmaxf(m, x[8 * j + 7]);
+                for (int j = 0; j < 8; ++j) {
+                    float m = max3f(x[8 * j], x[8 * j + 1], x[8 * j + 2]);
+                    m = max3f(m, x[8 * j + 3], x[8 * j + 4]);
+                    m = max3f(m, x[8 * j + 5], x[8 * j + 6]);
+                    m8[j] = fmaxf(m, x[8 * j + 7]);
+                }
+                const float xmax =
+                    max3f(max3f(m8[0], m8[1], m8[2]), max3f(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+                slow = !(xmax <= kTau);
             }
-            const float xmax = max3f(max3f(m8[0], m8[1], m8[2]), max3f(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
-            if (bar_red_or(bar_id, !(xmax <= kTau))) {
-                // (experiment: a real slow path updates the shared running max here)
+            if (bar_red_or(bar_id, slow)) {
+                if (DBG && dbgp && r == 0) atomicAdd(dbgp + 8, 1);
+                // ---- slow path (quad): x is relative to m_used[grp]
 #pragma unroll
-                for (int k = 0; k < 64; ++k) x[k] = fminf(x[k], kTau);
+                for (int k = 0; k < 64; ++k) s_red2[grp][wq][c0 + k] = redux_max(x[k]);
+                named_bar(bar_id, 128);
+                bool grew = false;
+                if (r < 64) {
+                    const int c = c0 + r;
+                    const float tm = fmaxf(fmaxf(s_red2[grp][0][c], s_red2[grp][1][c]),
+                                           fmaxf(s_red2[grp][2][c], s_red2[grp][3][c]));
+                    const float mu = s_mused[grp][c];
+                    const float tabs = tm + (mu == -INFINITY ? 0.f : mu);  // absolute column max
+                    const float mc = unord_f32(static_cast<uint32_t>(
+                        *reinterpret_cast<volatile unsigned long long*>(&s_mcur[c]) >> 32));
+                    if (tm > -INFINITY && (mc == -INFINITY || tabs > mc + kTau)) {
+                        const float b = F16Traits<T>::round(fminf(fmaxf(-tabs / (16.f * sl2), -60000.f), 60000.f));
+                        const float mnew = -16.f * b * sl2;
+                        const uint32_t bb = F16Traits<T>::pack(b, b) & 0xFFFFu;
+                        atomicMax(&s_mcur[c], (static_cast<unsigned long long>(ord_f32(mnew)) << 32) | bb);
+                        grew = true;
+                    }
+                }
+                grew = bar_red_or(bar_id, grew);  // every atomicMax of the quad done
+                if (DBG && dbgp && grew && r == 0) atomicAdd(dbgp + 10, 1);
+                if (r == 0) {
+                    if (grew) atomicAdd(&s_ver[ch], 1);
+                    s_vsnap[grp][ch] = *reinterpret_cast<volatile int*>(&s_ver[ch]);
+                }
+                named_bar(bar_id, 128);
+                bver = s_vsnap[grp][ch];  // values read below are at least this recent
+                bool pend = false;
+                if (r < 64) {
+                    const int c = c0 + r;
+                    const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(&s_mcur[c]);
+                    const float mt = unord_f32(static_cast<uint32_t>(cur >> 32));
+                    const float mu = s_mused[grp][c];
+                    s_dl[grp][c] = mt == -INFINITY ? 0.f : mt - (mu == -INFINITY ? 0.f : mu);
+                    s_mused[grp][c] = mt;
+                    const uint32_t w = mt == -INFINITY ? 0u : static_cast<uint32_t>(cur & 0xFFFFu) * 0x10001u;
+                    bias_rows[sb * 128 + c] = make_uint4(w, w, w, w);  // GEMM1(t+2) reads it after sempty
+                    pend = mt == -INFINITY;
+                    fence_async_smem();
+                }
+                pending = bar_red_or(bar_id, pend);  // also publishes s_dl / s_mused / bias rows
+#pragma unroll
+                for (int k = 0; k < 64; ++k) x[k] -= s_dl[grp][c0 + k];
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_sempty[sb]);
-            if (t >= 2) mbar_wait(&bar_pempty[sb], ((t >> 1) - 1) & 1);
+            if (lane == 0) mbar_arrive(&bar_sempty[sb]);  // S^T[sb] consumed
+            if (t >= 2) mbar_wait_dbg(&bar_pempty[sb], ((t >> 1) - 1) & 1, dbgp, 22);  // P^T[sb] free (GEMM2(t-2) done)
             uint8_t* const pbuf = pbuf0 + sb * lay.p_bytes;
 #pragma unroll
             for (int g8 = 0; g8 < 8; ++g8) {
@@ -777,24 +879,101 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 }
                 const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
                                             F16Traits<T>::pack(p[4], p[5]), F16Traits<T>::pack(p[6], p[7]));
-                *reinterpret_cast<uint4*>(pbuf + pt_base_h + ((static_cast<uint32_t>(g8) ^ r7) << 4)) = hi;
+                const uint32_t pto = pt_base_h + ((static_cast<uint32_t>(g8) ^ r7) << 4);
+                *reinterpret_cast<uint4*>(pbuf + pto) = hi;
+                if (HILO) {
+                    float rr[8];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t w = (&hi.x)[k];
+                        rr[2 * k] = p[2 * k] - F16Traits<T>::to_float(static_cast<uint16_t>(w & 0xFFFF));
+                        rr[2 * k + 1] = p[2 * k + 1] - F16Traits<T>::to_float(static_cast<uint16_t>(w >> 16));
+                    }
+                    const uint4 lo = make_uint4(F16Traits<T>::pack(rr[0], rr[1]), F16Traits<T>::pack(rr[2], rr[3]),
+                                                F16Traits<T>::pack(rr[4], rr[5]), F16Traits<T>::pack(rr[6], rr[7]));
+                    *reinterpret_cast<uint4*>(pbuf + 32768 + pto) = lo;
+                }
+            }
+            // ---- publish the m this tile used; O^T / l to it when tile t-1 used another
+            // (between GEMM2(t-1) and GEMM2(t)).  Per-column compare of exact values:
+            // a version match alone does not imply equal values across the groups.
+            if (r < 64) s_mt[grp][slot][c0 + r] = s_mused[grp][c0 + r];
+            bool need = false;
+            if (t >= 1) {
+                const int pg = grp ^ 1, ps = ((t - 1) >> 1) & 1;
+                if (lane == 0) {
+                    long long spins = 0;
+                    while (ld_acquire_cta(&s_tdone[pg][ps][ch]) != t - 1) {
+                        __nanosleep(32);
+                        if (DBG && dbgp && ++spins > (1ll << 22)) {
+                            if (atomicCAS(dbgp, 0, 25) == 0) {
+                                dbgp[1] = ld_acquire_cta(&s_tdone[pg][ps][ch]);
+                                dbgp[2] = static_cast<int>(blockIdx.x + 1000 * blockIdx.y + 100000 * blockIdx.z);
+                                dbgp[3] = static_cast<int>(threadIdx.x) + 10000 * t;
+                                __threadfence_system();
+                            }
+                            asm volatile("trap;");
+                        }
+                    }
+                }
+                __syncwarp();
+                if (r < 64) need = s_mt[pg][ps][c0 + r] != s_mused[grp][c0 + r];
+            }
+            need = bar_red_or(bar_id, need);  // also: this quad's s_mt values are all stored
+            if (r == 0) st_release(&s_tdone[grp][slot][ch], t);
+            if (need) {
+                if (DBG && dbgp && r == 0) atomicAdd(dbgp + 9, 1);
+                const int pg = grp ^ 1, ps = ((t - 1) >> 1) & 1;
+                mbar_wait_dbg(&bar_pempty[pg], ((t - 1) >> 1) & 1, dbgp, 23);  // GEMM2(t-1) complete
+                tc_fence_after();
+                if (r < 64) {
+                    const int c = c0 + r;
+                    const float mp = s_mt[pg][ps][c], mt = s_mused[grp][c];
+                    s_al[grp][c] = (mp == -INFINITY || mt == -INFINITY) ? 1.f : fast_exp2(mp - mt);
+                }
+                named_bar(bar_id, 128);
+#pragma unroll 1
+                for (int k8 = 0; k8 < 64; k8 += 8) {
+                    uint32_t v[8];
+                    tmem_ld_cols<8>(tO + lane_off + c0 + k8, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) v[k] = __float_as_uint(__uint_as_float(v[k]) * s_al[grp][c0 + k8 + k]);
+                    tmem_st4(tO + lane_off + c0 + k8, v[0], v[1], v[2], v[3]);
+                    tmem_st4(tO + lane_off + c0 + k8 + 4, v[4], v[5], v[6], v[7]);
+                }
+                if ((wq >> 1) == ch) {  // this lane quarter holds l of queries 32 wq + lane
+                    uint32_t lv;
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(lv) : "r"(tL + lane_off));
+                    tmem_ld_wait();
+                    const float ln = __uint_as_float(lv) * s_al[grp][r];
+                    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tL + lane_off),
+                                 "r"(__float_as_uint(ln)));
+                }
+                tmem_st_wait();
+                tc_fence_before();
             }
             fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_pfull[sb]);
         }
-        // epilogue: group 0 writes O^T / l (l from the l-MMA accumulator)
-        if (ntiles > 0) mbar_wait(&bar_pempty[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
-        tc_fence_after();
-        if (grp == 0) {
-            if (ch == 0) {
-                uint32_t lv[1];
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(lv[0]) : "r"(tmem + 416u + lane_off));
-                tmem_ld_wait();
-                const float l = __uint_as_float(lv[0]);
+        // ---- epilogue: O^T / l after the last GEMM2 (l from the row-sum accumulator),
+        // by the group of the last tile: it already waited on that P^T buffer's
+        // previous phase, so the parity wait below cannot alias an older phase
+        const int egrp = ntiles > 0 ? (ntiles - 1) & 1 : 0;
+        if (grp == egrp) {
+            if (ntiles > 0) mbar_wait_dbg(&bar_pempty[egrp], ((ntiles - 1) >> 1) & 1, dbgp, 24);
+            tc_fence_after();
+            if ((wq >> 1) == ch) {
+                uint32_t lv = 0;
+                if (ntiles > 0) {
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(lv) : "r"(tL + lane_off));
+                    tmem_ld_wait();
+                }
+                const float l = __uint_as_float(lv);
                 s_alpha[r] = l > 0.f ? 1.f / l : 0.f;
             }
-            named_bar(1, 256);
+            named_bar(5, 256);  // the epilogue group only (ids 1-4 are the quads' barriers)
             float* out = L.out + (static_cast<int64_t>(u * L.gqa + h) * L.n_q + q0) * kHeadDim;
 #pragma unroll 1
             for (int k16 = 0; k16 < 64; k16 += 16) {
@@ -804,12 +983,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
 #pragma unroll
                 for (int k = 0; k < 16; ++k) {
                     const int c = c0 + k16 + k;
-                    if (c < rows_q) out[c * kHeadDim + r] = v[k] * s_alpha[c];
+                    if (c < rows_q) out[c * kHeadDim + r] = ntiles > 0 ? v[k] * s_alpha[c] : 0.f;
                 }
             }
         }
-    }
-#else
     } else {
         // ------------------------------------------------------- softmax WGs
         // kSoftWG warpgroups; WG g owns query columns [kCols*g, kCols*(g+1)); warp
@@ -1066,7 +1243,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             }
         }
     }
-#endif
     tc_fence_before();
     __syncthreads();
     if (warp == kWarpMma) tmem_dealloc(tmem, 512);
@@ -1094,7 +1270,6 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     lay.off_q = 0;
     lay.off_p = 32768;
     lay.p_bytes = hilo ? 65536u : 32768u;  // P^T (hi [+ lo]) per buffer
-    const uint32_t budget = 227u * 1024u - 8192u /*static smem*/ - 1024u /*align*/ - tiles_bytes - kBiasBytes;
     // Preference order: 2 K + 2 V stages with two P^T buffers, then fewer P^T
     // buffers, then shallower rings.
     // V(t) is consumed a softmax period after K(t), so one V stage is enough to
@@ -1102,24 +1277,35 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     // tiles leave no room for both.
     const uint32_t plans[][3] = {{2, 3, 3}, {2, 2, 3}, {2, 3, 2}, {2, 2, 2}, {2, 3, 1}, {2, 2, 1}, {1, 2, 2},
                                  {2, 1, 2}, {1, 2, 1}, {1, 1, 2}, {1, 1, 1}};
-    bool ok = false;
-    for (const auto& pl : plans) {
-        const uint32_t need = 32768u + pl[0] * lay.p_bytes + pl[1] * lay.k_stage + pl[2] * lay.v_stage;
-        if (need <= budget) {
-            lay.n_pbuf = pl[0];
-            lay.nk = pl[1];
-            lay.nv = pl[2];
-            ok = true;
-            break;
+    auto choose = [&](uint32_t static_bytes) {
+        const uint32_t budget = 227u * 1024u - static_bytes - 1024u /*align*/ - tiles_bytes - kBiasBytes;
+        for (const auto& pl : plans) {
+            const uint32_t need = 32768u + pl[0] * lay.p_bytes + pl[1] * lay.k_stage + pl[2] * lay.v_stage;
+            if (need <= budget) {
+                lay.n_pbuf = pl[0];
+                lay.nk = pl[1];
+                lay.nv = pl[2];
+                return true;
+            }
         }
-    }
-    if (!ok) return cudaErrorInvalidConfiguration;
+        return false;
+    };
+    // The ping-pong softmax (alternate tiles per 8-warp group, row sums on the
+    // tensor core) needs one P^T buffer per group: fp16 P (bf16 P^T is hi + lo,
+    // 64 KB a buffer) and a plan with two buffers.  It pays when the softmax
+    // bounds the tile (fully 2:4 caches: +13% at 32K); with dense stages the
+    // shallow rings bound it and the lockstep softmax is 6-9% faster.
+    bool pp = !hilo && !kden && !vden && getenv("HS_PREFILL_NO_PP") == nullptr && choose(12288u) &&
+              lay.n_pbuf == 2;
+    if (getenv("HS_PREFILL_FORCE_PP")) pp = !hilo && choose(12288u) && lay.n_pbuf == 2;  // tools
+    if (!pp && !choose(8192u)) return cudaErrorInvalidConfiguration;
     if (const char* env = getenv("HS_PREFILL_PLAN")) {  // tools: "pbuf,nk,nv"
         unsigned a, b, c;
         if (sscanf(env, "%u,%u,%u", &a, &b, &c) == 3) {
             lay.n_pbuf = a;
             lay.nk = b;
             lay.nv = c;
+            pp = pp && a == 2;
         }
     }
     lay.off_k = lay.off_p + lay.n_pbuf * lay.p_bytes;
@@ -1127,8 +1313,8 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     lay.off_tiles = lay.off_v + lay.nv * lay.v_stage;
     lay.off_bias = lay.off_tiles + tiles_bytes;
     size_t smem = lay.off_bias + kBiasBytes + 1024;
-    const size_t epi = lay.off_p + kSoftWG * 128 * (kCols + 1) * 4 + 1024;
-    if (smem < epi) smem = epi;
+    const size_t epi = lay.off_p + kSoftWG * 128 * (kCols + 1) * 4 + 1024;  // lockstep epilogue scratch
+    if (!pp && smem < epi) smem = epi;
     {
         const int kb = L.n_units * L.k_sparse_count, vb = L.n_units * L.v_sparse_count;
         if (kb + vb > 0) {
@@ -1153,8 +1339,13 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
         return cudaSuccess;
     };
     cudaError_t e;
-    if (L.bf16) e = dbg ? launch(prefill_kernel<__nv_bfloat16, true, true>) : launch(prefill_kernel<__nv_bfloat16, true, false>);
-    else e = dbg ? launch(prefill_kernel<__half, false, true>) : launch(prefill_kernel<__half, false, false>);
+    if (L.bf16)
+        e = dbg ? launch(prefill_kernel<__nv_bfloat16, true, true, false>)
+                : launch(prefill_kernel<__nv_bfloat16, true, false, false>);
+    else if (pp)
+        e = dbg ? launch(prefill_kernel<__half, false, true, true>) : launch(prefill_kernel<__half, false, false, true>);
+    else
+        e = dbg ? launch(prefill_kernel<__half, false, true, false>) : launch(prefill_kernel<__half, false, false, false>);
     if (e) return e;
     return cudaGetLastError();
 }
