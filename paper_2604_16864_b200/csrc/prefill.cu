@@ -1277,9 +1277,17 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     // tiles leave no room for both.
     const uint32_t plans[][3] = {{2, 3, 3}, {2, 2, 3}, {2, 3, 2}, {2, 2, 2}, {2, 3, 1}, {2, 2, 1}, {1, 2, 2},
                                  {2, 1, 2}, {1, 2, 1}, {1, 1, 2}, {1, 1, 1}};
-    auto choose = [&](uint32_t static_bytes) {
+    // The ping-pong softmax moves the bound to the rings: it prefers two V stages
+    // over two K stages when dense stages leave room for only three.
+    const uint32_t plans_pp[][3] = {{2, 3, 3}, {2, 2, 3}, {2, 3, 2}, {2, 2, 2}, {2, 1, 3}, {2, 1, 2}, {2, 3, 1},
+                                    {2, 2, 1}};
+    auto choose = [&](uint32_t static_bytes, bool for_pp) {
         const uint32_t budget = 227u * 1024u - static_bytes - 1024u /*align*/ - tiles_bytes - kBiasBytes;
-        for (const auto& pl : plans) {
+        const uint32_t(*list)[3] = for_pp ? plans_pp : plans;
+        const int n = for_pp ? static_cast<int>(sizeof(plans_pp) / sizeof(plans_pp[0]))
+                             : static_cast<int>(sizeof(plans) / sizeof(plans[0]));
+        for (int i = 0; i < n; ++i) {
+            const uint32_t* pl = list[i];
             const uint32_t need = 32768u + pl[0] * lay.p_bytes + pl[1] * lay.k_stage + pl[2] * lay.v_stage;
             if (need <= budget) {
                 lay.n_pbuf = pl[0];
@@ -1292,13 +1300,12 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     };
     // The ping-pong softmax (alternate tiles per 8-warp group, row sums on the
     // tensor core) needs one P^T buffer per group: fp16 P (bf16 P^T is hi + lo,
-    // 64 KB a buffer) and a plan with two buffers.  It pays when the softmax
-    // bounds the tile (fully 2:4 caches: +13% at 32K); with dense stages the
-    // shallow rings bound it and the lockstep softmax is 6-9% faster.
-    bool pp = !hilo && !kden && !vden && getenv("HS_PREFILL_NO_PP") == nullptr && choose(12288u) &&
-              lay.n_pbuf == 2;
-    if (getenv("HS_PREFILL_FORCE_PP")) pp = !hilo && choose(12288u) && lay.n_pbuf == 2;  // tools
-    if (!pp && !choose(8192u)) return cudaErrorInvalidConfiguration;
+    // 64 KB a buffer) and a plan with two buffers.  Measured at 64K: +11% on
+    // fully 2:4 caches (softmax-bound), +1-2% with dense stages (ring-bound, hence
+    // the two-V-stage plan preference above).
+    bool pp = !hilo && getenv("HS_PREFILL_NO_PP") == nullptr && choose(12288u, true) && lay.n_pbuf == 2;
+    if (getenv("HS_PREFILL_FORCE_PP")) pp = !hilo && choose(12288u, true) && lay.n_pbuf == 2;  // tools
+    if (!pp && !choose(8192u, false)) return cudaErrorInvalidConfiguration;
     if (const char* env = getenv("HS_PREFILL_PLAN")) {  // tools: "pbuf,nk,nv"
         unsigned a, b, c;
         if (sscanf(env, "%u,%u,%u", &a, &b, &c) == 3) {
