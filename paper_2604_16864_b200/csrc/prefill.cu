@@ -230,7 +230,7 @@ __device__ __forceinline__ void exp2_fma2(float& x0, float& x1) {
 #ifndef HS_PREFILL_POLY
 #define HS_PREFILL_POLY 2  // of every 8 exponentials, this many run on the FMA pipe
 #endif
-constexpr int kPolyPer8 = HS_PREFILL_POLY;
+constexpr int kPolyPer8 = HS_PREFILL_POLY;  // default for the lockstep softmax
 static_assert(kPolyPer8 % 2 == 0, "polynomial exponentials run in packed pairs");
 
 #ifndef HS_PREFILL_EXP_F16X2
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(128) tail_prep_kernel(const uint16_t* __restri
     }
 }
 
-template <typename T, bool HILO, bool DBG, bool PP>
+template <typename T, bool HILO, bool DBG, bool PP, int POLY = kPolyPer8>
 __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_constant__ PrefillLaunch L,
                                                                PrefillLayout lay) {
     // DBG: tools-only instrumentation (per-tile trace, watchdog waits, mode
@@ -870,9 +870,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             for (int g8 = 0; g8 < 8; ++g8) {
                 float p[8];
 #pragma unroll
-                for (int k = 0; k < 8 - kPolyPer8; ++k) p[k] = fast_exp2(x[8 * g8 + k]);
+                for (int k = 0; k < 8 - POLY; ++k) p[k] = fast_exp2(x[8 * g8 + k]);
 #pragma unroll
-                for (int k = 8 - kPolyPer8; k < 8; k += 2) {
+                for (int k = 8 - POLY; k < 8; k += 2) {
                     p[k] = x[8 * g8 + k];
                     p[k + 1] = x[8 * g8 + k + 1];
                     exp2_fma2(p[k], p[k + 1]);
@@ -1186,9 +1186,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 }
                 float p[8];
 #pragma unroll
-                for (int k = 0; k < 8 - kPolyPer8; ++k) p[k] = fast_exp2(x[8 * g8 + k]);  // exp2(-inf) = 0
+                for (int k = 0; k < 8 - POLY; ++k) p[k] = fast_exp2(x[8 * g8 + k]);  // exp2(-inf) = 0
 #pragma unroll
-                for (int k = 8 - kPolyPer8; k < 8; k += 2) {
+                for (int k = 8 - POLY; k < 8; k += 2) {
                     p[k] = x[8 * g8 + k];
                     p[k + 1] = x[8 * g8 + k + 1];
                     exp2_fma2(p[k], p[k + 1]);
@@ -1349,8 +1349,10 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     if (L.bf16)
         e = dbg ? launch(prefill_kernel<__nv_bfloat16, true, true, false>)
                 : launch(prefill_kernel<__nv_bfloat16, true, false, false>);
-    else if (pp)
-        e = dbg ? launch(prefill_kernel<__half, false, true, true>) : launch(prefill_kernel<__half, false, false, true>);
+    else if (pp && !kden && !vden)  // softmax-bound: a quarter of the exponentials on the FMA pipe
+        e = dbg ? launch(prefill_kernel<__half, false, true, true, 2>) : launch(prefill_kernel<__half, false, false, true, 2>);
+    else if (pp)  // ring-bound (dense stages): every exponential on the SFU (2.5% faster than a quarter)
+        e = dbg ? launch(prefill_kernel<__half, false, true, true, 0>) : launch(prefill_kernel<__half, false, false, true, 0>);
     else
         e = dbg ? launch(prefill_kernel<__half, false, true, false>) : launch(prefill_kernel<__half, false, false, false>);
     if (e) return e;
