@@ -172,3 +172,28 @@ def test_prefill_rejects_invalid(hs, port):
     big = np.zeros((1, 1, 512, 128), np.float32)
     with pytest.raises(ConfigError):
         hs.prefill_attention(to_torch(big, "f16"), kc, vc, causal=True)  # n_q > n_kv
+
+
+@pytest.mark.parametrize("seed", [7, 8])
+def test_prefill_random_shapes(hs, port, seed):
+    """Randomised shapes (sequence length, query count, sparsity, protection,
+    causality, units, GQA) on the fp16 ping-pong path against the oracle."""
+    rng = np.random.default_rng(seed)
+    for i in range(4):
+        L = int(rng.choice([128, 256, 384, 640, 1024]))
+        n_q = int(rng.integers(1, L + 1))
+        s = float(rng.choice([0.0, 0.25, 0.5, 0.75, 1.0]))
+        sink, window = int(rng.choice([0, 64, 100])), int(rng.choice([0, 128, 200]))
+        causal = bool(rng.integers(0, 2))
+        U, gqa = int(rng.integers(1, 3)), int(rng.integers(1, 3))
+        kc, vc, q = setup(hs, port, U, L, s, "f16", gqa, n_q, sink, window, seed=seed * 10 + i)
+        scale = np.float32(1.0 / math.sqrt(128))
+        got = hs.prefill_attention(to_torch(q, "f16"), kc, vc, causal=causal, scale=float(scale)).cpu().numpy()
+
+        def one(ug):
+            u, g = divmod(ug, gqa)
+            return port.prefill(q[u, g], device_to_oracle(kc, u), device_to_oracle(vc, u), None, None, causal,
+                                scale, 64)
+        want = np.stack(parallel(one, range(U * gqa))).reshape(U, gqa, n_q, 128)
+        mx, mr = err_stats(got, want)
+        assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (L, n_q, s, sink, window, causal, U, gqa, mx, mr)
