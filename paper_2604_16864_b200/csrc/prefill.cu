@@ -13,17 +13,22 @@
 // sparse pairs, then dense pairs, then single/mixed and diagonal blocks (order
 // only changes float rounding; attention is order invariant over visible keys).
 //
-// Warp roles (352 threads):
-//   0-7  softmax, two warpgroups: WG g owns query columns 64g..64g+63; warp w
-//        reads TMEM lanes 32(w%4).. (key row r of the tile = d row of O^T).
-//        Exact per-tile column max (redux.f32 + smem), running max updated only
-//        when it grows by > 2^8 (FA4-style lazy rescale), P^T written to smem
-//        (MN-major SW128, N-atom g) for GEMM2, O^T / l rescaled only on the rare
-//        max update; epilogue normalises O.
-//   8    TMA producer: Q once; per key tile K/V pools + canonical metadata.
-//   9    MMA issuer: tcgen05.cp metadata -> TMEM, GEMM1 (t), GEMM2 (t-1).
-//   10   metadata: permutes canonical 2-bit codes (nm_metadata.hpp:42-46) into
-//        the tcgen05 TMEM metadata atom (pinned by tools/probes/umma_probe.cu).
+// Warp roles (608 threads, 19 warps, 96 registers):
+//   0-15 softmax.  fp16 (ping-pong): two 8-warp groups take alternate tiles
+//        (group g: S^T buffer g, P^T buffer g, GEMM1 bias operand g); warp
+//        (g, wq, ch) covers key lanes 32 wq.. and query columns 64 ch..; row sums
+//        l come from the tensor core.  bf16 (lockstep): 4 warpgroups of 32 query
+//        columns work on every tile, l in registers.  Both: the running max is
+//        folded into GEMM1 as a rank-1 bias MMA (x = S^T * scale log2e), a tile
+//        needs no cross-lane reduction unless a column grows past m + tau
+//        (FA4-style lazy rescale), P^T is written to smem (MN-major SW128) for
+//        GEMM2, a quarter of the exponentials can run on the FMA pipe.
+//   16   TMA producer: tile list, Q once, K tiles (3-D box for dense) and V
+//        tiles (256-row box for consecutive slots) with prepared metadata atoms.
+//   17   GEMM1 issuer: tcgen05.cp metadata -> TMEM, bias MMA + K Q^T (mma.sp for
+//        2:4 tiles); TMEM owner.
+//   18   GEMM2 issuer: O^T += V^T P^T (+ the l MMA P^T x ones in ping-pong mode).
+// See DESIGN.md section 3.3 for the measured bounds and the rejected variants.
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -37,7 +42,7 @@ namespace {
 #ifndef HS_PREFILL_WG
 #define HS_PREFILL_WG 4
 #endif
-constexpr int kSoftWG = HS_PREFILL_WG;     // softmax warpgroups (each owns kCols query columns); 4 + 4 role warps = 20 warps
+constexpr int kSoftWG = HS_PREFILL_WG;     // lockstep softmax warpgroups (each owns kCols query columns)
 constexpr int kCols = 128 / kSoftWG;       // query columns per softmax thread
 constexpr int kSoftWarps = 4 * kSoftWG;
 constexpr int kWarpK = kSoftWarps;         // TMA producer: tile list, Q and K tiles
