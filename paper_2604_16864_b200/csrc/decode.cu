@@ -7,16 +7,20 @@
 // the sparse tensor-core MMA and the canonical metadata words feed the MMA
 // metadata register unchanged.
 //
-// Data path (HBM-bound): one producer warp streams each block's surviving
-// values (TMA 2-D tiles, hardware swizzle) and metadata (1-D bulk copies) into
-// an mbarrier ring; consumer warps each own a block at a time:
+// Data path (HBM-bound): every consumer warp streams its own blocks' surviving
+// values (TMA 2-D tiles, hardware swizzle) and metadata (1-D bulk copies) through
+// a private mbarrier-tracked stage and owns one block at a time.  In auto-split
+// mode with short ranges, lane 0 claims the unit's next block with an atomic
+// (dynamic balance); otherwise a CTA streams its contiguous static range:
 //   GEMM1  mma.sp m16n8k32  K nnz [64 keys x 64] x Q^T (GQA rows stacked on N)
 //   softmax in registers (fp32), warp shuffles over the key lanes
 //   P^T    movmatrix relayout of the accumulator fragment (the paper's
 //          "RelayoutFragment"); bf16 P as a hi+lo pair
 //   GEMM2  mma.sp m16n8k32  V^T nnz [128 ch x 32] x P^T
 // Dense blocks take the dense m16n8k16 path.  Warps, then CTAs of a unit,
-// merge (m, l, O) with the reference combine; the last CTA per unit finishes.
+// merge (m, l, O) with the reference combine: cooperatively (every CTA merges a
+// slice once the unit's partials are in) when the grid is resident, otherwise
+// in the unit's last CTA.
 #include "common.cuh"
 #include "kernels.h"
 
