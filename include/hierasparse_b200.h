@@ -100,6 +100,21 @@ typedef struct {
 HS_API const char* hs_last_error(void);
 HS_API int hs_version(void);
 
+/* Status words.  Entry points that validate *data* (the reference's DataErrors
+ * raised while reading a cache or a mask) stay asynchronous: their kernels
+ * record the first error, in the reference's iteration order, into a
+ * caller-owned, zero-initialised device uint64 (`status`; NULL = not
+ * reported).  The caller reads the word whenever it synchronises anyway and
+ * hs_status_word_decode turns it into the status code + hs_last_error()
+ * message the reference would have thrown:
+ *   decompress: index map holds a zero entry / dangling dense offset /
+ *   dangling sparse offset (compressed_cache.hpp:279-286); unpack_metadata:
+ *   corrupt metadata, codes not increasing (nm_metadata.hpp:107); compress:
+ *   group keeps more / fewer than n_keep elements (compressed_cache.hpp:216-223)
+ *   -> HS_ERR_DATA; a BlockMask whose dense count differs from the cache's
+ *   dense pool -> HS_ERR_CONFIG.  Several calls may share one word. */
+HS_API hs_status hs_status_word_decode(uint64_t word);
+
 /* Pool geometry known before any data is seen (no device sync needed):
  * protected prefix/suffix rounding and clamping (masks.hpp:93-98,
  * pruner.hpp:127-131) and quota = floor(S * prunable) (pruner.hpp:106-108). */
@@ -132,19 +147,33 @@ HS_API hs_status hs_prune_compress(const void* src, uint64_t src_unit_stride, ui
 
 /* fused_magnitude_compress (compressed_cache.hpp:262-267) under a given
  * BlockMask: flags u8 [n_units][nb] device, 1 = dense.  out->dense_count and
- * sparse_count must equal the flag counts. */
+ * sparse_count must equal the flag counts (checked on the device: status). */
 HS_API hs_status hs_compress_with_flags(const void* src, uint64_t src_unit_stride, uint64_t rows,
-                                        const uint8_t* flags, hs_device_cache* out, void* stream);
+                                        const uint8_t* flags, hs_device_cache* out, uint64_t* status,
+                                        void* stream);
+
+/* compress (compressed_cache.hpp:196-225): the two-phase packer under an
+ * explicit HierarchicalMask = ElementMask (u8 [n_units][rows][head_dim],
+ * nonzero = kept, unit stride mask_unit_stride elements; 0 = rows*head_dim)
+ * + BlockMask (flags as above).  Dense blocks are copied verbatim; every 2:4
+ * group of a sparse block must keep exactly two elements, else status records
+ * "group keeps more / fewer than n_keep elements" for the first offending
+ * group (block, stored row, group order). */
+HS_API hs_status hs_compress_with_mask(const void* src, uint64_t src_unit_stride, uint64_t rows,
+                                       const uint8_t* element_mask, uint64_t mask_unit_stride,
+                                       const uint8_t* flags, hs_device_cache* out, uint64_t* status,
+                                       void* stream);
 
 /* Decode-phase re-prune of an already compressed cache (pipeline.hpp:227-240:
  * decompress -> prune_cache at the decode sparsity -> compress) in one pass over
  * the input pools: blocks are expanded on the fly, never written dense to HBM.
  * Results are bit-identical to hs_decompress followed by hs_prune_compress;
- * a corrupt input returns HS_ERR_DATA with decompress's messages.  in and out
+ * a corrupt input records decompress's DataErrors in status.  in and out
  * share axis, dtype, units and shape; out's pools are sized by hs_pool_counts
  * for rows = in->logical_blocks * block_size. */
 HS_API hs_status hs_recompress(const hs_device_cache* in, const hs_sparsity_config* cfg, double sparsity,
-                               hs_device_cache* out, double* losses, uint8_t* flags, void* stream);
+                               hs_device_cache* out, double* losses, uint8_t* flags, uint64_t* status,
+                               void* stream);
 
 /* Dense-tail growth (CacheView::dense_tail attention.hpp:19-31):
  * the cache re-pruned over its blocks followed by tail_rows (a multiple of
@@ -157,10 +186,12 @@ HS_API hs_status hs_recompress(const hs_device_cache* in, const hs_sparsity_conf
  * tail's remaining (< block_size) tokens as the new dense tail. */
 HS_API hs_status hs_absorb_tail(const hs_device_cache* in, const void* tail, uint64_t tail_unit_stride,
                                 uint64_t tail_rows, const hs_sparsity_config* cfg, double sparsity,
-                                hs_device_cache* out, double* losses, uint8_t* flags, void* stream);
+                                hs_device_cache* out, double* losses, uint8_t* flags, uint64_t* status,
+                                void* stream);
 
-/* decompress (compressed_cache.hpp:271-298): dst dtype [n_units][rows][d]. */
-HS_API hs_status hs_decompress(const hs_device_cache* c, void* dst, void* stream);
+/* decompress (compressed_cache.hpp:271-298): dst dtype [n_units][rows][d];
+ * zero / dangling index entries and corrupt metadata are recorded in status. */
+HS_API hs_status hs_decompress(const hs_device_cache* c, void* dst, uint64_t* status, void* stream);
 
 /* ----------------------------------------------------------- attention --- */
 /* decode_attention (attention.hpp:360-409) for every unit at once.

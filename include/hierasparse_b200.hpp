@@ -227,36 +227,89 @@ inline std::pair<DeviceCompressedCache, DeviceCompressedCache> prune_cache(const
             compress_one(value, dtype, n_units, rows, cfg, cfg.s_value, GroupAxis::kSequence, stream)};
 }
 
+// Device status word (hierasparse_b200.h "status words"): the data-validating
+// entry points record the reference's DataErrors here asynchronously.
+class StatusWord {
+public:
+    explicit StatusWord(cudaStream_t stream = nullptr) : w_(1) {
+        check_cuda(cudaMemsetAsync(w_.get(), 0, sizeof(uint64_t), stream), "cudaMemsetAsync");
+    }
+    uint64_t* get() const { return w_.get(); }
+    // Synchronises on `stream` and throws what the reference would have thrown.
+    void check(cudaStream_t stream = nullptr) const {
+        uint64_t h = 0;
+        check_cuda(cudaMemcpyAsync(&h, w_.get(), sizeof h, cudaMemcpyDeviceToHost, stream), "cudaMemcpyAsync");
+        check_cuda(cudaStreamSynchronize(stream), "status word");
+        hierasparse::b200::check(hs_status_word_decode(h));
+    }
+
+private:
+    DeviceBuffer<uint64_t> w_;
+};
+
 // fused_magnitude_compress (compressed_cache.hpp:262-267) under an explicit
 // BlockMask: flags device u8 [n_units][nb], 1 = dense; dense_count per unit.
+// status == nullptr: checked (synchronising) like the reference; otherwise the
+// ConfigError of a mismatched dense count is left in *status (asynchronous).
 inline DeviceCompressedCache fused_magnitude_compress(const void* src, const uint8_t* flags_dev,
                                                       uint32_t dense_count, DType dtype, uint32_t n_units,
                                                       std::size_t rows, GroupAxis axis, std::size_t block_size = 64,
-                                                      cudaStream_t stream = nullptr, uint32_t head_dim = 128) {
+                                                      cudaStream_t stream = nullptr, uint32_t head_dim = 128,
+                                                      StatusWord* status = nullptr) {
     if (block_size == 0 || rows % block_size) throw ConfigError("compress: sequence length not divisible by block_size");
     const uint32_t nb = static_cast<uint32_t>(rows / block_size);
     DeviceCompressedCache out(dtype, axis, n_units, nb, dense_count, nb - dense_count, head_dim,
                               static_cast<uint32_t>(block_size));
-    check(hs_compress_with_flags(src, rows * head_dim, rows, flags_dev, &out.desc(), stream));
+    StatusWord own(stream);
+    StatusWord* st = status ? status : &own;
+    check(hs_compress_with_flags(src, rows * head_dim, rows, flags_dev, &out.desc(), st->get(), stream));
+    if (!status) own.check(stream);
+    return out;
+}
+
+// compress (compressed_cache.hpp:196-225) under an explicit HierarchicalMask:
+// element mask device u8 [n_units][rows][head_dim] + BlockMask flags.  Groups of
+// sparse blocks keeping != 2 elements throw DataError (or land in *status).
+inline DeviceCompressedCache compress(const void* src, const uint8_t* element_mask_dev, const uint8_t* flags_dev,
+                                      uint32_t dense_count, DType dtype, uint32_t n_units, std::size_t rows,
+                                      GroupAxis axis, std::size_t block_size = 64, cudaStream_t stream = nullptr,
+                                      uint32_t head_dim = 128, StatusWord* status = nullptr) {
+    if (block_size == 0 || rows % block_size) throw ConfigError("compress: sequence length not divisible by block_size");
+    const uint32_t nb = static_cast<uint32_t>(rows / block_size);
+    DeviceCompressedCache out(dtype, axis, n_units, nb, dense_count, nb - dense_count, head_dim,
+                              static_cast<uint32_t>(block_size));
+    StatusWord own(stream);
+    StatusWord* st = status ? status : &own;
+    check(hs_compress_with_mask(src, rows * head_dim, rows, element_mask_dev, rows * head_dim, flags_dev,
+                                &out.desc(), st->get(), stream));
+    if (!status) own.check(stream);
     return out;
 }
 
 // decompress (compressed_cache.hpp:271-298) into dst [n_units][rows][d].
-inline void decompress(const DeviceCompressedCache& c, void* dst, cudaStream_t stream = nullptr) {
-    check(hs_decompress(&c.desc(), dst, stream));
+inline void decompress(const DeviceCompressedCache& c, void* dst, cudaStream_t stream = nullptr,
+                       StatusWord* status = nullptr) {
+    StatusWord own(stream);
+    StatusWord* st = status ? status : &own;
+    check(hs_decompress(&c.desc(), dst, st->get(), stream));
+    if (!status) own.check(stream);
 }
 
 // Decode-phase re-prune (pipeline.hpp:227-240: decompress -> prune_cache at the
-// decode sparsity -> compress) in one pass over c's pools.
+// decode sparsity -> compress) in one pass over c's pools.  A corrupt input
+// throws decompress's DataError (status == nullptr) or is left in *status.
 inline DeviceCompressedCache recompress(const DeviceCompressedCache& c, const SparsityConfig& cfg, double sparsity,
-                                        cudaStream_t stream = nullptr) {
+                                        cudaStream_t stream = nullptr, StatusWord* status = nullptr) {
     const hs_device_cache& in = c.desc();
     const PoolCounts p = pool_counts(static_cast<std::size_t>(in.logical_blocks) * in.block_size, cfg, sparsity);
     DeviceCompressedCache out(static_cast<DType>(in.dtype), static_cast<GroupAxis>(in.axis), in.n_units,
                               p.logical_blocks, p.dense_count, p.sparse_count, in.head_dim,
                               static_cast<uint32_t>(cfg.block_size));
     const hs_sparsity_config cc = cfg.c();
-    check(hs_recompress(&in, &cc, sparsity, &out.desc(), out.losses(), out.flags(), stream));
+    StatusWord own(stream);
+    StatusWord* st = status ? status : &own;
+    check(hs_recompress(&in, &cc, sparsity, &out.desc(), out.losses(), out.flags(), st->get(), stream));
+    if (!status) own.check(stream);
     return out;
 }
 
@@ -265,7 +318,7 @@ inline DeviceCompressedCache recompress(const DeviceCompressedCache& c, const Sp
 // stride tail_unit_stride elements; 0 = tail_rows * d) in one pass.
 inline DeviceCompressedCache absorb_tail(const DeviceCompressedCache& c, const void* tail, std::size_t tail_rows,
                                          const SparsityConfig& cfg, double sparsity, cudaStream_t stream = nullptr,
-                                         std::size_t tail_unit_stride = 0) {
+                                         std::size_t tail_unit_stride = 0, StatusWord* status = nullptr) {
     const hs_device_cache& in = c.desc();
     const std::size_t rows = static_cast<std::size_t>(in.logical_blocks) * in.block_size + tail_rows;
     const PoolCounts p = pool_counts(rows, cfg, sparsity);
@@ -273,8 +326,11 @@ inline DeviceCompressedCache absorb_tail(const DeviceCompressedCache& c, const v
                               p.logical_blocks, p.dense_count, p.sparse_count, in.head_dim,
                               static_cast<uint32_t>(cfg.block_size));
     const hs_sparsity_config cc = cfg.c();
+    StatusWord own(stream);
+    StatusWord* st = status ? status : &own;
     check(hs_absorb_tail(&in, tail, tail_unit_stride ? tail_unit_stride : tail_rows * in.head_dim, tail_rows, &cc,
-                         sparsity, &out.desc(), out.losses(), out.flags(), stream));
+                         sparsity, &out.desc(), out.losses(), out.flags(), st->get(), stream));
+    if (!status) own.check(stream);
     return out;
 }
 

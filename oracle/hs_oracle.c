@@ -246,7 +246,7 @@ static inline void group_elem(int axis, size_t B, size_t b, size_t sr, size_t g,
  * layout (value cache transposed), sparse blocks keep each group's top-2 and
  * pack 2-bit codes (nm_metadata.hpp:63-88). */
 static int assemble(const float* x, size_t rows, size_t cols, size_t B, int axis,
-                    const uint8_t* flags, hso_cache* c) {
+                    const uint8_t* flags, const uint8_t* emask, hso_cache* c) {
     CHECK_CONFIG(B > 0 && B % 4 == 0,
                  "SparsityConfig: block_size must be a positive multiple of m_group");
     CHECK_CONFIG(rows % B == 0, "compress: sequence length not divisible by block_size");
@@ -289,7 +289,22 @@ static int assemble(const float* x, size_t rows, size_t cols, size_t B, int axis
                         grp[i] = x[lr * cols + lc];
                     }
                     int kept[2];
-                    top2_of_4(grp, kept);
+                    if (emask) {
+                        /* compress (compressed_cache.hpp:208-223): the mask's kept
+                         * elements in ascending position; exactly n_keep = 2 */
+                        int n = 0;
+                        for (size_t i = 0; i < 4; ++i) {
+                            size_t lr, lc;
+                            group_elem(axis, B, b, sr, g, i, &lr, &lc);
+                            if (emask[lr * cols + lc]) {
+                                if (n >= 2) return fail(HSO_DATA, "compress: group keeps more than n_keep elements");
+                                kept[n++] = (int)i;
+                            }
+                        }
+                        if (n != 2) return fail(HSO_DATA, "compress: group keeps fewer than n_keep elements");
+                    } else {
+                        top2_of_4(grp, kept);
+                    }
                     for (int i = 0; i < 2; ++i) {
                         nnz[v++] = grp[kept[i]];
                         meta[code / 8] |= (uint16_t)(kept[i] << (2 * (code % 8)));
@@ -364,14 +379,21 @@ int hso_prune_compress(const float* x, size_t rows, size_t cols, const hso_confi
         for (size_t b = 0; b < nblocks; ++b)
             if (flags[b]) memset(element_mask + b * B * cols, 1, B * cols);
     }
-    return assemble(x, rows, cols, B, axis, flags, out);
+    return assemble(x, rows, cols, B, axis, flags, NULL, out);
 }
 
 /* fused_magnitude_compress (compressed_cache.hpp:262-267) under a given
  * block mask. */
 int hso_compress_with_flags(const float* x, size_t rows, size_t cols, const hso_config* cfg,
                             int axis, const uint8_t* flags, hso_cache* out) {
-    return assemble(x, rows, cols, cfg->block_size, axis, flags, out);
+    return assemble(x, rows, cols, cfg->block_size, axis, flags, NULL, out);
+}
+
+/* compress (compressed_cache.hpp:196-225) under an explicit element mask
+ * (u8 [rows][cols], nonzero = kept) and block mask. */
+int hso_compress_with_mask(const float* x, size_t rows, size_t cols, const hso_config* cfg,
+                           int axis, const uint8_t* element_mask, const uint8_t* flags, hso_cache* out) {
+    return assemble(x, rows, cols, cfg->block_size, axis, flags, element_mask, out);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -65,6 +65,10 @@ typedef struct {
     int prefix##compress_with_flags(const float* x, size_t rows, size_t cols,                \
                                     const hso_config* cfg, int axis, const uint8_t* flags,   \
                                     hso_cache* out);                                         \
+    int prefix##compress_with_mask(const float* x, size_t rows, size_t cols,                 \
+                                   const hso_config* cfg, int axis,                          \
+                                   const uint8_t* element_mask, const uint8_t* flags,        \
+                                   hso_cache* out);                                          \
     int prefix##decompress(const hso_cache* c, float* out);                                  \
     int prefix##attend_rows(const float* q, size_t rows, size_t d, const hso_cache* k,       \
                             const hso_cache* v, const float* k_tail, const float* v_tail,    \

@@ -152,6 +152,8 @@ class Oracle:
                                         C.c_double, C.c_int, C.POINTER(_Cache), vp, vp, vp]
         f("compress_with_flags").argtypes = [vp, C.c_size_t, C.c_size_t, C.POINTER(_Config),
                                              C.c_int, vp, C.POINTER(_Cache)]
+        f("compress_with_mask").argtypes = [vp, C.c_size_t, C.c_size_t, C.POINTER(_Config),
+                                            C.c_int, vp, vp, C.POINTER(_Cache)]
         f("decompress").argtypes = [C.POINTER(_Cache), vp]
         f("attend_rows").argtypes = [vp, C.c_size_t, C.c_size_t, C.POINTER(_Cache),
                                      C.POINTER(_Cache), vp, vp, C.c_size_t, C.c_size_t,
@@ -267,6 +269,20 @@ class Oracle:
         cc = cfg._c()
         rc = self._fn("compress_with_flags")(x.ctypes.data, rows, cols, C.byref(cc), axis,
                                              flags.ctypes.data, C.byref(cs))
+        self._check(rc)
+        return self._finish(c, cs)
+
+    def compress_with_mask(self, x, cfg: SparsityConfig, axis: int, element_mask, flags) -> CompressedCache:
+        """compress (compressed_cache.hpp:196-225) under an explicit element + block mask."""
+        x = np.ascontiguousarray(x, np.float32)
+        rows, cols = x.shape
+        em = np.ascontiguousarray(element_mask, np.uint8).reshape(rows, cols)
+        flags = np.ascontiguousarray(flags, np.uint8)
+        c = self._empty_cache(rows, cols, cfg.block_size if cfg.block_size else 1, axis)
+        cs = c._c()
+        cc = cfg._c()
+        rc = self._fn("compress_with_mask")(x.ctypes.data, rows, cols, C.byref(cc), axis, em.ctypes.data,
+                                            flags.ctypes.data, C.byref(cs))
         self._check(rc)
         return self._finish(c, cs)
 

@@ -150,6 +150,23 @@ int ref_compress_with_flags(const float* x, size_t rows, size_t cols, const hso_
     });
 }
 
+// compress (compressed_cache.hpp:196-225) under an explicit HierarchicalMask.
+int ref_compress_with_mask(const float* x, size_t rows, size_t cols, const hso_config* cfg, int axis,
+                           const uint8_t* element_mask, const uint8_t* flags, hso_cache* out) {
+    return guarded([&] {
+        const Tensor2D t = to_tensor(x, rows, cols);
+        HierarchicalMask hm;
+        const std::size_t nb = cfg->block_size ? rows / cfg->block_size : 0;
+        hm.block.flags.assign(flags, flags + nb);
+        hm.block.losses.assign(nb, 0.0);
+        hm.element = ElementMask(rows, cols, 0);
+        for (std::size_t r = 0; r < rows; ++r)
+            for (std::size_t c = 0; c < cols; ++c) hm.element.set(r, c, element_mask[r * cols + c] != 0);
+        const CompressedCache cc = compress(t, hm, to_cfg(cfg), axis == 0 ? GroupAxis::kChannel : GroupAxis::kSequence);
+        from_cache(cc, out);
+    });
+}
+
 int ref_decompress(const hso_cache* c, float* out) {
     return guarded([&] {
         const Tensor2D t = decompress(to_cache(c));

@@ -33,9 +33,10 @@ class DeviceCacheC(C.Structure):
 
 
 # Exported symbols (every one declared in include/hierasparse_b200.h).
-EXPORTS = ("hs_last_error", "hs_version", "hs_pool_counts", "hs_cache_bytes", "hs_prune_compress",
-           "hs_compress_with_flags", "hs_decompress", "hs_recompress", "hs_absorb_tail", "hs_decode", "hs_decode_partial",
-           "hs_decode_combine", "hs_prefill", "hs_kernel_launches")
+EXPORTS = ("hs_last_error", "hs_version", "hs_status_word_decode", "hs_pool_counts", "hs_cache_bytes",
+           "hs_prune_compress", "hs_compress_with_flags", "hs_compress_with_mask", "hs_decompress", "hs_recompress",
+           "hs_absorb_tail", "hs_decode", "hs_decode_partial", "hs_decode_combine", "hs_prefill",
+           "hs_kernel_launches")
 
 _lib = None
 
@@ -57,11 +58,13 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hs_pool_counts": [u64, P(SparsityConfigC), C.c_double, P(u32), P(u32), P(u32), P(u32), P(u32)],
         "hs_cache_bytes": [P(DeviceCacheC), P(u64), P(u64), P(u64), P(u64), P(u64)],
         "hs_prune_compress": [vp, u64, u64, P(SparsityConfigC), C.c_double, P(DeviceCacheC), vp, vp, vp],
-        "hs_compress_with_flags": [vp, u64, u64, vp, P(DeviceCacheC), vp],
-        "hs_decompress": [P(DeviceCacheC), vp, vp],
-        "hs_recompress": [P(DeviceCacheC), P(SparsityConfigC), C.c_double, P(DeviceCacheC), vp, vp, vp],
+        "hs_status_word_decode": [u64],
+        "hs_compress_with_flags": [vp, u64, u64, vp, P(DeviceCacheC), vp, vp],
+        "hs_compress_with_mask": [vp, u64, u64, vp, u64, vp, P(DeviceCacheC), vp, vp],
+        "hs_decompress": [P(DeviceCacheC), vp, vp, vp],
+        "hs_recompress": [P(DeviceCacheC), P(SparsityConfigC), C.c_double, P(DeviceCacheC), vp, vp, vp, vp],
         "hs_absorb_tail": [P(DeviceCacheC), vp, u64, u64, P(SparsityConfigC), C.c_double, P(DeviceCacheC), vp, vp,
-                           vp],
+                           vp, vp],
         "hs_decode": [vp, P(DeviceCacheC), P(DeviceCacheC), vp, vp, u32, u32, C.c_float, u32, vp, vp],
         "hs_decode_partial": [vp, P(DeviceCacheC), P(DeviceCacheC), vp, vp, u32, u32, C.c_float, u32, u32,
                               i32, vp, vp],
@@ -88,6 +91,12 @@ def check(rc: int) -> None:
     if rc == HS_ERR_IO:
         raise IoError(msg)
     raise CudaError(msg)
+
+
+def check_status_word(word: int) -> None:
+    """Raise the reference exception recorded in a device status word (0 = OK)."""
+    if word:
+        check(load().hs_status_word_decode(word & 0xFFFFFFFFFFFFFFFF))
 
 
 def kernel_launches() -> int:

@@ -330,7 +330,7 @@ HS_API hs_status hs_cache_bytes(const hs_device_cache* c, uint64_t* index_bytes,
 static hs_status prune_compress_common(const void* src, uint64_t src_unit_stride, uint64_t rows,
                                        const hs_sparsity_config* cfg, double sparsity,
                                        hs_device_cache* out, double* losses, uint8_t* flags,
-                                       void* stream, const hs_device_cache* in) {
+                                       uint64_t* status, void* stream, const hs_device_cache* in) {
     HS_CHECK_CONFIG(out != nullptr && (src != nullptr || in != nullptr), "prune_cache: null argument");
     uint32_t nb, dc, sc, pre, suf, quota;
     hs_status st = pool_counts(rows, cfg, sparsity, &nb, &dc, &sc, &pre, &suf, &quota);
@@ -385,22 +385,12 @@ static hs_status prune_compress_common(const void* src, uint64_t src_unit_stride
         L.in_dense = in->dense_pool;
         L.in_nnz = in->nnz_pool;
         L.in_meta = in->meta_pool;
-        L.bad = static_cast<int*>(workspace(s, 64, kWsMisc, &st));
-        if (st) return st;
-        cudaMemsetAsync(L.bad, 0, sizeof(int), s);
+        // decompress's DataErrors on a corrupt input cache go to the status word
+        L.status = reinterpret_cast<unsigned long long*>(status);
     }
     cudaError_t e = hs::launch_prune_compress(L, s);
     count_launch(static_sel ? 2 : 4);
     if (e != cudaSuccess) return cuda_fail(e, "prune_compress launch");
-    if (in) {
-        // decompress's DataError semantics for a corrupt input cache
-        int hbad = 0;
-        e = cudaMemcpyAsync(&hbad, L.bad, sizeof(int), cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) return cuda_fail(e, "recompress");
-        if (hbad == 1) return fail(HS_ERR_DATA, "decompress: index map holds a zero or dangling entry");
-        if (hbad == 2) return fail(HS_ERR_DATA, "unpack_metadata: corrupt metadata, codes not increasing");
-    }
     return HS_OK;
 }
 
@@ -409,13 +399,14 @@ HS_API hs_status hs_prune_compress(const void* src, uint64_t src_unit_stride, ui
                                    hs_device_cache* out, double* losses, uint8_t* flags,
                                    void* stream) {
     HS_CHECK_CONFIG(src != nullptr, "prune_cache: null argument");
-    return prune_compress_common(src, src_unit_stride, rows, cfg, sparsity, out, losses, flags, stream, nullptr);
+    return prune_compress_common(src, src_unit_stride, rows, cfg, sparsity, out, losses, flags, nullptr, stream,
+                                 nullptr);
 }
 
 static hs_status recompress_common(const hs_device_cache* in, const void* tail, uint64_t tail_unit_stride,
                                    uint64_t tail_rows, const hs_sparsity_config* cfg, double sparsity,
-                                   hs_device_cache* out, double* losses, uint8_t* flags, void* stream,
-                                   const char* what) {
+                                   hs_device_cache* out, double* losses, uint8_t* flags, uint64_t* status,
+                                   void* stream, const char* what) {
     HS_CHECK_CONFIG(in != nullptr && out != nullptr, "%s: null argument", what);
     hs_status st = check_device_cache(in, what);
     if (st) return st;
@@ -430,42 +421,40 @@ static hs_status recompress_common(const hs_device_cache* in, const void* tail, 
                     "%s: tail unit stride too small", what);
     return prune_compress_common(tail, tail_unit_stride,
                                  static_cast<uint64_t>(in->logical_blocks) * in->block_size + tail_rows, cfg,
-                                 sparsity, out, losses, flags, stream, in);
+                                 sparsity, out, losses, flags, status, stream, in);
 }
 
 HS_API hs_status hs_recompress(const hs_device_cache* in, const hs_sparsity_config* cfg, double sparsity,
-                               hs_device_cache* out, double* losses, uint8_t* flags, void* stream) {
-    return recompress_common(in, nullptr, 0, 0, cfg, sparsity, out, losses, flags, stream, "recompress");
+                               hs_device_cache* out, double* losses, uint8_t* flags, uint64_t* status,
+                               void* stream) {
+    return recompress_common(in, nullptr, 0, 0, cfg, sparsity, out, losses, flags, status, stream, "recompress");
 }
 
 HS_API hs_status hs_absorb_tail(const hs_device_cache* in, const void* tail, uint64_t tail_unit_stride,
                                 uint64_t tail_rows, const hs_sparsity_config* cfg, double sparsity,
-                                hs_device_cache* out, double* losses, uint8_t* flags, void* stream) {
-    return recompress_common(in, tail, tail_unit_stride, tail_rows, cfg, sparsity, out, losses, flags, stream,
-                             "absorb_tail");
+                                hs_device_cache* out, double* losses, uint8_t* flags, uint64_t* status,
+                                void* stream) {
+    return recompress_common(in, tail, tail_unit_stride, tail_rows, cfg, sparsity, out, losses, flags, status,
+                             stream, "absorb_tail");
 }
 
-HS_API hs_status hs_compress_with_flags(const void* src, uint64_t src_unit_stride, uint64_t rows,
-                                        const uint8_t* flags, hs_device_cache* out, void* stream) {
-    HS_CHECK_CONFIG(out != nullptr && src != nullptr && flags != nullptr, "compress: null argument");
-    HS_CHECK_CONFIG(out->block_size == hs::kBlock, "compress: device kernels need block_size 64");
+static hs_status compress_flags_common(const void* src, uint64_t src_unit_stride, uint64_t rows,
+                                       const uint8_t* flags, const uint8_t* element_mask,
+                                       uint64_t mask_unit_stride, hs_device_cache* out, uint64_t* status,
+                                       void* stream, const char* what) {
+    HS_CHECK_CONFIG(out != nullptr && src != nullptr && flags != nullptr, "%s: null argument", what);
+    HS_CHECK_CONFIG(out->block_size == hs::kBlock, "%s: device kernels need block_size 64", what);
     HS_CHECK_CONFIG(rows % out->block_size == 0, "compress: sequence length not divisible by block_size");
     const uint32_t nb = static_cast<uint32_t>(rows / out->block_size);
     HS_CHECK_CONFIG(out->logical_blocks == nb, "compress: block mask does not cover the sequence");
-    hs_status st = check_device_cache(out, "compress");
+    hs_status st = check_device_cache(out, what);
     if (st) return st;
+    HS_CHECK_CONFIG(out->n_units == 1 || src_unit_stride >= rows * out->head_dim, "%s: unit stride too small", what);
+    HS_CHECK_CONFIG(element_mask == nullptr || out->n_units == 1 || mask_unit_stride >= rows * out->head_dim,
+                    "%s: element mask unit stride too small", what);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    // Validate the pool counts against the mask (host read; off the hot path).
-    std::vector<uint8_t> hf(static_cast<size_t>(out->n_units) * nb);
-    cudaError_t e = cudaMemcpyAsync(hf.data(), flags, hf.size(), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return cuda_fail(e, "compress: reading the block mask");
-    for (uint32_t u = 0; u < out->n_units; ++u) {
-        uint32_t d = 0;
-        for (uint32_t b = 0; b < nb; ++b) d += hf[static_cast<size_t>(u) * nb + b] != 0;
-        HS_CHECK_CONFIG(d == out->dense_count, "compress: unit %u has %u dense blocks, cache holds %u", u, d,
-                        out->dense_count);
-    }
+    // The BlockMask's dense count per unit must equal out->dense_count: checked on
+    // the device (status word, ConfigError) with no host round trip.
     hs::CompressLaunch L{};
     L.bf16 = out->dtype == HS_DTYPE_BF16;
     L.axis = out->axis;
@@ -476,40 +465,67 @@ HS_API hs_status hs_compress_with_flags(const void* src, uint64_t src_unit_strid
     L.src = src;
     L.src_unit_stride = src_unit_stride;
     L.flags_in = flags;
+    L.element_mask = element_mask;
+    L.mask_unit_stride = mask_unit_stride ? mask_unit_stride : rows * out->head_dim;
+    L.status = reinterpret_cast<unsigned long long*>(status);
     L.index_map = out->index_map;
     L.slot_block = out->slot_block;
     L.dense_pool = out->dense_pool;
     L.nnz_pool = out->nnz_pool;
     L.meta_pool = out->meta_pool;
     if (nb == 0) return HS_OK;
-    e = hs::launch_prune_compress(L, s);
+    cudaError_t e = hs::launch_prune_compress(L, s);
     count_launch(2);
     if (e != cudaSuccess) return cuda_fail(e, "compress launch");
     return HS_OK;
 }
 
-HS_API hs_status hs_decompress(const hs_device_cache* c, void* dst, void* stream) {
+HS_API hs_status hs_compress_with_flags(const void* src, uint64_t src_unit_stride, uint64_t rows,
+                                        const uint8_t* flags, hs_device_cache* out, uint64_t* status,
+                                        void* stream) {
+    return compress_flags_common(src, src_unit_stride, rows, flags, nullptr, 0, out, status, stream,
+                                 "fused_magnitude_compress");
+}
+
+HS_API hs_status hs_compress_with_mask(const void* src, uint64_t src_unit_stride, uint64_t rows,
+                                       const uint8_t* element_mask, uint64_t mask_unit_stride,
+                                       const uint8_t* flags, hs_device_cache* out, uint64_t* status,
+                                       void* stream) {
+    HS_CHECK_CONFIG(element_mask != nullptr, "compress: null element mask");
+    return compress_flags_common(src, src_unit_stride, rows, flags, element_mask, mask_unit_stride, out, status,
+                                 stream, "compress");
+}
+
+HS_API hs_status hs_decompress(const hs_device_cache* c, void* dst, uint64_t* status, void* stream) {
     hs_status st = check_device_cache(c, "decompress");
     if (st) return st;
     HS_CHECK_CONFIG(dst != nullptr, "decompress: null destination");
     if (c->logical_blocks == 0) return HS_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    int* bad = static_cast<int*>(workspace(s, 64, kWsMisc, &st));
-    if (st) return st;
-    cudaMemsetAsync(bad, 0, sizeof(int), s);
     hs::DecompressLaunch L{c->axis, static_cast<int>(c->n_units), static_cast<int>(c->logical_blocks),
                            static_cast<int>(c->dense_count), static_cast<int>(c->sparse_count),
-                           c->index_map, c->dense_pool, c->nnz_pool, c->meta_pool, dst, bad};
+                           c->index_map, c->dense_pool, c->nnz_pool, c->meta_pool, dst,
+                           reinterpret_cast<unsigned long long*>(status)};
     cudaError_t e = hs::launch_decompress(L, s);
     count_launch();
     if (e != cudaSuccess) return cuda_fail(e, "decompress launch");
-    int hbad = 0;
-    e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return cuda_fail(e, "decompress");
-    if (hbad == 1) return fail(HS_ERR_DATA, "decompress: index map holds a zero or dangling entry");
-    if (hbad == 2) return fail(HS_ERR_DATA, "unpack_metadata: corrupt metadata, codes not increasing");
     return HS_OK;
+}
+
+HS_API hs_status hs_status_word_decode(uint64_t word) {
+    if (word == 0) return HS_OK;
+    switch (static_cast<uint32_t>(word & 0xFFu)) {
+        case hs::kReasonZeroEntry: return fail(HS_ERR_DATA, "decompress: index map holds a zero entry");
+        case hs::kReasonDanglingDense: return fail(HS_ERR_DATA, "decompress: dangling dense offset");
+        case hs::kReasonDanglingSparse: return fail(HS_ERR_DATA, "decompress: dangling sparse offset");
+        case hs::kReasonCodesOrder:
+            return fail(HS_ERR_DATA, "unpack_metadata: corrupt metadata, codes not increasing");
+        case hs::kReasonKeepsMore: return fail(HS_ERR_DATA, "compress: group keeps more than n_keep elements");
+        case hs::kReasonKeepsFewer: return fail(HS_ERR_DATA, "compress: group keeps fewer than n_keep elements");
+        case hs::kReasonMaskCount:
+            return fail(HS_ERR_CONFIG, "compress: block mask dense count differs from the cache's dense pool");
+        default: return fail(HS_ERR_DATA, "device status word 0x%llx", static_cast<unsigned long long>(word));
+    }
 }
 
 constexpr int kDynamicMaxBlocks = 256;  // blocks per split up to which decode claims blocks dynamically

@@ -44,6 +44,15 @@ template <> struct F16Traits<__half> {
     }
 };
 
+// ------------------------------------------------------- status words ---
+// Asynchronous error reporting (include/hierasparse_b200.h, "status words"):
+// a kernel that finds invalid data records (reason, position key) into a
+// caller-owned uint64 with one atomicMax, so the first error in the
+// reference's iteration order wins and no host synchronisation is needed.
+__device__ __forceinline__ void record_status(unsigned long long* st, uint64_t key, uint32_t reason) {
+    if (st != nullptr) atomicMax(st, static_cast<unsigned long long>(((kStatusKeyMax - key) << 8) | reason));
+}
+
 // |x| of a 16-bit float as an integer key: for finite values magnitude order is
 // integer order of the low 15 bits (+0 and -0 compare equal).
 __device__ __forceinline__ uint32_t mag16(uint16_t b) { return b & 0x7FFFu; }

@@ -197,7 +197,9 @@ struct PackArgs {
     const uint16_t* in_dense;
     const uint16_t* in_nnz;
     const uint16_t* in_meta;
-    int* bad;                 // 1: zero / dangling index entry, 2: codes not increasing
+    unsigned long long* status; // SRC 1: decompress's DataErrors (status word, kernels.h reasons)
+    const uint8_t* element_mask;  // mask_pack_kernel: explicit ElementMask u8 [u][rows][d]
+    uint64_t mask_unit_stride;
 };
 
 // One stored 2:4 group (kept pair word, 4-bit code) back to its four logical
@@ -253,7 +255,9 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
         in_e = a.in_index[static_cast<int64_t>(u) * a.in_nb + b];
         const int slot = (in_e > 0 ? in_e : -in_e) - 1;
         if (in_e == 0 || (in_e > 0 && slot >= a.in_dense_count) || (in_e < 0 && slot >= a.in_sparse_count)) {
-            if (t == 0) atomicExch(a.bad, 1);
+            if (t == 0)
+                record_status(a.status, static_cast<uint64_t>(u) * a.nb + b,
+                              in_e == 0 ? kReasonZeroEntry : in_e > 0 ? kReasonDanglingDense : kReasonDanglingSparse);
             in_e = 0;  // read as zeros
         } else if (in_e > 0) {
             in_den = a.in_dense + (static_cast<uint64_t>(u) * a.in_dense_count + slot) * (kBlock * kHeadDim);
@@ -270,6 +274,9 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
         const int e = a.index_map[static_cast<int64_t>(u) * a.nb + b];
         dense = e > 0;
         slot = (e > 0 ? e : -e) - 1;
+        // a block mask whose dense count differs from the pool capacity was
+        // reported by assign_slots_kernel; never write past a pool
+        if (e == 0 || slot >= (dense ? a.dense_count : a.sparse_count)) return;
     }
     constexpr bool kLoss = MODE != 1;
     LossAcc acc;
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
         }
     }
 
-    if (SRC == 1 && in_bad) atomicExch(a.bad, 2);
+    if (SRC == 1 && in_bad) record_status(a.status, static_cast<uint64_t>(u) * a.nb + b, kReasonCodesOrder);
     if (kLoss) {
         const bool exact = loss_reduce<T>(acc, s_sum, s_min, nullptr);
         if (t == 0) {
@@ -415,8 +422,113 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
     }
 }
 
+// compress (compressed_cache.hpp:196-225): pack under an explicit ElementMask
+// (u8 [u][rows][d] logical, nonzero = kept).  Dense-flagged blocks are copied
+// verbatim (the mask is not consulted); every group of a sparse block must keep
+// exactly n_keep = 2 elements, else the first offending group in the
+// reference's order (block, stored row, group) is recorded as "keeps more" /
+// "keeps fewer" (:216-223).  Same thread layout as block_kernel.
+template <int AXIS>
+__global__ void __launch_bounds__(kThreads) mask_pack_kernel(PackArgs a) {
+    const int b = blockIdx.x, u = blockIdx.y, t = threadIdx.x;
+    const int e = a.index_map[static_cast<int64_t>(u) * a.nb + b];
+    const bool dense = e > 0;
+    const int slot = (e > 0 ? e : -e) - 1;
+    if (e == 0 || slot >= (dense ? a.dense_count : a.sparse_count)) return;
+    const uint16_t* blk = unit_src(a.src, a.src_stride, u) + static_cast<uint64_t>(b) * kBlock * kHeadDim;
+    const uint8_t* mblk = a.element_mask + static_cast<uint64_t>(u) * a.mask_unit_stride +
+                          static_cast<uint64_t>(b) * kBlock * kHeadDim;
+    constexpr int kGroupsPerBlock = kBlock * kHeadDim / 4;
+    const uint64_t key0 = (static_cast<uint64_t>(u) * a.nb + b) * kGroupsPerBlock;
+    // one 2:4 group from its four 16-bit values (lo = g0 | g1 << 16, hi = g2 | g3 << 16)
+    // and mask nibble: kept pair (ascending positions), code, validity
+    auto pack = [&](uint32_t lo, uint32_t hi, uint32_t m, uint64_t gkey, uint32_t& kept) -> uint32_t {
+        const int n = __popc(m);
+        if (n != 2) {
+            record_status(a.status, key0 + gkey, n > 2 ? kReasonKeepsMore : kReasonKeepsFewer);
+            kept = 0u;
+            return 0u;
+        }
+        const uint32_t p0 = __ffs(m) - 1, p1 = __ffs(m & (m - 1)) - 1;
+        kept = __byte_perm(lo, hi, 0x1010u + p0 * 0x22u + p1 * 0x2200u);
+        return p0 | (p1 << 2);
+    };
+    auto nib = [](uint32_t w) {  // 4 mask bytes -> nibble of their nonzero flags
+        uint32_t r = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r |= static_cast<uint32_t>(((w >> (8 * k)) & 0xFFu) != 0u) << k;
+        return r;
+    };
+    if (AXIS == 0) {
+        const int c = t & 15;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const int r = p * 16 + (t >> 4);
+            const uint4 v = *reinterpret_cast<const uint4*>(blk + r * kHeadDim + c * 8);
+            if (dense) {
+                uint16_t* dst = a.dense_pool + (static_cast<uint64_t>(u) * a.dense_count + slot) * (kBlock * kHeadDim);
+                *reinterpret_cast<uint4*>(dst + r * kHeadDim + c * 8) = v;
+                continue;
+            }
+            const uint2 mw = *reinterpret_cast<const uint2*>(mblk + r * kHeadDim + c * 8);
+            uint32_t k0, k1;
+            const uint32_t c0 = pack(v.x, v.y, nib(mw.x), r * (kHeadDim / 4) + 2 * c, k0);
+            const uint32_t c1 = pack(v.z, v.w, nib(mw.y), r * (kHeadDim / 4) + 2 * c + 1, k1);
+            const uint64_t sb = static_cast<uint64_t>(u) * a.sparse_count + slot;
+            uint16_t* nnz = a.nnz_pool + sb * (kBlock * kHeadDim / 2);
+            *reinterpret_cast<uint2*>(nnz + r * (kHeadDim / 2) + c * 4) = make_uint2(k0, k1);
+            uint8_t* meta = reinterpret_cast<uint8_t*>(a.meta_pool + sb * (kBlock * kHeadDim / 16));
+            meta[r * (kHeadDim / 8) + c] = static_cast<uint8_t>(c0 | (c1 << 4));
+        }
+    } else {
+        // stored transposed [d][B]: channel c, token groups 8h..8h+7
+        const int c = t & 127, h = t >> 7;
+        if (dense) {
+            uint16_t* dst = a.dense_pool + (static_cast<uint64_t>(u) * a.dense_count + slot) * (kBlock * kHeadDim) +
+                            c * kBlock + 32 * h;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t w[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = 32 * h + 8 * q + 2 * j;
+                    w[j] = blk[r * kHeadDim + c] | (static_cast<uint32_t>(blk[(r + 1) * kHeadDim + c]) << 16);
+                }
+                reinterpret_cast<uint4*>(dst)[q] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+            return;
+        }
+        uint32_t vals[8], meta = 0;
+#pragma unroll
+        for (int gi = 0; gi < 8; ++gi) {
+            const int r0 = 32 * h + 4 * gi;
+            const uint32_t lo = blk[r0 * kHeadDim + c] | (static_cast<uint32_t>(blk[(r0 + 1) * kHeadDim + c]) << 16);
+            const uint32_t hi = blk[(r0 + 2) * kHeadDim + c] | (static_cast<uint32_t>(blk[(r0 + 3) * kHeadDim + c]) << 16);
+            uint32_t m = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) m |= static_cast<uint32_t>(mblk[(r0 + k) * kHeadDim + c] != 0) << k;
+            meta |= pack(lo, hi, m, c * (kBlock / 4) + 8 * h + gi, vals[gi]) << (4 * gi);
+        }
+        const uint64_t sb = static_cast<uint64_t>(u) * a.sparse_count + slot;
+        uint16_t* nnz = a.nnz_pool + sb * (kBlock * kHeadDim / 2) + c * (kBlock / 2) + 16 * h;
+        reinterpret_cast<uint4*>(nnz)[0] = make_uint4(vals[0], vals[1], vals[2], vals[3]);
+        reinterpret_cast<uint4*>(nnz)[1] = make_uint4(vals[4], vals[5], vals[6], vals[7]);
+        uint16_t* mp = a.meta_pool + sb * (kBlock * kHeadDim / 16) + c * (kBlock / 16) + 2 * h;
+        *reinterpret_cast<uint32_t*>(mp) = meta;
+    }
+}
+
 // select_blocks (pruner.hpp:94-117) as a rank: block i (prunable) is sparse iff
-// #{j prunable: L_j < L_i or (L_j == L_i and j < i)} < quota.
+// #{j prunable: L_j < L_i or (L_j == L_i and j < i)} < quota.  The order is a
+// strict total order with NaN above +inf (ties to the lower index), so exactly
+// quota blocks are flagged whatever the losses hold (a NaN loss comes from 3+
+// NaNs in one 2:4 group); the reference's std::stable_sort with `<` has no
+// defined order for NaN (pruner.hpp:111-113) but also flags exactly quota.
+__device__ __forceinline__ bool loss_before(double lj, int j, double li, int i) {
+    const bool nj = isnan(lj), ni = isnan(li);
+    if (nj || ni) return (!nj && ni) || (nj && ni && j < i);
+    return lj < li || (lj == li && j < i);
+}
 __global__ void __launch_bounds__(256) rank_kernel(const double* losses, int nb, int prefix,
                                                    int suffix, int quota, uint8_t* flags) {
     const int u = blockIdx.y;
@@ -431,10 +543,7 @@ __global__ void __launch_bounds__(256) rank_kernel(const double* losses, int nb,
         for (int j = threadIdx.x; j < 1024 && j0 + j < hi; j += 256) tile[j] = L[j0 + j];
         __syncthreads();
         const int n = min(1024, hi - j0);
-        for (int j = 0; j < n; ++j) {
-            const double lj = tile[j];
-            rank += (lj < li) || (lj == li && j0 + j < i);
-        }
+        for (int j = 0; j < n; ++j) rank += loss_before(tile[j], j0 + j, li, i);
     }
     if (i < nb) {
         const bool prunable = i >= lo && i < hi;
@@ -446,10 +555,14 @@ __global__ void __launch_bounds__(256) rank_kernel(const double* losses, int nb,
 // index_map = +(dense rank + 1) or -(sparse rank + 1); slot_block inverts it.
 // flags_in == nullptr selects the static pattern (protected dense, prunable
 // sparse iff all_sparse).
+// A BlockMask whose dense count differs from the pool capacity (explicit masks
+// only) is a ConfigError recorded in the status word; slots past a pool are
+// then never written (block kernels skip them, slot_block stays in range).
 __global__ void __launch_bounds__(1024) assign_slots_kernel(const uint8_t* flags_in, int nb,
                                                             int prefix, int suffix, int all_sparse,
                                                             int dense_count, int16_t* index_map,
-                                                            int32_t* slot_block, uint8_t* flags_out) {
+                                                            int32_t* slot_block, uint8_t* flags_out,
+                                                            unsigned long long* status) {
     const int u = blockIdx.x, t = threadIdx.x;
     const int per = (nb + 1023) / 1024;
     const int b0 = min(nb, t * per), b1 = min(nb, b0 + per);
@@ -480,17 +593,18 @@ __global__ void __launch_bounds__(1024) assign_slots_kernel(const uint8_t* flags
     __syncthreads();
     int dense_before = x - nd + ((t >> 5) ? warp_sums[(t >> 5) - 1] : 0);
     int sparse_before = b0 - dense_before;
+    if (t == 0 && warp_sums[31] != dense_count) record_status(status, 0, kReasonMaskCount);
     int16_t* im = index_map + static_cast<int64_t>(u) * nb;
     int32_t* sb = slot_block ? slot_block + static_cast<int64_t>(u) * nb : nullptr;
     for (int b = b0; b < b1; ++b) {
         const int f = flag_of(b);
         if (f) {
             im[b] = static_cast<int16_t>(dense_before + 1);
-            if (sb) sb[dense_before] = b;
+            if (sb && dense_before < dense_count) sb[dense_before] = b;
             ++dense_before;
         } else {
             im[b] = static_cast<int16_t>(-(sparse_before + 1));
-            if (sb) sb[dense_count + sparse_before] = b;
+            if (sb && dense_count + sparse_before < nb) sb[dense_count + sparse_before] = b;
             ++sparse_before;
         }
         if (flags_out) flags_out[static_cast<int64_t>(u) * nb + b] = static_cast<uint8_t>(f);
@@ -504,15 +618,18 @@ __global__ void __launch_bounds__(kThreads) decompress_kernel(const int16_t* ind
                                                               const uint16_t* dense_pool,
                                                               const uint16_t* nnz_pool,
                                                               const uint16_t* meta_pool,
-                                                              uint16_t* dst, int* bad) {
+                                                              uint16_t* dst, unsigned long long* status) {
     const int b = blockIdx.x, u = blockIdx.y, t = threadIdx.x;
     const int e = index_map[static_cast<int64_t>(u) * nb + b];
     const int slot = (e > 0 ? e : -e) - 1;
     uint16_t* out = dst + (static_cast<uint64_t>(u) * nb + b) * kBlock * kHeadDim;
+    const uint64_t key = static_cast<uint64_t>(u) * nb + b;
     if (e == 0 || (e > 0 && slot >= dense_count) || (e < 0 && slot >= sparse_count)) {
-        if (t == 0) atomicExch(bad, 1);
+        if (t == 0)
+            record_status(status, key, e == 0 ? kReasonZeroEntry : e > 0 ? kReasonDanglingDense : kReasonDanglingSparse);
         return;
     }
+    bool bad = false;
     for (int i = t; i < kBlock * kHeadDim; i += kThreads) {
         // stored coordinates (sr, sc) of logical element i = (lr, lc)
         const int lr = i / kHeadDim, lc = i % kHeadDim;
@@ -528,11 +645,12 @@ __global__ void __launch_bounds__(kThreads) decompress_kernel(const int16_t* ind
             const int g = sc >> 2, pos = sc & 3;
             const uint32_t code = (meta[g >> 2] >> (4 * (g & 3))) & 0xF;
             const int p0 = code & 3, p1 = code >> 2;
-            if (p1 <= p0) atomicExch(bad, 2);  // unpack_metadata: codes not increasing
+            bad |= p1 <= p0;  // unpack_metadata: codes not increasing
             v = pos == p0 ? nnz[2 * g] : (pos == p1 ? nnz[2 * g + 1] : static_cast<uint16_t>(0));
         }
         out[i] = v;
     }
+    if (bad) record_status(status, key, kReasonCodesOrder);
 }
 
 }  // namespace
@@ -576,23 +694,31 @@ cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
     a.in_dense = static_cast<const uint16_t*>(L.in_dense);
     a.in_nnz = static_cast<const uint16_t*>(L.in_nnz);
     a.in_meta = L.in_meta;
-    a.bad = L.bad;
+    a.status = L.status;
     auto blocks = [&](int mode) {
         return L.bf16 ? launch_block_kernel<__nv_bfloat16>(L.axis, mode, a, L.n_units, s)
                       : launch_block_kernel<__half>(L.axis, mode, a, L.n_units, s);
     };
     cudaError_t err;
     if (L.flags_in) {
-        // fused_magnitude_compress under an explicit BlockMask.
+        // fused_magnitude_compress under an explicit BlockMask, or compress under
+        // an explicit ElementMask + BlockMask (compressed_cache.hpp:196-225).
         assign_slots_kernel<<<L.n_units, 1024, 0, s>>>(L.flags_in, L.nb, 0, 0, 0, L.dense_count,
-                                                       L.index_map, L.slot_block, L.flags_out);
+                                                       L.index_map, L.slot_block, L.flags_out, L.status);
         if ((err = cudaGetLastError())) return err;
+        if (L.element_mask) {
+            a.element_mask = L.element_mask;
+            a.mask_unit_stride = L.mask_unit_stride;
+            if (L.axis == 0) mask_pack_kernel<0><<<dim3(L.nb, L.n_units), kThreads, 0, s>>>(a);
+            else mask_pack_kernel<1><<<dim3(L.nb, L.n_units), kThreads, 0, s>>>(a);
+            return cudaGetLastError();
+        }
         return blocks(1);
     }
     if (L.static_selection) {
         assign_slots_kernel<<<L.n_units, 1024, 0, s>>>(nullptr, L.nb, L.prefix, L.suffix,
                                                        L.all_sparse, L.dense_count, L.index_map,
-                                                       L.slot_block, L.flags_out);
+                                                       L.slot_block, L.flags_out, nullptr);
         if ((err = cudaGetLastError())) return err;
         return blocks(L.losses ? 2 : 1);
     }
@@ -602,7 +728,7 @@ cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
                                                                      L.suffix, L.quota, L.flags_tmp);
     if ((err = cudaGetLastError())) return err;
     assign_slots_kernel<<<L.n_units, 1024, 0, s>>>(L.flags_tmp, L.nb, 0, 0, 0, L.dense_count,
-                                                   L.index_map, L.slot_block, L.flags_out);
+                                                   L.index_map, L.slot_block, L.flags_out, nullptr);
     if ((err = cudaGetLastError())) return err;
     return blocks(1);
 }
@@ -613,12 +739,12 @@ cudaError_t launch_decompress(const DecompressLaunch& L, cudaStream_t s) {
         decompress_kernel<0><<<grid, kThreads, 0, s>>>(L.index_map, L.nb, L.dense_count, L.sparse_count,
                                                        static_cast<const uint16_t*>(L.dense_pool),
                                                        static_cast<const uint16_t*>(L.nnz_pool),
-                                                       L.meta_pool, static_cast<uint16_t*>(L.dst), L.bad);
+                                                       L.meta_pool, static_cast<uint16_t*>(L.dst), L.status);
     else
         decompress_kernel<1><<<grid, kThreads, 0, s>>>(L.index_map, L.nb, L.dense_count, L.sparse_count,
                                                        static_cast<const uint16_t*>(L.dense_pool),
                                                        static_cast<const uint16_t*>(L.nnz_pool),
-                                                       L.meta_pool, static_cast<uint16_t*>(L.dst), L.bad);
+                                                       L.meta_pool, static_cast<uint16_t*>(L.dst), L.status);
     return cudaGetLastError();
 }
 

@@ -10,6 +10,19 @@ namespace hs {
 constexpr int kBlock = 64;    // B: tokens per block (masks.hpp:76 default)
 constexpr int kHeadDim = 128; // d: Llama-3.1-8B head dim
 
+// Status words (hs_status_word in hierasparse_b200.h): ((kStatusKeyMax - key) << 8) | reason,
+// key = position of the offending block / group in the reference's iteration order.
+constexpr uint64_t kStatusKeyMax = (uint64_t(1) << 48) - 1;
+enum StatusReason : uint32_t {
+    kReasonZeroEntry = 1,      // decompress: index map holds a zero entry
+    kReasonDanglingDense = 2,  // decompress: dangling dense offset
+    kReasonDanglingSparse = 3, // decompress: dangling sparse offset
+    kReasonCodesOrder = 4,     // unpack_metadata: corrupt metadata, codes not increasing
+    kReasonKeepsMore = 5,      // compress: group keeps more than n_keep elements
+    kReasonKeepsFewer = 6,     // compress: group keeps fewer than n_keep elements
+    kReasonMaskCount = 7,      // compress: block mask dense count differs from the dense pool (ConfigError)
+};
+
 struct CompressLaunch {
     bool bf16;
     int axis;
@@ -37,7 +50,9 @@ struct CompressLaunch {
     const void* in_dense;
     const void* in_nnz;
     const uint16_t* in_meta;
-    int* bad;
+    unsigned long long* status;  // decompress's DataErrors / BlockMask count (status word), may be null
+    const uint8_t* element_mask; // compress under an explicit ElementMask: u8 [u][rows][d] (mask_unit_stride)
+    uint64_t mask_unit_stride;
 };
 cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s);
 
@@ -48,7 +63,7 @@ struct DecompressLaunch {
     const void* nnz_pool;
     const uint16_t* meta_pool;
     void* dst;
-    int* bad;
+    unsigned long long* status;
 };
 cudaError_t launch_decompress(const DecompressLaunch& L, cudaStream_t s);
 

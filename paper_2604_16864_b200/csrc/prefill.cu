@@ -676,6 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 }
                 if constexpr (PP) {
                 umma_commit(&bar_vempty[s]);  // V stage free once the O^T MMAs are done
+#ifndef HS_PREFILL_XP_NO_LMMA
                 {   // row sums l[q] += sum_k P^T[q][k]: P^T as an MN-major A operand, ones as B (N = 16)
                     const uint32_t id_l = umma_idesc_f16(bf, 128, 16, true, false, false);
                     const uint64_t pa = dP + (pbuf_of(tp) * lay.p_bytes) / 16;
@@ -685,6 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                         for (int kk = 0; kk < 8; ++kk)
                             umma_f16(tmem + 416u, pa + pass * 2048 + 128 * kk, dOnes, id_l, tp > 0 || pass > 0 || kk > 0);
                 }
+#endif
                 umma_commit(&bar_pempty[pbuf_of(tp)]);  // P^T buffer free; O^T and l through tile tp final
                 } else {
                 umma_commit(&bar_pempty[pbuf_of(tp)]);  // P^T buffer free; O^T through tile tp final
@@ -885,6 +887,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
                                             F16Traits<T>::pack(p[4], p[5]), F16Traits<T>::pack(p[6], p[7]));
                 const uint32_t pto = pt_base_h + ((static_cast<uint32_t>(g8) ^ r7) << 4);
+#ifdef HS_PREFILL_XP_NO_PSTORE
+                if (hi.x == 0x7fff7fffu)  // experiment: keep the math, drop the P^T stores
+#endif
                 *reinterpret_cast<uint4*>(pbuf + pto) = hi;
                 if (HILO) {
                     float rr[8];

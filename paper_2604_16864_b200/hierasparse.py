@@ -127,6 +127,25 @@ class DeviceCompressedCache:
         return self.n_units * sum(self.measure_size().values())
 
 
+class StatusWord:
+    """A device status word (hierasparse_b200.h "status words"): the kernels that
+    validate data record the first DataError in the reference's order into it
+    without a host synchronisation.  check() synchronises and raises it."""
+
+    def __init__(self, device):
+        self.word = torch.zeros(1, dtype=torch.int64, device=device)
+
+    def ptr(self) -> int:
+        return self.word.data_ptr()
+
+    def check(self) -> None:
+        capi.check_status_word(int(self.word.item()))
+
+
+def _status(status: StatusWord | None, device) -> StatusWord:
+    return status if status is not None else StatusWord(device)
+
+
 def _check_src(x: torch.Tensor) -> torch.Tensor:
     if not x.is_cuda:
         raise ConfigError("source must be a CUDA tensor (use the host-buffer entry points for host data)")
@@ -171,50 +190,98 @@ def prune_cache(key: torch.Tensor, value: torch.Tensor, cfg: SparsityConfig):
 
 
 def fused_magnitude_compress(x: torch.Tensor, flags: torch.Tensor, cfg: SparsityConfig,
-                             axis: int) -> DeviceCompressedCache:
+                             axis: int, check: bool = True, status: StatusWord | None = None) -> DeviceCompressedCache:
     """fused_magnitude_compress (compressed_cache.hpp:262-267) under a given BlockMask
-    (flags u8 [units, blocks], 1 = dense)."""
+    (flags u8 [units, blocks], 1 = dense).  Every unit's dense count must equal
+    unit 0's (the pooled layout); a mismatch raises ConfigError (device-checked)."""
     x = _check_src(x)
     U, rows, d = x.shape
     if rows % cfg.block_size:
         raise ConfigError("compress: sequence length not divisible by block_size")
     flags = flags.to(device=x.device, dtype=torch.uint8).reshape(U, -1).contiguous()
     nb = rows // cfg.block_size
-    dc = int(flags[0].sum().item()) if nb else 0
+    if flags.shape[1] != nb:
+        raise ConfigError("compress: block mask does not cover the sequence")
+    dc = int((flags[0] != 0).sum().item()) if nb else 0
     out = DeviceCompressedCache(x.dtype, axis, U, nb, dc, nb - dc, x.device, d, cfg.block_size, cfg)
-    c = out.c()
+    st = _status(status, x.device)
     capi.check(capi.load().hs_compress_with_flags(x.data_ptr(), _unit_stride(x), rows, flags.data_ptr(),
-                                                  C.byref(c), _stream()))
-    out.flags.copy_(flags)
+                                                  out.cref(), st.ptr(), _stream()))
+    out.flags.copy_(flags != 0)
+    out.status = st
+    if check:
+        st.check()
     return out
 
 
-def decompress(c: DeviceCompressedCache) -> torch.Tensor:
-    """decompress (compressed_cache.hpp:271-298) -> [units, rows, d]."""
+def compress(x: torch.Tensor, element_mask: torch.Tensor, flags: torch.Tensor, cfg: SparsityConfig, axis: int,
+             check: bool = True, status: StatusWord | None = None) -> DeviceCompressedCache:
+    """compress (compressed_cache.hpp:196-225): pack under an explicit HierarchicalMask
+    -- element_mask (bool/u8 [units, rows, d], nonzero = kept) and BlockMask flags
+    (u8 [units, blocks], 1 = dense).  Dense blocks are copied verbatim; every 2:4
+    group of a sparse block must keep exactly 2 elements, else DataError
+    ("compress: group keeps more / fewer than n_keep elements")."""
+    x = _check_src(x)
+    U, rows, d = x.shape
+    em = element_mask.to(device=x.device, dtype=torch.uint8).reshape(U, rows, d).contiguous()
+    if em.shape != x.shape:
+        raise ConfigError("compress: element mask shape mismatch")
+    if rows % cfg.block_size:
+        raise ConfigError("compress: sequence length not divisible by block_size")
+    flags = flags.to(device=x.device, dtype=torch.uint8).reshape(U, -1).contiguous()
+    nb = rows // cfg.block_size
+    if flags.shape[1] != nb:
+        raise ConfigError("compress: block mask does not cover the sequence")
+    dc = int((flags[0] != 0).sum().item()) if nb else 0
+    out = DeviceCompressedCache(x.dtype, axis, U, nb, dc, nb - dc, x.device, d, cfg.block_size, cfg)
+    st = _status(status, x.device)
+    capi.check(capi.load().hs_compress_with_mask(x.data_ptr(), _unit_stride(x), rows, em.data_ptr(), rows * d,
+                                                 flags.data_ptr(), out.cref(), st.ptr(), _stream()))
+    out.flags.copy_(flags != 0)
+    out.status = st
+    if check:
+        st.check()
+    return out
+
+
+def decompress(c: DeviceCompressedCache, check: bool = True, status: StatusWord | None = None) -> torch.Tensor:
+    """decompress (compressed_cache.hpp:271-298) -> [units, rows, d].  Corrupt
+    index maps / metadata raise DataError (check=True: synchronises to read the
+    status word; check=False: the word is left on the result as .status)."""
     out = torch.empty((c.n_units, c.sequence_length, c.head_dim), dtype=c.dtype, device=c.index_map.device)
-    cs = c.c()
-    capi.check(capi.load().hs_decompress(C.byref(cs), out.data_ptr(), _stream()))
+    st = _status(status, out.device)
+    capi.check(capi.load().hs_decompress(c.cref(), out.data_ptr(), st.ptr(), _stream()))
+    if check:
+        st.check()
     return out
 
 
-def recompress(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: float) -> DeviceCompressedCache:
+def recompress(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: float, check: bool = True,
+               status: StatusWord | None = None) -> DeviceCompressedCache:
     """The decode-phase re-prune (pipeline.hpp:227-240): decompress
     (compressed_cache.hpp:271-298) -> hierarchical_mask_for at the decode sparsity
     (pruner.hpp:121-158) -> fused_magnitude_compress, for every unit on the
     device, in one pass over the input pools (hs_recompress: blocks are expanded
     on the fly, the dense cache is never materialised).  Bit-identical to the
-    reference's chain on the same pools."""
+    reference's chain on the same pools.  A corrupt input cache raises
+    decompress's DataError (check=False defers it to out.status.check(), so the
+    call stays free of host synchronisation, e.g. inside a CUDA graph)."""
     rows = c.logical_blocks * c.block_size
     nb, dc, sc, _, _ = pool_counts(rows, cfg, sparsity)
     out = DeviceCompressedCache(c.dtype, c.axis, c.n_units, nb, dc, sc, c.index_map.device, c.head_dim,
                                  cfg.block_size, cfg)
-    cin, cout, cc = c.c(), out.c(), cfg.c()
-    capi.check(capi.load().hs_recompress(C.byref(cin), C.byref(cc), sparsity, C.byref(cout),
-                                         out.losses.data_ptr(), out.flags.data_ptr(), _stream()))
+    cc = cfg.c()
+    st = _status(status, out.index_map.device)
+    capi.check(capi.load().hs_recompress(c.cref(), C.byref(cc), sparsity, out.cref(), out.losses.data_ptr(),
+                                         out.flags.data_ptr(), st.ptr(), _stream()))
+    out.status = st
+    if check:
+        st.check()
     return out
 
 
-def absorb_tail(c: DeviceCompressedCache, tail: torch.Tensor, cfg: SparsityConfig, sparsity: float):
+def absorb_tail(c: DeviceCompressedCache, tail: torch.Tensor, cfg: SparsityConfig, sparsity: float,
+                check: bool = True, status: StatusWord | None = None):
     """Dense-tail growth during decode: once the dense tail
     (CacheView::dense_tail, attention.hpp:19-31) holds whole blocks, re-prune the
     cache over its blocks followed by those tail blocks -- prune_cache + compress
@@ -234,10 +301,14 @@ def absorb_tail(c: DeviceCompressedCache, tail: torch.Tensor, cfg: SparsityConfi
     rows = c.logical_blocks * B + full
     nb, dc, sc, _, _ = pool_counts(rows, cfg, sparsity)
     out = DeviceCompressedCache(c.dtype, c.axis, U, nb, dc, sc, c.index_map.device, d, cfg.block_size, cfg)
-    cin, cout, cc = c.c(), out.c(), cfg.c()
-    capi.check(capi.load().hs_absorb_tail(C.byref(cin), src.data_ptr(), _unit_stride(src), full, C.byref(cc),
-                                          sparsity, C.byref(cout), out.losses.data_ptr(), out.flags.data_ptr(),
-                                          _stream()))
+    cc = cfg.c()
+    st = _status(status, out.index_map.device)
+    capi.check(capi.load().hs_absorb_tail(c.cref(), src.data_ptr(), _unit_stride(src), full, C.byref(cc),
+                                          sparsity, out.cref(), out.losses.data_ptr(), out.flags.data_ptr(),
+                                          st.ptr(), _stream()))
+    out.status = st
+    if check:
+        st.check()
     return out, tail[:, full:]
 
 

@@ -130,8 +130,114 @@ def test_decompress_rejects_corrupt_index_map(hs, port):
     x = gen_units(port, 1, 256, 128, seed=1, role=0, dtype="bf16")
     dev = hs.prune_compress(to_torch(x, "bf16"), hs.SparsityConfig(1, 1, 64), 1.0, 0)
     dev.index_map[0, 1] = 0
-    with pytest.raises(DataError):
+    with pytest.raises(DataError, match="index map holds a zero entry"):
         hs.decompress(dev)
+
+
+def test_decompress_errors_in_reference_order(hs, port):
+    """The first offending block in the reference's loop order decides the message
+    (compressed_cache.hpp:277-287), whatever order the device blocks ran in; the
+    messages are the oracle's.  The call itself never synchronises (check=False)."""
+    import torch
+    from oracle.oracle import SparsityConfig as OCfg
+    x = gen_units(port, 2, 1024, 128, seed=2, role=1, dtype="bf16")
+    dev = hs.prune_compress(to_torch(x, "bf16"), hs.SparsityConfig(0.5, 0.5, 64), 0.5, 1)
+    dense_slot = int(dev.index_map[0][dev.index_map[0] > 0][0])
+    sparse_b = int(torch.nonzero(dev.index_map[1] < 0)[0])
+    dense_b = int(torch.nonzero(dev.index_map[1] > 0)[-1])
+    dev.index_map[1, dense_b] = 100            # dangling dense offset (unit 1, late block)
+    dev.meta_pool[1, -int(dev.index_map[1, sparse_b]) - 1, 5] = 0x0003  # codes (3, 0) in unit 1
+    out = hs.decompress(dev, check=False)      # asynchronous: no raise, no sync
+    first = "dangling dense offset" if dense_b < sparse_b else "codes not increasing"
+    st = hs.StatusWord(out.device)
+    hs.decompress(dev, check=False, status=st)
+    with pytest.raises(hs.DataError, match=first):
+        st.check()
+    want_msg = None
+    try:
+        port.decompress(device_to_oracle(dev, 1))
+    except Exception as e:  # noqa: BLE001
+        want_msg = str(e)
+    assert want_msg is not None and first in want_msg
+    del dense_slot, out, OCfg
+
+
+def test_dangling_sparse_offset_message(hs, port):
+    x = gen_units(port, 1, 512, 128, seed=4, role=0, dtype="f16")
+    dev = hs.prune_compress(to_torch(x, "f16"), hs.SparsityConfig(1, 1, 64), 1.0, 0)
+    dev.index_map[0, 2] = -50
+    with pytest.raises(hs.DataError, match="dangling sparse offset"):
+        hs.decompress(dev)
+
+
+@pytest.mark.parametrize("axis", [0, 1])
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+def test_compress_with_element_mask_matches_oracle(hs, port, axis, dtype):
+    """compress (compressed_cache.hpp:196-225) under an explicit HierarchicalMask:
+    random valid 2-of-4 masks and a random block mask, bit-exact vs the oracle."""
+    import torch
+    from oracle.oracle import SparsityConfig as OCfg
+    rng = np.random.default_rng(40 + axis)
+    U, L, d = 2, 1024, 128
+    x = gen_units(port, U, L, d, seed=17, role=axis, dtype=dtype)
+    pairs = np.array([[1, 1, 0, 0], [1, 0, 1, 0], [1, 0, 0, 1], [0, 1, 1, 0], [0, 1, 0, 1], [0, 0, 1, 1]], np.uint8)
+    if axis == 0:
+        em = pairs[rng.integers(0, 6, (U, L, d // 4))].reshape(U, L, d)
+    else:
+        em = pairs[rng.integers(0, 6, (U, L // 4, d))].transpose(0, 1, 3, 2).reshape(U, L, d)
+    nb = L // 64
+    flags = np.zeros((U, nb), np.uint8)
+    for u in range(U):
+        flags[u, rng.choice(nb, 5, replace=False)] = 1
+    dev = hs.compress(to_torch(x, dtype), torch.from_numpy(em), torch.from_numpy(flags), hs.SparsityConfig(), axis)
+    for u in range(U):
+        want = port.compress_with_mask(x[u], OCfg(block_size=64), axis, em[u], flags[u])
+        got = device_to_oracle(dev, u)
+        for f in ("index_map", "dense_pool", "nnz_pool", "meta_pool"):
+            assert (getattr(got, f) == getattr(want, f)).all(), (u, f)
+
+
+@pytest.mark.parametrize("axis", [0, 1])
+def test_compress_with_element_mask_rejects_bad_groups(hs, port, axis):
+    """The first group (unit, block, stored row, group order) keeping != 2 elements
+    decides the DataError, as in the oracle; groups of dense blocks are ignored."""
+    import torch
+    from oracle.oracle import SparsityConfig as OCfg
+    U, L, d = 1, 256, 128
+    x = gen_units(port, U, L, d, seed=5, role=axis, dtype="bf16")
+    em = np.zeros((U, L, d), np.uint8)
+    if axis == 0:
+        em[..., 0::4] = 1
+        em[..., 1::4] = 1
+    else:
+        em[:, 0::4] = 1
+        em[:, 1::4] = 1
+    flags = np.array([[1, 0, 0, 0]], np.uint8)
+    em[0, 10, 0:4] = 1 if axis == 0 else em[0, 10, 0:4]  # dense block 0: ignored
+    if axis == 0:
+        em[0, 64 + 3, 8:12] = [1, 1, 1, 0]    # block 1, stored row 3, group 2: three kept
+        em[0, 128 + 1, 4:8] = [0, 1, 0, 0]    # block 2: one kept (later)
+        msg = "more than n_keep"
+    else:
+        em[0, 64 + 4:64 + 8, 7] = [0, 0, 0, 1]  # block 1, channel 7, token group 1: one kept
+        em[0, 128:132, 2] = [1, 1, 1, 1]        # block 2: four kept (later)
+        msg = "fewer than n_keep"
+    with pytest.raises(hs.DataError, match=msg):
+        hs.compress(to_torch(x, "bf16"), torch.from_numpy(em), torch.from_numpy(flags), hs.SparsityConfig(), axis)
+    with pytest.raises(Exception, match=msg):
+        port.compress_with_mask(x[0], OCfg(block_size=64), axis, em[0], flags[0])
+
+
+def test_block_mask_count_mismatch_is_config_error(hs, port):
+    """Pooled units share one dense count: a unit whose BlockMask differs raises
+    ConfigError from the device check, and no pool is written out of bounds."""
+    import torch
+    x = gen_units(port, 2, 512, 128, seed=6, role=0, dtype="bf16")
+    flags = np.zeros((2, 8), np.uint8)
+    flags[0, [1, 2]] = 1
+    flags[1, [1, 2, 3, 4]] = 1
+    with pytest.raises(hs.ConfigError, match="dense count"):
+        hs.fused_magnitude_compress(to_torch(x, "bf16"), torch.from_numpy(flags), hs.SparsityConfig(), 0)
 
 
 def test_golden_reference_vectors_on_gpu(hs):
@@ -261,7 +367,7 @@ def test_recompress_rejects_corrupt_input(hs, port):
     kc = hs.prune_compress(to_torch(kx, "bf16"), hs.SparsityConfig(1.0, 1.0, 64), 1.0, 0)
     bad = hs.recompress(kc, hs.SparsityConfig(1.0, 1.0, 64), 1.0)
     bad.index_map[0, 3] = 0
-    with pytest.raises(hs.DataError, match="zero or dangling"):
+    with pytest.raises(hs.DataError, match="zero entry"):
         hs.recompress(bad, hs.SparsityConfig(0.5, 0.5, 64), 0.5)
     bad2 = hs.recompress(kc, hs.SparsityConfig(1.0, 1.0, 64), 1.0)
     bad2.meta_pool[0, 0, 0] = 0x0003  # first group codes (3, 0): not increasing

@@ -299,3 +299,65 @@ def test_port_equals_reference_random_attention(port, ref):
             ref.decode(qd, kc, vc, kt, vt, sc, spl).tobytes()
         assert port.flop_and_byte_count(n_q, d, kc, vc, tail, causal) == \
             ref.flop_and_byte_count(n_q, d, kc, vc, tail, causal)
+
+
+# ------------------------------------------------- compress (explicit mask) ----
+def _masked_groups(rng, x, axis, block, cfg, port):
+    """A valid HierarchicalMask from the pruner, then the flags it came with."""
+    c = port.prune_compress(x, cfg, axis, cfg.s_key, element_mask=True)
+    return c.element_mask.copy(), c.flags.copy()
+
+
+@pytest.mark.parametrize("axis", [0, 1])
+def test_compress_with_mask_equals_fused(port, ref, axis):
+    """compress(cache, prune_cache mask) is field-identical to fused_magnitude_compress
+    (test_compressor.cpp:114-134), in the port and in the reference."""
+    rng = np.random.default_rng(3 + axis)
+    x = port.round_to(rng.standard_normal((256, 32)).astype(np.float32), "bf16")
+    cfg = SparsityConfig(0.5, 0.5, 16)
+    em, flags = _masked_groups(rng, x, axis, 16, cfg, port)
+    for o in (port, ref):
+        a = o.compress_with_mask(x, cfg, axis, em, flags)
+        b = o.compress_with_flags(x, cfg, axis, flags)
+        assert (a.index_map == b.index_map).all() and (a.nnz_pool == b.nnz_pool).all()
+        assert (a.meta_pool == b.meta_pool).all() and (a.dense_pool == b.dense_pool).all()
+
+
+@pytest.mark.parametrize("axis", [0, 1])
+def test_compress_with_mask_random_masks_port_equals_reference(port, ref, axis):
+    """Arbitrary valid 2-of-4 masks (not magnitude-chosen): the port packs them
+    exactly like the reference's compress."""
+    rng = np.random.default_rng(11 + axis)
+    rows, cols, B = 128, 16, 16
+    x = rng.standard_normal((rows, cols)).astype(np.float32)
+    em = np.zeros((rows, cols), np.uint8)
+    pairs = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
+    for r in range(rows if axis == 0 else rows // 4):
+        for g in range(cols // 4 if axis == 0 else cols):
+            p = pairs[rng.integers(0, 6)]
+            for i in p:
+                if axis == 0:
+                    em[r, 4 * g + i] = 1
+                else:
+                    em[4 * r + i, g] = 1
+    flags = (rng.random(rows // B) < 0.3).astype(np.uint8)
+    cfg = SparsityConfig(block_size=B)
+    a, b = port.compress_with_mask(x, cfg, axis, em, flags), ref.compress_with_mask(x, cfg, axis, em, flags)
+    for f in ("index_map", "dense_pool", "nnz_pool", "meta_pool"):
+        assert (getattr(a, f) == getattr(b, f)).all(), f
+
+
+@pytest.mark.parametrize("kept,msg", [(3, "more than n_keep"), (1, "fewer than n_keep"), (0, "fewer than n_keep")])
+def test_compress_with_mask_rejects_bad_groups(port, ref, kept, msg):
+    """compressed_cache.hpp:216-223: a sparse block's group keeping != 2 -> DataError."""
+    x = np.arange(64, dtype=np.float32).reshape(16, 4)
+    em = np.zeros((16, 4), np.uint8)
+    em[:, :2] = 1
+    em[5, :] = 0
+    em[5, :kept] = 1
+    for o in (port, ref):
+        with pytest.raises(DataError, match=msg):
+            o.compress_with_mask(x, SparsityConfig(block_size=4), 0, em, [0, 0, 0, 0])
+    # the same group in a dense block is never consulted
+    for o in (port, ref):
+        o.compress_with_mask(x, SparsityConfig(block_size=4), 0, em, [0, 1, 0, 0])
