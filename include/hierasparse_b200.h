@@ -210,6 +210,18 @@ HS_API hs_status hs_decode(const void* q, const hs_device_cache* k, const hs_dev
                            const void* k_tail, const void* v_tail, uint32_t tail, uint32_t gqa,
                            float scale, uint32_t splits, float* out, void* stream);
 
+/* hs_decode with a caller-owned workspace (split partials + arrival counters):
+ * a captured decode graph that owns its workspace shares no state with other
+ * decode work, whatever stream handle it is replayed on.  The workspace must
+ * hold hs_decode_workspace_bytes(k, gqa, splits) bytes and be zeroed before
+ * its first use (the kernels re-arm their counters). */
+HS_API hs_status hs_decode_workspace_bytes(const hs_device_cache* k, uint32_t gqa, uint32_t splits,
+                                           uint64_t* bytes);
+HS_API hs_status hs_decode_ws(const void* q, const hs_device_cache* k, const hs_device_cache* v,
+                              const void* k_tail, const void* v_tail, uint32_t tail, uint32_t gqa, float scale,
+                              uint32_t splits, float* out, void* workspace, uint64_t workspace_bytes,
+                              void* stream);
+
 /* attend_range (attention.hpp:249-304) over blocks [block_begin, block_end)
  * (+ the tail when include_tail), non-causal, returning the unnormalised
  * SplitPartial (attention.hpp:65-69) per unit:

@@ -35,8 +35,8 @@ class DeviceCacheC(C.Structure):
 # Exported symbols (every one declared in include/hierasparse_b200.h).
 EXPORTS = ("hs_last_error", "hs_version", "hs_status_word_decode", "hs_pool_counts", "hs_cache_bytes",
            "hs_prune_compress", "hs_compress_with_flags", "hs_compress_with_mask", "hs_decompress", "hs_recompress",
-           "hs_absorb_tail", "hs_decode", "hs_decode_partial", "hs_decode_combine", "hs_prefill",
-           "hs_kernel_launches")
+           "hs_absorb_tail", "hs_decode", "hs_decode_workspace_bytes", "hs_decode_ws", "hs_decode_partial",
+           "hs_decode_combine", "hs_prefill", "hs_kernel_launches")
 
 _lib = None
 
@@ -66,6 +66,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hs_absorb_tail": [P(DeviceCacheC), vp, u64, u64, P(SparsityConfigC), C.c_double, P(DeviceCacheC), vp, vp,
                            vp, vp],
         "hs_decode": [vp, P(DeviceCacheC), P(DeviceCacheC), vp, vp, u32, u32, C.c_float, u32, vp, vp],
+        "hs_decode_workspace_bytes": [P(DeviceCacheC), u32, u32, P(u64)],
+        "hs_decode_ws": [vp, P(DeviceCacheC), P(DeviceCacheC), vp, vp, u32, u32, C.c_float, u32, vp, vp, u64, vp],
         "hs_decode_partial": [vp, P(DeviceCacheC), P(DeviceCacheC), vp, vp, u32, u32, C.c_float, u32, u32,
                               i32, vp, vp],
         "hs_decode_combine": [vp, u32, u32, u32, u32, vp, vp],

@@ -165,18 +165,21 @@ std::map<std::tuple<int, cudaStream_t, int>, Workspace> g_ws;
 
 enum WsKind { kWsCompress = 0, kWsDecode = 1, kWsMisc = 2, kWsPrefill = 3 };
 
+std::vector<void*> g_ws_retired;  // outgrown workspaces: never freed (a captured graph may still use them)
+
 // Per (device, stream, purpose) scratch; grows on demand and is zeroed on
 // (re)allocation (the decode arrival counters rely on that and self-reset).
+// An outgrown buffer is retired, not freed: a CUDA graph captured earlier on
+// this stream handle keeps pointing at it.  Graphs that must not share state
+// with other work on a recycled stream handle pass their own workspace
+// (hs_decode_ws).
 void* workspace(cudaStream_t s, size_t bytes, int kind, hs_status* st) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_ws_mu);
     Workspace& w = g_ws[std::make_tuple(dev, s, kind)];
     if (w.bytes < bytes) {
-        if (w.ptr) {
-            cudaStreamSynchronize(s);
-            cudaFree(w.ptr);
-        }
+        if (w.ptr) g_ws_retired.push_back(w.ptr);
         w.ptr = nullptr;
         w.bytes = 0;
         const size_t nb = bytes + (bytes >> 2) + 4096;
@@ -530,10 +533,22 @@ HS_API hs_status hs_status_word_decode(uint64_t word) {
 
 constexpr int kDynamicMaxBlocks = 256;  // blocks per split up to which decode claims blocks dynamically
 
+// Split count and workspace bytes of a decode launch (counters + split partials).
+static void decode_geometry(uint32_t n_units, uint32_t span, uint32_t gqa, uint32_t splits, int* ns_out,
+                            size_t* cnt_bytes, size_t* part_bytes) {
+    int ns = splits ? static_cast<int>(splits) : choose_splits(static_cast<int>(n_units), static_cast<int>(span));
+    if (ns > static_cast<int>(span)) ns = static_cast<int>(span);  // attention.hpp:373-374 clamp
+    if (ns < 1) ns = 1;
+    *ns_out = ns;
+    *part_bytes = static_cast<size_t>(n_units) * ns * gqa * (hs::kHeadDim + 2) * sizeof(float);
+    *cnt_bytes = ((3 * static_cast<size_t>(n_units) * sizeof(int) + 255) / 256) * 256;
+}
+
 static hs_status decode_common(const void* q, const hs_device_cache* k, const hs_device_cache* v,
                                const void* k_tail, const void* v_tail, uint32_t tail, uint32_t gqa,
                                float scale, uint32_t splits, uint32_t block_begin, uint32_t block_end,
-                               int include_tail, float* out, int out_mode, void* stream) {
+                               int include_tail, float* out, int out_mode, void* user_ws,
+                               uint64_t user_ws_bytes, void* stream) {
     hs_status st = check_pair(k, v);
     if (st) return st;
     HS_CHECK_CONFIG(q != nullptr && out != nullptr, "decode_attention: null argument");
@@ -574,26 +589,34 @@ static hs_status decode_common(const void* q, const hs_device_cache* k, const hs
     L.block_end = block_end;
     L.include_tail = include_tail;
     const int span = static_cast<int>(block_end - block_begin);
-    int ns = splits ? static_cast<int>(splits) : choose_splits(L.n_units, span);
-    if (ns > span) ns = span;  // attention.hpp:373-374 clamp
-    if (ns < 1) ns = 1;
+    int ns;
+    size_t cnt_bytes, part_bytes;
+    decode_geometry(L.n_units, static_cast<uint32_t>(span), gqa, splits, &ns, &cnt_bytes, &part_bytes);
     L.nsplit = ns;
     L.max_blocks_per_cta = (span + ns - 1) / ns + 1;
     HS_CHECK_CONFIG(L.max_blocks_per_cta <= 8192,
                     "decode_attention: %d blocks per CTA exceeds the index stage; use more splits",
                     L.max_blocks_per_cta);
     if ((st = fill_decode_maps(L, k, v))) return st;
-    const size_t part_bytes = static_cast<size_t>(L.n_units) * ns * gqa * (hs::kHeadDim + 2) * sizeof(float);
-    const size_t cnt_bytes = ((3 * static_cast<size_t>(L.n_units) * sizeof(int) + 255) / 256) * 256;
-    uint8_t* ws = static_cast<uint8_t*>(workspace(s, cnt_bytes + part_bytes, kWsDecode, &st));
-    if (st) return st;
+    uint8_t* ws;
+    if (user_ws != nullptr) {
+        HS_CHECK_CONFIG(user_ws_bytes >= cnt_bytes + part_bytes,
+                        "decode_attention: workspace of %llu bytes is smaller than the %llu needed",
+                        static_cast<unsigned long long>(user_ws_bytes),
+                        static_cast<unsigned long long>(cnt_bytes + part_bytes));
+        ws = static_cast<uint8_t*>(user_ws);
+    } else {
+        ws = static_cast<uint8_t*>(workspace(s, cnt_bytes + part_bytes, kWsDecode, &st));
+        if (st) return st;
+    }
     L.counters = reinterpret_cast<int*>(ws);
     L.partial = reinterpret_cast<float*>(ws + cnt_bytes);
     L.out = out;
     L.out_mode = out_mode;
     // The parallel combine spins on the unit's arrivals: only when the whole grid
-    // is resident at once (one wave of decode_ctas_per_sm() CTAs per SM).
-    L.coop_combine = static_cast<int64_t>(ns) * L.n_units <= static_cast<int64_t>(hs::decode_ctas_per_sm()) * sm_count();
+    // fits at once (occupancy of this smem plan); it is then launched cooperatively
+    // so residency is guaranteed, not assumed (decode.cu launch_t).
+    L.coop_combine = static_cast<int64_t>(ns) * L.n_units <= static_cast<int64_t>(hs::decode_resident_ctas(L, sm_count()));
     if (const char* env = getenv("HS_DECODE_COOP")) L.coop_combine = L.coop_combine && atoi(env) != 0;
     L.blk_ctr = L.counters + 2 * L.n_units;
     // splits == 0 (auto): the unit's CTAs claim blocks dynamically (balanced across
@@ -633,7 +656,27 @@ HS_API hs_status hs_decode(const void* q, const hs_device_cache* k, const hs_dev
                            float scale, uint32_t splits, float* out, void* stream) {
     HS_CHECK_CONFIG(k != nullptr, "decode_attention: null key cache");
     return decode_common(q, k, v, k_tail, v_tail, tail, gqa, scale, splits, 0, k->logical_blocks, 1, out, 0,
-                         stream);
+                         nullptr, 0, stream);
+}
+
+HS_API hs_status hs_decode_workspace_bytes(const hs_device_cache* k, uint32_t gqa, uint32_t splits,
+                                           uint64_t* bytes) {
+    HS_CHECK_CONFIG(k != nullptr && bytes != nullptr, "decode_attention: null argument");
+    int ns;
+    size_t cnt, part;
+    decode_geometry(k->n_units, k->logical_blocks, gqa, splits, &ns, &cnt, &part);
+    *bytes = cnt + part;
+    return HS_OK;
+}
+
+HS_API hs_status hs_decode_ws(const void* q, const hs_device_cache* k, const hs_device_cache* v,
+                              const void* k_tail, const void* v_tail, uint32_t tail, uint32_t gqa, float scale,
+                              uint32_t splits, float* out, void* workspace_ptr, uint64_t workspace_bytes,
+                              void* stream) {
+    HS_CHECK_CONFIG(k != nullptr, "decode_attention: null key cache");
+    HS_CHECK_CONFIG(workspace_ptr != nullptr, "decode_attention: null workspace");
+    return decode_common(q, k, v, k_tail, v_tail, tail, gqa, scale, splits, 0, k->logical_blocks, 1, out, 0,
+                         workspace_ptr, workspace_bytes, stream);
 }
 
 HS_API hs_status hs_decode_partial(const void* q, const hs_device_cache* k, const hs_device_cache* v,
@@ -641,7 +684,7 @@ HS_API hs_status hs_decode_partial(const void* q, const hs_device_cache* k, cons
                                    float scale, uint32_t block_begin, uint32_t block_end, int include_tail,
                                    float* partial, void* stream) {
     return decode_common(q, k, v, k_tail, v_tail, tail, gqa, scale, 0, block_begin, block_end, include_tail,
-                         partial, 1, stream);
+                         partial, 1, nullptr, 0, stream);
 }
 
 HS_API hs_status hs_decode_combine(const float* partials, uint32_t n_parts, uint32_t n_units, uint32_t gqa,
@@ -668,7 +711,7 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     HS_CHECK_CONFIG(k->logical_blocks / 2 + 8 <= 4096,
                     "prefill_attention: %u blocks exceed the kernel's key-tile list (max 8184 blocks)",
                     k->logical_blocks);
-    HS_CHECK_CONFIG(k->slot_block != nullptr, "prefill_attention: key cache needs slot_block");
+    HS_CHECK_CONFIG(k->logical_blocks == 0 || k->slot_block != nullptr, "prefill_attention: key cache needs slot_block");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     hs::PrefillLaunch L{};
     L.bf16 = k->dtype == HS_DTYPE_BF16;

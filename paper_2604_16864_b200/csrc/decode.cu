@@ -21,6 +21,10 @@
 // merge (m, l, O) with the reference combine: cooperatively (every CTA merges a
 // slice once the unit's partials are in) when the grid is resident, otherwise
 // in the unit's last CTA.
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -582,8 +586,7 @@ __global__ void combine_kernel(const float* partials, int n_parts, int n_units, 
 }
 
 template <typename T, int NW, bool HILO>
-cudaError_t launch_t(const DecodeLaunch& L, int spw, StageLayout lay, size_t smem,
-                     cudaStream_t s) {
+cudaError_t configure_t(size_t smem) {
     auto k = decode_kernel<T, NW, HILO>;
     static int configured_smem = 0;  // per instantiation; raise the opt-in once
     if (static_cast<int>(smem) > configured_smem) {
@@ -591,7 +594,57 @@ cudaError_t launch_t(const DecodeLaunch& L, int spw, StageLayout lay, size_t sme
         if (err) return err;
         configured_smem = static_cast<int>(smem);
     }
-    k<<<dim3(L.nsplit, L.n_units), 32 * NW, smem, s>>>(L, spw, lay);
+    return cudaSuccess;
+}
+
+// Resident CTAs of this instantiation at `smem` bytes over the whole device.
+template <typename T, int NW, bool HILO>
+int resident_t(size_t smem, int sms) {
+    static std::mutex mu;
+    static std::map<std::pair<size_t, int>, int> cache;  // (smem, device) -> CTAs per SM
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({smem, dev});
+    if (it != cache.end()) return it->second * sms;
+    if (configure_t<T, NW, HILO>(smem) != cudaSuccess) return 0;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<T, NW, HILO>, 32 * NW, smem) !=
+        cudaSuccess)
+        return 0;
+    cache[{smem, dev}] = per_sm;
+    return per_sm * sms;
+}
+
+// The cooperative combine spins on the other CTAs of its unit, so it is only
+// launched with cudaLaunchAttributeCooperative: the driver then guarantees the
+// whole grid is co-resident or refuses the launch (MPS / green-context SM
+// limits, concurrent kernels holding SMs), and the caller falls back to the
+// last-CTA ticket combine.
+template <typename T, int NW, bool HILO>
+cudaError_t launch_t(const DecodeLaunch& L, int spw, StageLayout lay, size_t smem,
+                     cudaStream_t s) {
+    cudaError_t err = configure_t<T, NW, HILO>(smem);
+    if (err) return err;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(L.nsplit, L.n_units);
+    cfg.blockDim = dim3(32 * NW);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = L.coop_combine ? 1 : 0;
+    err = cudaLaunchKernelEx(&cfg, decode_kernel<T, NW, HILO>, L, spw, lay);
+    if (err != cudaSuccess && L.coop_combine) {
+        (void)cudaGetLastError();  // cooperative launch refused: ticket combine instead
+        DecodeLaunch L2 = L;
+        L2.coop_combine = 0;
+        cfg.numAttrs = 0;
+        err = cudaLaunchKernelEx(&cfg, decode_kernel<T, NW, HILO>, L2, spw, lay);
+    }
+    if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }
 
@@ -631,6 +684,14 @@ size_t decode_smem_bytes(const DecodeLaunch& L, int* nw_out, int* spw_out, Stage
     *spw_out = spw;
     *lay_out = lay;
     return smem;
+}
+
+int decode_resident_ctas(const DecodeLaunch& L, int sms) {
+    int nw, spw;
+    StageLayout lay;
+    const size_t smem = decode_smem_bytes(L, &nw, &spw, &lay);
+    if (nw == 4) return L.bf16 ? resident_t<__nv_bfloat16, 4, true>(smem, sms) : resident_t<__half, 4, false>(smem, sms);
+    return L.bf16 ? resident_t<__nv_bfloat16, 8, true>(smem, sms) : resident_t<__half, 8, false>(smem, sms);
 }
 
 cudaError_t launch_decode(const DecodeLaunch& L, cudaStream_t s) {

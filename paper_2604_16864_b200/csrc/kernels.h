@@ -103,6 +103,7 @@ struct DecodeLaunch {
     CUtensorMap tm_knnz, tm_kden, tm_vnnz, tm_vden;
 };
 cudaError_t launch_decode(const DecodeLaunch& L, cudaStream_t s);
+int decode_resident_ctas(const DecodeLaunch& L, int sms);  // co-resident CTAs at L's smem plan
 int decode_ctas_per_sm();  // CTAs the decode ring is sized for (1 or 2)
 cudaError_t launch_combine(const float* partials, int n_parts, int n_units, int gqa, int d,
                            float* out, cudaStream_t s);

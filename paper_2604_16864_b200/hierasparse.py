@@ -335,9 +335,12 @@ def recompress_pair(k: DeviceCompressedCache, v: DeviceCompressedCache, cfg: Spa
     return recompress(k, cfg, cfg.s_key), recompress(v, cfg, cfg.s_value)
 
 
-def _tails(k_tail, v_tail, U, d):
+def _tails(k_tail, v_tail, U, d, dtype):
     if k_tail is None or k_tail.numel() == 0:
         return None, None, 0
+    for t in (k_tail, v_tail):
+        if t is None or not t.is_cuda or t.dtype != dtype:
+            raise ConfigError(f"attention: dense tails must be CUDA tensors of the caches' dtype {dtype}")
     k_tail = k_tail.reshape(U, -1, d).contiguous()
     v_tail = v_tail.reshape(U, -1, d).contiguous()
     if k_tail.shape != v_tail.shape:
@@ -345,16 +348,47 @@ def _tails(k_tail, v_tail, U, d):
     return k_tail, v_tail, k_tail.shape[1]
 
 
-def decode_attention(q: torch.Tensor, k: DeviceCompressedCache, v: DeviceCompressedCache,
+def _check_queries(q: torch.Tensor, k: DeviceCompressedCache, what: str) -> None:
+    """The device kernels read q as [units, ..., head_dim] of the caches' 16-bit
+    dtype: reject anything else instead of reinterpreting its bits."""
+    if not isinstance(q, torch.Tensor) or not q.is_cuda:
+        raise ConfigError(f"{what}: queries must be a CUDA tensor")
+    if q.dtype != k.dtype:
+        raise ConfigError(f"{what}: query dtype {q.dtype} differs from the caches' {k.dtype}")
+    if q.dim() < 2 or q.shape[0] != k.n_units or q.shape[-1] != k.head_dim:
+        raise ConfigError(f"{what}: queries {tuple(q.shape)} do not match {k.n_units} units x head_dim "
+                          f"{k.head_dim}")
+
+
+def _tail_only_view(k, v, k_tail, v_tail, q, what):
+    """CacheView{compressed = nullptr, dense_tail} (attention.hpp:22-31): the
+    attention runs over the tail alone, through zero-block caches."""
+    if k is not None and v is not None:
+        return k, v
+    if k is not None or v is not None:
+        raise ConfigError(f"{what}: key and value caches must both be given or both be None")
+    if k_tail is None or k_tail.numel() == 0:
+        raise ConfigError(f"{what}: empty key/value cache")
+    U = q.shape[0]
+    d = k_tail.shape[-1]
+    ke = DeviceCompressedCache(k_tail.dtype, capi.AXIS_CHANNEL, U, 0, 0, 0, k_tail.device, d)
+    ve = DeviceCompressedCache(k_tail.dtype, capi.AXIS_SEQUENCE, U, 0, 0, 0, k_tail.device, d)
+    return ke, ve
+
+
+def decode_attention(q: torch.Tensor, k: DeviceCompressedCache | None, v: DeviceCompressedCache | None,
                      k_tail: torch.Tensor | None = None, v_tail: torch.Tensor | None = None,
                      scale: float | None = None, splits: int = 0,
                      out: torch.Tensor | None = None) -> torch.Tensor:
-    """decode_attention (attention.hpp:360-409) for every unit: q [units, gqa, d] -> fp32."""
+    """decode_attention (attention.hpp:360-409) for every unit: q [units, gqa, d] -> fp32.
+    k = v = None attends to the dense tail alone (CacheView without a compressed cache)."""
+    k, v = _tail_only_view(k, v, k_tail, v_tail, q, "decode_attention")
+    _check_queries(q, k, "decode_attention")
     U = k.n_units
-    if q.dim() != 3 or q.shape[0] != U or not q.is_contiguous():
+    if q.dim() != 3 or not q.is_contiguous():
         q = q.reshape(U, -1, k.head_dim).contiguous()
     gqa = q.shape[1]
-    kt, vt, tail = _tails(k_tail, v_tail, U, k.head_dim)
+    kt, vt, tail = _tails(k_tail, v_tail, U, k.head_dim, k.dtype)
     scale = 1.0 / math.sqrt(k.head_dim) if scale is None else scale
     if out is None:
         out = torch.empty((U, gqa, k.head_dim), dtype=torch.float32, device=q.device)
@@ -366,24 +400,38 @@ def decode_attention(q: torch.Tensor, k: DeviceCompressedCache, v: DeviceCompres
 class DecodePlan:
     """A decode step captured once as a CUDA graph and replayed per token:
     hs_decode's kernels with fixed caches, query and output buffers (the host
-    enqueue cost disappears from the step; inputs are refreshed in place)."""
+    enqueue cost disappears from the step; inputs are refreshed in place).
+    The plan owns its workspace (split partials + arrival counters,
+    hs_decode_ws), so replays share no state with other decode work."""
 
     def __init__(self, q: torch.Tensor, k: DeviceCompressedCache, v: DeviceCompressedCache,
                  scale: float | None = None, splits: int = 0):
+        _check_queries(q, k, "DecodePlan")
         self.q = q.contiguous().clone()
         self.k, self.v = k, v
-        self.out = torch.empty((k.n_units, self.q.shape[1], k.head_dim), dtype=torch.float32, device=q.device)
-        # Warm up on the capture stream so its workspace and TMA descriptors exist
-        # before capture (no allocation may happen inside the graph).
+        gqa = self.q.shape[1]
+        self.out = torch.empty((k.n_units, gqa, k.head_dim), dtype=torch.float32, device=q.device)
+        lib = capi.load()
+        nbytes = C.c_uint64()
+        capi.check(lib.hs_decode_workspace_bytes(k.cref(), gqa, splits, C.byref(nbytes)))
+        self.workspace = torch.zeros(int(nbytes.value), dtype=torch.uint8, device=q.device)
+        scale = 1.0 / math.sqrt(k.head_dim) if scale is None else scale
+
+        def step():
+            capi.check(lib.hs_decode_ws(self.q.data_ptr(), k.cref(), v.cref(), None, None, 0, gqa, scale, splits,
+                                        self.out.data_ptr(), self.workspace.data_ptr(), self.workspace.numel(),
+                                        _stream()))
+        # Warm up on the capture stream so the TMA descriptors exist before
+        # capture (no allocation may happen inside the graph).
         self.stream = torch.cuda.Stream()
         self.stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.stream):
-            decode_attention(self.q, k, v, scale=scale, splits=splits, out=self.out)
+            step()
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
         n0 = capi.kernel_launches()
         with torch.cuda.graph(self.graph, stream=self.stream):
-            decode_attention(self.q, k, v, scale=scale, splits=splits, out=self.out)
+            step()
         torch.cuda.synchronize()
         self.kernels_per_step = capi.kernel_launches() - n0  # native kernels inside the graph
 
@@ -398,14 +446,15 @@ def decode_partial(q, k: DeviceCompressedCache, v: DeviceCompressedCache, block_
                    k_tail=None, v_tail=None, include_tail: bool = True, scale: float | None = None):
     """attend_range (attention.hpp:249-304) over [block_begin, block_end) as an
     unnormalised SplitPartial per unit: float [units, gqa, d + 2] = (O, m, l)."""
+    k, v = _tail_only_view(k, v, k_tail, v_tail, q, "attend_range")
+    _check_queries(q, k, "attend_range")
     U = k.n_units
     q = q.reshape(U, -1, k.head_dim).contiguous()
     gqa = q.shape[1]
-    kt, vt, tail = _tails(k_tail, v_tail, U, k.head_dim)
+    kt, vt, tail = _tails(k_tail, v_tail, U, k.head_dim, k.dtype)
     scale = 1.0 / math.sqrt(k.head_dim) if scale is None else scale
     out = torch.empty((U, gqa, k.head_dim + 2), dtype=torch.float32, device=q.device)
-    kc, vc = k.c(), v.c()
-    capi.check(capi.load().hs_decode_partial(q.data_ptr(), C.byref(kc), C.byref(vc), _ptr(kt), _ptr(vt), tail,
+    capi.check(capi.load().hs_decode_partial(q.data_ptr(), k.cref(), v.cref(), _ptr(kt), _ptr(vt), tail,
                                              gqa, scale, block_begin, block_end, int(include_tail),
                                              out.data_ptr(), _stream()))
     return out
@@ -413,6 +462,8 @@ def decode_partial(q, k: DeviceCompressedCache, v: DeviceCompressedCache, block_
 
 def decode_combine(partials: torch.Tensor) -> torch.Tensor:
     """LSE combine (attention.hpp:387-407) of partials [parts, units, gqa, d + 2]."""
+    if not partials.is_cuda or partials.dtype != torch.float32 or partials.dim() != 4:
+        raise ConfigError("decode_combine: partials must be a CUDA float32 [parts, units, gqa, d + 2] tensor")
     partials = partials.contiguous()
     P, U, gqa, d2 = partials.shape
     out = torch.empty((U, gqa, d2 - 2), dtype=torch.float32, device=partials.device)
@@ -420,21 +471,27 @@ def decode_combine(partials: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def prefill_attention(q: torch.Tensor, k: DeviceCompressedCache, v: DeviceCompressedCache,
+def prefill_attention(q: torch.Tensor, k: DeviceCompressedCache | None, v: DeviceCompressedCache | None,
                       k_tail=None, v_tail=None, causal: bool = True, scale: float | None = None,
                       out: torch.Tensor | None = None) -> torch.Tensor:
-    """prefill_attention (attention.hpp:323-354): q [units, gqa, n_q, d] -> fp32."""
+    """prefill_attention (attention.hpp:323-354): q [units, gqa, n_q, d] -> fp32.
+    k = v = None attends to the dense tail alone (CacheView without a compressed cache)."""
+    k, v = _tail_only_view(k, v, k_tail, v_tail, q, "prefill_attention")
+    _check_queries(q, k, "prefill_attention")
     U = k.n_units
     if q.dim() == 3:
         q = q.unsqueeze(1)
+    if q.dim() != 4:
+        raise ConfigError("prefill_attention: queries must be [units, gqa, n_q, head_dim]")
     q = q.contiguous()
     _, gqa, n_q, d = q.shape
-    kt, vt, tail = _tails(k_tail, v_tail, U, k.head_dim)
+    kt, vt, tail = _tails(k_tail, v_tail, U, k.head_dim, k.dtype)
     scale = 1.0 / math.sqrt(k.head_dim) if scale is None else scale
     if out is None:
         out = torch.empty((U, gqa, n_q, d), dtype=torch.float32, device=q.device)
-    kc, vc = k.c(), v.c()
-    capi.check(capi.load().hs_prefill(q.data_ptr(), n_q, gqa, C.byref(kc), C.byref(vc), _ptr(kt), _ptr(vt), tail,
+    elif out.shape != (U, gqa, n_q, d) or out.dtype != torch.float32 or not out.is_contiguous():
+        raise ConfigError("prefill_attention: out must be a contiguous float32 [units, gqa, n_q, head_dim] tensor")
+    capi.check(capi.load().hs_prefill(q.data_ptr(), n_q, gqa, k.cref(), v.cref(), _ptr(kt), _ptr(vt), tail,
                                       int(causal), scale, out.data_ptr(), _stream()))
     return out
 

@@ -136,3 +136,67 @@ def test_decode_fixed_splits_deterministic(hs, port):
     assert all((r == runs[0]).all() for r in runs[1:])
     auto = [hs.decode_attention(q, kc, vc).cpu().numpy() for _ in range(3)]
     assert max(np.abs(a - runs[0]).max() for a in auto) < 1e-5
+
+
+def test_decode_concurrent_streams(hs, port):
+    """Two full-machine decodes (auto splits: the cooperative combine) launched on
+    two streams at once never deadlock and each equals its single-stream result:
+    the cooperative launch guarantees co-residency instead of assuming it."""
+    import torch
+    U, L = 8, 16384
+    kx, vx, kc, vc = build_caches(hs, port, U, L, 1.0, "bf16", seed=3)
+    kx2, vx2, kc2, vc2 = build_caches(hs, port, U, L, 0.5, "bf16", seed=4)
+    q = to_torch(decode_queries(port, U, 4, "bf16"), "bf16")
+    want1 = hs.decode_attention(q, kc, vc).clone()
+    want2 = hs.decode_attention(q, kc2, vc2).clone()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs1, outs2 = [], []
+    torch.cuda.synchronize()
+    for _ in range(20):
+        with torch.cuda.stream(s1):
+            outs1.append(hs.decode_attention(q, kc, vc))
+        with torch.cuda.stream(s2):
+            outs2.append(hs.decode_attention(q, kc2, vc2))
+    torch.cuda.synchronize()
+    for a in outs1:
+        assert (a - want1).abs().max().item() < 1e-5
+    for b in outs2:
+        assert (b - want2).abs().max().item() < 1e-5
+
+
+def test_decode_plans_own_their_workspaces(hs, port):
+    """DecodePlan graphs replayed interleaved (and on recycled stream handles)
+    share no split partials or arrival counters (hs_decode_ws)."""
+    import torch
+    U = 4
+    plans, wants = [], []
+    for i, L in enumerate((4096, 32768, 8192)):
+        kx, vx, kc, vc = build_caches(hs, port, U, L, 1.0, "bf16", seed=10 + i)
+        q = to_torch(decode_queries(port, U, 4, "bf16", seed=10 + i), "bf16")
+        wants.append(hs.decode_attention(q, kc, vc).clone())
+        plans.append(hs.DecodePlan(q, kc, vc))
+    # a later, larger decode on the default path must not disturb the plans
+    kx, vx, kcb, vcb = build_caches(hs, port, 8, 65536, 1.0, "bf16", seed=20)
+    hs.decode_attention(to_torch(decode_queries(port, 8, 8, "bf16"), "bf16"), kcb, vcb)
+    for _ in range(5):
+        for p, w in zip(plans, wants):
+            p()
+        torch.cuda.synchronize()
+        for p, w in zip(plans, wants):
+            assert (p.out - w).abs().max().item() < 1e-5
+
+
+@pytest.mark.parametrize("tail", [1, 37, 200])
+def test_decode_tail_only_view(hs, port, tail):
+    """CacheView{compressed = nullptr, dense_tail} (attention.hpp:22-31): decode over
+    the tail alone equals the reference's dense oracle on the tail tokens."""
+    U, gqa = 2, 4
+    kx = gen_units(port, U, tail, 128, 8, 0, "bf16")
+    vx = gen_units(port, U, tail, 128, 8, 1, "bf16")
+    q = decode_queries(port, U, gqa, "bf16", seed=8)
+    scale = np.float32(1.0 / math.sqrt(128))
+    got = hs.decode_attention(to_torch(q, "bf16"), None, None, to_torch(kx, "bf16"), to_torch(vx, "bf16"),
+                              scale=float(scale)).cpu().numpy()
+    want = np.stack([port.dense_attention(q[u], kx[u], vx[u], False, scale) for u in range(U)])
+    mx, mr = err_stats(got, want)
+    assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)

@@ -143,12 +143,13 @@ def test_prefill_logit_ranges(hs, port, dtype, qscale, negative):
 ])
 def test_prefill_with_dense_tail(hs, port, dtype, L, tail, n_q, s, causal):
     """prefill_attention with CacheView::dense_tail (attention.hpp:19-31, :289-297)."""
-    if L == 0:
-        pytest.skip("a cache needs at least one compressed block on the device path")
     U, gqa = 2, 2
     kx = gen_units(port, U, L + tail, 128, 13, 0, dtype)
     vx = gen_units(port, U, L + tail, 128, 13, 1, dtype)
-    kc, vc = hs.prune_cache(to_torch(kx[:, :L], dtype), to_torch(vx[:, :L], dtype), hs.SparsityConfig(s, s, 64))
+    if L == 0:  # CacheView{compressed = nullptr, dense_tail} (attention.hpp:22-31)
+        kc = vc = None
+    else:
+        kc, vc = hs.prune_cache(to_torch(kx[:, :L], dtype), to_torch(vx[:, :L], dtype), hs.SparsityConfig(s, s, 64))
     q = np.stack([np.stack([port.round_to(port.random_gaussian(n_q, 128, port.head_seed(13, u, 2 + g)), dtype)
                             for g in range(gqa)]) for u in range(U)])
     scale = np.float32(1.0 / math.sqrt(128))
@@ -157,11 +158,29 @@ def test_prefill_with_dense_tail(hs, port, dtype, L, tail, n_q, s, causal):
 
     def one(ug):
         u, g = divmod(ug, gqa)
+        if kc is None:  # the tail alone: the reference's dense oracle over the tail tokens
+            return port.dense_attention(q[u, g], kx[u, L:], vx[u, L:], causal, scale)
         return port.prefill(q[u, g], device_to_oracle(kc, u), device_to_oracle(vc, u), kx[u, L:], vx[u, L:], causal,
                             scale, 64)
     want = np.stack(parallel(one, range(U * gqa))).reshape(U, gqa, n_q, 128)
     mx, mr = err_stats(got, want)
     assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
+
+
+def test_attention_rejects_mismatched_queries(hs, port):
+    """Queries are validated against the caches (dtype, units, head_dim, device)
+    instead of being reinterpreted (fp32 queries are a natural reference call)."""
+    import torch
+    kc, vc, q = setup(hs, port, 2, 256, 1.0, "f16", 1, 64)
+    qt = to_torch(q, "f16")
+    bad = [qt.float(), qt.to(torch.bfloat16), qt[:1], qt[..., :64].contiguous(), qt.cpu()]
+    for b in bad:
+        with pytest.raises(hs.ConfigError):
+            hs.prefill_attention(b, kc, vc)
+        with pytest.raises(hs.ConfigError):
+            hs.decode_attention(b[:, 0, :4], kc, vc)
+    with pytest.raises(hs.ConfigError):
+        hs.prefill_attention(qt, kc, vc, out=torch.empty(2, 1, 64, 64, device="cuda"))
 
 
 def test_prefill_rejects_invalid(hs, port):
