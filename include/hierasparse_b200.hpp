@@ -359,11 +359,14 @@ inline void decode_combine(const float* partials, uint32_t n_parts, uint32_t n_u
     check(hs_decode_combine(partials, n_parts, n_units, gqa, d, out, stream));
 }
 
-// prefill_attention (attention.hpp:323-354): q [n_units][gqa][n_q][d] -> out fp32.
+// prefill_attention (attention.hpp:323-354): q [n_units][gqa][n_q][d] -> out fp32,
+// over the compressed caches followed by an optional dense tail
+// k_tail / v_tail [n_units][tail][d] (CacheView::dense_tail, attention.hpp:19-31).
 inline void prefill_attention(const void* q, uint32_t n_q, uint32_t gqa, const DeviceCompressedCache& k,
                               const DeviceCompressedCache& v, bool causal, float scale, float* out,
-                              cudaStream_t stream = nullptr) {
-    check(hs_prefill(q, n_q, gqa, &k.desc(), &v.desc(), nullptr, nullptr, 0, causal ? 1 : 0, scale, out, stream));
+                              cudaStream_t stream = nullptr, const void* k_tail = nullptr,
+                              const void* v_tail = nullptr, uint32_t tail = 0) {
+    check(hs_prefill(q, n_q, gqa, &k.desc(), &v.desc(), k_tail, v_tail, tail, causal ? 1 : 0, scale, out, stream));
 }
 
 // flop_and_byte_count byte side (attention.hpp:415-467) for one unit.
@@ -451,35 +454,97 @@ DeviceBuffer<uint16_t> upload_units(const std::vector<const Tensor*>& units, DTy
     return d;
 }
 
-// decode_attention with host tensors: queries (gqa x d) and the two device caches
-// of one unit -> host output (gqa x d), the reference's Tensor2D shape.
+// Host-side views: a list of per-unit Tensor2D-like matrices (the reference's
+// Tensor2D per (request, KV head) unit; every unit of a call has the same shape).
+template <class Tensor>
+using UnitList = std::vector<const Tensor*>;
+
+namespace detail {
+template <class Tensor>
+std::vector<Tensor> download_units(const DeviceBuffer<float>& out, std::size_t n_units, std::size_t rows,
+                                   std::size_t cols) {
+    const auto h = out.to_host();
+    std::vector<Tensor> res;
+    res.reserve(n_units);
+    for (std::size_t u = 0; u < n_units; ++u) {
+        Tensor o(rows, cols);
+        std::copy(h.begin() + u * rows * cols, h.begin() + (u + 1) * rows * cols, o.data.begin());
+        res.push_back(std::move(o));
+    }
+    return res;
+}
+template <class Tensor>
+DeviceBuffer<uint16_t> upload_tails(const UnitList<Tensor>& tails, DType t, std::size_t n_units,
+                                    uint32_t* tail_rows) {
+    *tail_rows = 0;
+    if (tails.empty()) return DeviceBuffer<uint16_t>();
+    if (tails.size() != n_units) throw ConfigError("attention: one dense tail per unit");
+    *tail_rows = static_cast<uint32_t>(tails[0]->rows);
+    if (*tail_rows == 0) return DeviceBuffer<uint16_t>();
+    return upload_units<Tensor>(tails, t);
+}
+}  // namespace detail
+
+// decode_attention over every unit with host tensors: queries[u] (gqa x d), the
+// device caches of all units and optional dense tails (tail x d per unit) ->
+// one output Tensor2D (gqa x d) per unit.
+template <class Tensor>
+std::vector<Tensor> decode_attention_host(const UnitList<Tensor>& queries, const DeviceCompressedCache& k,
+                                          const DeviceCompressedCache& v, float scale, uint32_t splits = 0,
+                                          const UnitList<Tensor>& k_tails = {},
+                                          const UnitList<Tensor>& v_tails = {}) {
+    if (queries.size() != k.n_units()) throw ConfigError("decode_attention: one query matrix per unit");
+    const DType t = k.dtype();
+    const std::size_t gqa = queries[0]->rows, d = queries[0]->cols;
+    auto qd = upload_units<Tensor>(queries, t);
+    uint32_t tail = 0, tail_v = 0;
+    auto kt = detail::upload_tails<Tensor>(k_tails, t, k.n_units(), &tail);
+    auto vt = detail::upload_tails<Tensor>(v_tails, t, k.n_units(), &tail_v);
+    if (tail != tail_v) throw ConfigError("attention: key/value token counts differ");
+    DeviceBuffer<float> out(queries.size() * gqa * d);
+    decode_attention(qd.get(), k, v, static_cast<uint32_t>(gqa), scale, out.get(), nullptr, splits, kt.get(),
+                     vt.get(), tail);
+    check_cuda(cudaDeviceSynchronize(), "decode_attention");
+    return detail::download_units<Tensor>(out, queries.size(), gqa, d);
+}
+
+// One unit (the reference's decode_attention signature shape).
 template <class Tensor>
 Tensor decode_attention_host(const Tensor& queries, const DeviceCompressedCache& k, const DeviceCompressedCache& v,
                              float scale, uint32_t splits = 0) {
     if (k.n_units() != 1) throw ConfigError("decode_attention_host: one unit per call");
+    return std::move(decode_attention_host<Tensor>(UnitList<Tensor>{&queries}, k, v, scale, splits)[0]);
+}
+
+// prefill_attention over every unit and query head with host tensors:
+// queries[u * gqa + g] (n_q x d), optional dense tails per unit -> one output
+// Tensor2D (n_q x d) per (unit, query head), in the same order.
+template <class Tensor>
+std::vector<Tensor> prefill_attention_host(const UnitList<Tensor>& queries, uint32_t gqa,
+                                           const DeviceCompressedCache& k, const DeviceCompressedCache& v,
+                                           bool causal, float scale, const UnitList<Tensor>& k_tails = {},
+                                           const UnitList<Tensor>& v_tails = {}) {
+    if (gqa == 0 || queries.size() != static_cast<std::size_t>(k.n_units()) * gqa)
+        throw ConfigError("prefill_attention: n_units x gqa query matrices expected");
     const DType t = k.dtype();
-    auto qd = upload_units<Tensor>({&queries}, t);
-    DeviceBuffer<float> out(queries.rows * queries.cols);
-    decode_attention(qd.get(), k, v, static_cast<uint32_t>(queries.rows), scale, out.get(), nullptr, splits);
-    check_cuda(cudaDeviceSynchronize(), "decode_attention");
-    Tensor o(queries.rows, queries.cols);
-    auto h = out.to_host();
-    std::copy(h.begin(), h.end(), o.data.begin());
-    return o;
+    const std::size_t n_q = queries[0]->rows, d = queries[0]->cols;
+    auto qd = upload_units<Tensor>(queries, t);
+    uint32_t tail = 0, tail_v = 0;
+    auto kt = detail::upload_tails<Tensor>(k_tails, t, k.n_units(), &tail);
+    auto vt = detail::upload_tails<Tensor>(v_tails, t, k.n_units(), &tail_v);
+    if (tail != tail_v) throw ConfigError("attention: key/value token counts differ");
+    DeviceBuffer<float> out(queries.size() * n_q * d);
+    prefill_attention(qd.get(), static_cast<uint32_t>(n_q), gqa, k, v, causal, scale, out.get(), nullptr, kt.get(),
+                      vt.get(), tail);
+    check_cuda(cudaDeviceSynchronize(), "prefill_attention");
+    return detail::download_units<Tensor>(out, queries.size(), n_q, d);
 }
 
 template <class Tensor>
 Tensor prefill_attention_host(const Tensor& queries, const DeviceCompressedCache& k, const DeviceCompressedCache& v,
                               bool causal, float scale) {
     if (k.n_units() != 1) throw ConfigError("prefill_attention_host: one unit per call");
-    auto qd = upload_units<Tensor>({&queries}, k.dtype());
-    DeviceBuffer<float> out(queries.rows * queries.cols);
-    prefill_attention(qd.get(), static_cast<uint32_t>(queries.rows), 1, k, v, causal, scale, out.get());
-    check_cuda(cudaDeviceSynchronize(), "prefill_attention");
-    Tensor o(queries.rows, queries.cols);
-    auto h = out.to_host();
-    std::copy(h.begin(), h.end(), o.data.begin());
-    return o;
+    return std::move(prefill_attention_host<Tensor>(UnitList<Tensor>{&queries}, 1, k, v, causal, scale)[0]);
 }
 
 }  // namespace hierasparse::b200

@@ -10,6 +10,7 @@
 //   3. prefill_attention (causal) within the same bar (attention.hpp:323)
 //   4. errors map to the reference taxonomy (errors.hpp:10-25)
 //   5. the fused decode-phase recompress equals decompress -> prune_cache -> compress
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -172,6 +173,142 @@ int main() {
             report(threw, "ragged sequence raises ConfigError");
         }
     }
+    // Multi-unit prefill with dense tails and GQA 2 through the host overloads,
+    // against the reference's prefill_attention per (unit, query head) with
+    // CacheView::dense_tail (attention.hpp:19-31, :289-297).
+    {
+        const std::size_t U = 2, G = 2, L = 512, T = 37, NQ = 200;
+        const gpu::DType dt = gpu::DType::kF16;
+        ref::SparsityConfig rcfg;
+        rcfg.s_key = rcfg.s_value = 0.5;
+        gpu::SparsityConfig gcfg{0.5, 0.5, 64, 0, 0};
+        std::vector<ref::Tensor2D> keys, vals, ktails, vtails, qs;
+        for (std::size_t u = 0; u < U; ++u) {
+            const ref::Tensor2D kf = rounded(ref::random_gaussian(L + T, d, head_seed(7, u, 0)), dt);
+            const ref::Tensor2D vf = rounded(ref::random_gaussian(L + T, d, head_seed(7, u, 1)), dt);
+            keys.push_back(ref::slice_rows(kf, 0, L));
+            vals.push_back(ref::slice_rows(vf, 0, L));
+            ktails.push_back(ref::slice_rows(kf, L, L + T));
+            vtails.push_back(ref::slice_rows(vf, L, L + T));
+            for (std::size_t g = 0; g < G; ++g)
+                qs.push_back(rounded(ref::random_gaussian(NQ, d, head_seed(7, u, 2 + g)), dt));
+        }
+        std::vector<const ref::Tensor2D*> kp, vp, ktp, vtp, qp;
+        for (std::size_t u = 0; u < U; ++u) {
+            kp.push_back(&keys[u]);
+            vp.push_back(&vals[u]);
+            ktp.push_back(&ktails[u]);
+            vtp.push_back(&vtails[u]);
+        }
+        for (auto& q : qs) qp.push_back(&q);
+        auto kd = gpu::upload_units<ref::Tensor2D>(kp, dt);
+        auto vd = gpu::upload_units<ref::Tensor2D>(vp, dt);
+        auto [gk, gv] = gpu::prune_cache(kd.get(), vd.get(), dt, U, L, gcfg);
+        const auto got = gpu::prefill_attention_host<ref::Tensor2D>(qp, G, gk, gv, true, scale, ktp, vtp);
+        bool ok = got.size() == U * G;
+        double worst_mx = 0, worst_mr = 0;
+        for (std::size_t u = 0; u < U && ok; ++u) {
+            const auto masks = ref::prune_cache(keys[u], vals[u], rcfg);
+            const ref::CompressedCache rk = ref::fused_magnitude_compress(keys[u], masks.first.block, rcfg,
+                                                                          ref::GroupAxis::kChannel);
+            const ref::CompressedCache rv = ref::fused_magnitude_compress(vals[u], masks.second.block, rcfg,
+                                                                          ref::GroupAxis::kSequence);
+            for (std::size_t g = 0; g < G; ++g) {
+                ref::AttentionWorkload w;
+                w.queries = qs[u * G + g];
+                w.key_cache.compressed = &rk;
+                w.key_cache.dense_tail = ktails[u];
+                w.value_cache.compressed = &rv;
+                w.value_cache.dense_tail = vtails[u];
+                w.scale = scale;
+                w.causal = true;
+                const ref::Tensor2D want = ref::prefill_attention(w, ref::TileConfig{});
+                double mx, mr;
+                err_stats(got[u * G + g], want, mx, mr);
+                worst_mx = std::max(worst_mx, mx);
+                worst_mr = std::max(worst_mr, mr);
+            }
+        }
+        report(ok && worst_mx < 2e-2 && worst_mr < 1e-3,
+               "prefill_attention multi-unit, GQA 2, dense tails (max-abs " + std::to_string(worst_mx) +
+                   ", mean-rel " + std::to_string(worst_mr) + ")");
+
+        // decode over the same units with tails: the multi-unit host overload
+        std::vector<ref::Tensor2D> dq;
+        std::vector<const ref::Tensor2D*> dqp;
+        for (std::size_t u = 0; u < U; ++u) dq.push_back(rounded(ref::random_gaussian(4, d, head_seed(7, u, 32)), dt));
+        for (auto& q : dq) dqp.push_back(&q);
+        const auto dgot = gpu::decode_attention_host<ref::Tensor2D>(dqp, gk, gv, scale, 0, ktp, vtp);
+        worst_mx = worst_mr = 0;
+        for (std::size_t u = 0; u < U; ++u) {
+            const auto masks = ref::prune_cache(keys[u], vals[u], rcfg);
+            const ref::CompressedCache rk = ref::fused_magnitude_compress(keys[u], masks.first.block, rcfg,
+                                                                          ref::GroupAxis::kChannel);
+            const ref::CompressedCache rv = ref::fused_magnitude_compress(vals[u], masks.second.block, rcfg,
+                                                                          ref::GroupAxis::kSequence);
+            ref::AttentionWorkload w;
+            w.queries = dq[u];
+            w.key_cache.compressed = &rk;
+            w.key_cache.dense_tail = ktails[u];
+            w.value_cache.compressed = &rv;
+            w.value_cache.dense_tail = vtails[u];
+            w.scale = scale;
+            w.gqa_group = 4;
+            w.phase = ref::Phase::kDecode;
+            double mx, mr;
+            err_stats(dgot[u], ref::decode_attention(w, 3), mx, mr);
+            worst_mx = std::max(worst_mx, mx);
+            worst_mr = std::max(worst_mr, mr);
+        }
+        report(worst_mx < 2e-2 && worst_mr < 1e-3,
+               "decode_attention multi-unit with dense tails (max-abs " + std::to_string(worst_mx) + ")");
+    }
+
+    // compress under an explicit HierarchicalMask (compressed_cache.hpp:196-225):
+    // the pruner's own masks -> bit-identical pools; a 3-kept group -> DataError.
+    {
+        const std::size_t L = 1024;
+        const gpu::DType dt = gpu::DType::kBF16;
+        const ref::Tensor2D key = rounded(ref::random_gaussian(L, d, head_seed(9, 0, 0)), dt);
+        const ref::Tensor2D val = rounded(ref::random_gaussian(L, d, head_seed(9, 0, 1)), dt);
+        ref::SparsityConfig rcfg;
+        rcfg.s_key = rcfg.s_value = 0.5;
+        const auto masks = ref::prune_cache(key, val, rcfg);
+        bool ok = true;
+        for (int which = 0; which < 2; ++which) {
+            const ref::Tensor2D& x = which == 0 ? key : val;
+            const auto& hm = which == 0 ? masks.first : masks.second;
+            const ref::GroupAxis ax = which == 0 ? ref::GroupAxis::kChannel : ref::GroupAxis::kSequence;
+            const ref::CompressedCache rc = ref::compress(x, hm, rcfg, ax);
+            auto xd = gpu::upload_units<ref::Tensor2D>({&x}, dt);
+            gpu::DeviceBuffer<uint8_t> em(L * d), fl(L / 64);
+            gpu::check_cuda(cudaMemcpy(em.get(), hm.element.bits.data(), L * d, cudaMemcpyHostToDevice), "H2D");
+            gpu::check_cuda(cudaMemcpy(fl.get(), hm.block.flags.data(), L / 64, cudaMemcpyHostToDevice), "H2D");
+            uint32_t dense = 0;
+            for (auto f : hm.block.flags) dense += f != 0;
+            const auto gc = gpu::compress(xd.get(), em.get(), fl.get(), dense, dt, 1, L,
+                                          which == 0 ? gpu::GroupAxis::kChannel : gpu::GroupAxis::kSequence);
+            ok = ok && pools_equal(rc, gc, dt);
+            if (which == 0) {
+                std::vector<uint8_t> bad = hm.element.bits;
+                std::size_t b = 0;
+                while (hm.block.flags[b]) ++b;  // first sparse block
+                bad[(b * 64 + 5) * d + 8 + 3] = 1;  // stored row 5, group 2: three or more kept
+                bad[(b * 64 + 5) * d + 8 + 0] = 1;
+                bad[(b * 64 + 5) * d + 8 + 1] = 1;
+                gpu::check_cuda(cudaMemcpy(em.get(), bad.data(), L * d, cudaMemcpyHostToDevice), "H2D");
+                bool threw = false;
+                try {
+                    gpu::compress(xd.get(), em.get(), fl.get(), dense, dt, 1, L, gpu::GroupAxis::kChannel);
+                } catch (const gpu::DataError& e) {
+                    threw = std::string(e.what()).find("more than n_keep") != std::string::npos;
+                }
+                report(threw, "compress: a group keeping 3 elements raises DataError");
+            }
+        }
+        report(ok, "compress under the pruner's HierarchicalMask bit-exact");
+    }
+
     std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
     return g_fail ? 1 : 0;
 }
