@@ -233,8 +233,11 @@ hs_status pool_counts(uint64_t rows, const hs_sparsity_config* cfg, double s, ui
 hs_status check_device_cache(const hs_device_cache* c, const char* what) {
     HS_CHECK_CONFIG(c != nullptr, "%s: null cache", what);
     HS_CHECK_CONFIG(c->dtype == HS_DTYPE_BF16 || c->dtype == HS_DTYPE_F16, "%s: unsupported dtype", what);
-    HS_CHECK_CONFIG(c->block_size == hs::kBlock, "%s: device kernels need block_size 64", what);
-    HS_CHECK_CONFIG(c->head_dim == hs::kHeadDim, "%s: device kernels need head_dim 128", what);
+    // masks.hpp:87 (block_size a positive multiple of m_group); pruner.hpp:172-173 /
+    // compressed_cache.hpp:123-126 (the channel grouping axis divisible by m_group)
+    HS_CHECK_CONFIG(c->block_size >= 4 && c->block_size % 4 == 0,
+                    "%s: block_size must be a positive multiple of m_group", what);
+    HS_CHECK_CONFIG(c->head_dim >= 4 && c->head_dim % 4 == 0, "%s: head dimension not divisible by m_group", what);
     HS_CHECK_CONFIG(c->n_units >= 1, "%s: n_units must be positive", what);
     HS_CHECK_CONFIG(c->dense_count + c->sparse_count == c->logical_blocks,
                     "%s: pool counts do not cover the block map", what);
@@ -339,7 +342,6 @@ static hs_status prune_compress_common(const void* src, uint64_t src_unit_stride
     hs_status st = pool_counts(rows, cfg, sparsity, &nb, &dc, &sc, &pre, &suf, &quota);
     if (st) return st;
     HS_CHECK_CONFIG(out->head_dim % 4 == 0, "prune_cache: head dimension not divisible by m_group");
-    HS_CHECK_CONFIG(cfg->block_size == hs::kBlock, "prune_cache: device kernels need block_size 64");
     HS_CHECK_CONFIG(out->block_size == cfg->block_size, "prune_cache: cache block size mismatch");
     HS_CHECK_CONFIG(out->logical_blocks == nb, "prune_cache: cache block count %u != %u", out->logical_blocks, nb);
     HS_CHECK_CONFIG(out->dense_count == dc && out->sparse_count == sc,
@@ -353,6 +355,8 @@ static hs_status prune_compress_common(const void* src, uint64_t src_unit_stride
     hs::CompressLaunch L{};
     L.bf16 = out->dtype == HS_DTYPE_BF16;
     L.axis = out->axis;
+    L.block_size = static_cast<int>(out->block_size);
+    L.head_dim = static_cast<int>(out->head_dim);
     L.n_units = out->n_units;
     L.nb = nb;
     L.dense_count = dc;
@@ -446,7 +450,6 @@ static hs_status compress_flags_common(const void* src, uint64_t src_unit_stride
                                        uint64_t mask_unit_stride, hs_device_cache* out, uint64_t* status,
                                        void* stream, const char* what) {
     HS_CHECK_CONFIG(out != nullptr && src != nullptr && flags != nullptr, "%s: null argument", what);
-    HS_CHECK_CONFIG(out->block_size == hs::kBlock, "%s: device kernels need block_size 64", what);
     HS_CHECK_CONFIG(rows % out->block_size == 0, "compress: sequence length not divisible by block_size");
     const uint32_t nb = static_cast<uint32_t>(rows / out->block_size);
     HS_CHECK_CONFIG(out->logical_blocks == nb, "compress: block mask does not cover the sequence");
@@ -461,6 +464,8 @@ static hs_status compress_flags_common(const void* src, uint64_t src_unit_stride
     hs::CompressLaunch L{};
     L.bf16 = out->dtype == HS_DTYPE_BF16;
     L.axis = out->axis;
+    L.block_size = static_cast<int>(out->block_size);
+    L.head_dim = static_cast<int>(out->head_dim);
     L.n_units = out->n_units;
     L.nb = nb;
     L.dense_count = out->dense_count;
@@ -508,7 +513,8 @@ HS_API hs_status hs_decompress(const hs_device_cache* c, void* dst, uint64_t* st
     hs::DecompressLaunch L{c->axis, static_cast<int>(c->n_units), static_cast<int>(c->logical_blocks),
                            static_cast<int>(c->dense_count), static_cast<int>(c->sparse_count),
                            c->index_map, c->dense_pool, c->nnz_pool, c->meta_pool, dst,
-                           reinterpret_cast<unsigned long long*>(status)};
+                           reinterpret_cast<unsigned long long*>(status), static_cast<int>(c->block_size),
+                           static_cast<int>(c->head_dim)};
     cudaError_t e = hs::launch_decompress(L, s);
     count_launch();
     if (e != cudaSuccess) return cuda_fail(e, "decompress launch");
@@ -544,6 +550,61 @@ static void decode_geometry(uint32_t n_units, uint32_t span, uint32_t gqa, uint3
     *cnt_bytes = ((3 * static_cast<size_t>(n_units) * sizeof(int) + 255) / 256) * 256;
 }
 
+// Fast kernels cover block_size 64 x head_dim 128 (the reference default B and
+// Llama-3.1-8B's d); other shapes run the generic CUDA-core attention.
+static bool specialised(const hs_device_cache* k) {
+    return k->block_size == static_cast<uint32_t>(hs::kBlock) && k->head_dim == static_cast<uint32_t>(hs::kHeadDim);
+}
+
+static hs_status generic_attention(const void* q, uint32_t n_q, uint32_t gqa, const hs_device_cache* k,
+                                   const hs_device_cache* v, const void* k_tail, const void* v_tail, uint32_t tail,
+                                   int causal, float scale, uint32_t block_begin, uint32_t block_end,
+                                   int include_tail, float* out, int out_mode, cudaStream_t s) {
+    HS_CHECK_CONFIG(k->head_dim <= static_cast<uint32_t>(hs::kGenericMaxHeadDim),
+                    "attention: head_dim %u above the generic kernel's %d", k->head_dim, hs::kGenericMaxHeadDim);
+    hs::GenericAttnLaunch G{};
+    G.bf16 = k->dtype == HS_DTYPE_BF16;
+    G.n_units = static_cast<int>(k->n_units);
+    G.nb = static_cast<int>(k->logical_blocks);
+    G.B = static_cast<int>(k->block_size);
+    G.d = static_cast<int>(k->head_dim);
+    G.gqa = static_cast<int>(gqa);
+    G.n_q = static_cast<int>(n_q);
+    G.tail = static_cast<int>(tail);
+    G.causal = causal;
+    G.scale = scale;
+    G.q = q;
+    G.k_index = k->index_map;
+    G.v_index = v->index_map;
+    G.k_dense_count = static_cast<int>(k->dense_count);
+    G.k_sparse_count = static_cast<int>(k->sparse_count);
+    G.v_dense_count = static_cast<int>(v->dense_count);
+    G.v_sparse_count = static_cast<int>(v->sparse_count);
+    G.k_dense = k->dense_pool;
+    G.k_nnz = k->nnz_pool;
+    G.k_meta = k->meta_pool;
+    G.v_dense = v->dense_pool;
+    G.v_nnz = v->nnz_pool;
+    G.v_meta = v->meta_pool;
+    G.k_tail = k_tail;
+    G.v_tail = v_tail;
+    G.block_begin = static_cast<int>(block_begin);
+    G.block_end = static_cast<int>(block_end);
+    G.include_tail = include_tail;
+    G.out = out;
+    G.out_mode = out_mode;
+    cudaError_t e = hs::launch_generic_attention(G, s);
+    count_launch();
+    if (e != cudaSuccess) return cuda_fail(e, "generic attention launch");
+    return HS_OK;
+}
+
+static hs_status decode_common_rows(const void* q, const hs_device_cache* k, const hs_device_cache* v,
+                                    const void* k_tail, const void* v_tail, uint32_t tail, uint32_t gqa,
+                                    uint32_t q_rows, uint32_t row0, float scale, uint32_t splits,
+                                    uint32_t block_begin, uint32_t block_end, int include_tail, float* out,
+                                    int out_mode, void* user_ws, uint64_t user_ws_bytes, cudaStream_t s);
+
 static hs_status decode_common(const void* q, const hs_device_cache* k, const hs_device_cache* v,
                                const void* k_tail, const void* v_tail, uint32_t tail, uint32_t gqa,
                                float scale, uint32_t splits, uint32_t block_begin, uint32_t block_end,
@@ -553,18 +614,44 @@ static hs_status decode_common(const void* q, const hs_device_cache* k, const hs
     if (st) return st;
     HS_CHECK_CONFIG(q != nullptr && out != nullptr, "decode_attention: null argument");
     HS_CHECK_CONFIG(gqa >= 1, "decode_attention: no query rows");
-    HS_CHECK_CONFIG(gqa <= 8, "decode_attention: device kernel supports up to 8 query rows per KV head");
     HS_CHECK_CONFIG(tail == 0 || (k_tail && v_tail), "decode_attention: null dense tail");
     HS_CHECK_CONFIG(static_cast<uint64_t>(k->logical_blocks) * k->block_size + tail > 0,
                     "decode_attention: empty cache");
     HS_CHECK_CONFIG(block_begin <= block_end && block_end <= k->logical_blocks,
                     "attend_range: block range out of bounds");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!specialised(k))
+        return generic_attention(q, 1, gqa, k, v, k_tail, v_tail, tail, 0, scale, block_begin, block_end, include_tail,
+                                 out, out_mode, s);
+    if (gqa > 8) {
+        // The mma.sp decode stacks up to 8 query rows on N: larger GQA groups run
+        // as chunks of 8 rows (q / out strides stay the group's).
+        for (uint32_t r0 = 0; r0 < gqa; r0 += 8) {
+            const uint32_t n = gqa - r0 < 8 ? gqa - r0 : 8;
+            hs_status st2 = decode_common_rows(q, k, v, k_tail, v_tail, tail, n, gqa, r0, scale, splits, block_begin,
+                                               block_end, include_tail, out, out_mode, user_ws, user_ws_bytes, s);
+            if (st2) return st2;
+        }
+        return HS_OK;
+    }
+    return decode_common_rows(q, k, v, k_tail, v_tail, tail, gqa, gqa, 0, scale, splits, block_begin, block_end,
+                              include_tail, out, out_mode, user_ws, user_ws_bytes, s);
+}
+
+static hs_status decode_common_rows(const void* q, const hs_device_cache* k, const hs_device_cache* v,
+                                    const void* k_tail, const void* v_tail, uint32_t tail, uint32_t gqa,
+                                    uint32_t q_rows, uint32_t row0, float scale, uint32_t splits,
+                                    uint32_t block_begin, uint32_t block_end, int include_tail, float* out,
+                                    int out_mode, void* user_ws, uint64_t user_ws_bytes, cudaStream_t s) {
+    hs_status st = HS_OK;
+    q = static_cast<const uint16_t*>(q) + static_cast<size_t>(row0) * hs::kHeadDim;
+    out += static_cast<size_t>(row0) * (out_mode == 0 ? hs::kHeadDim : hs::kHeadDim + 2);
     hs::DecodeLaunch L{};
     L.bf16 = k->dtype == HS_DTYPE_BF16;
     L.n_units = k->n_units;
     L.nb = k->logical_blocks;
     L.gqa = gqa;
+    L.q_rows = q_rows;
     L.tail = tail;
     L.k_dense_count = k->dense_count;
     L.k_sparse_count = k->sparse_count;
@@ -664,7 +751,7 @@ HS_API hs_status hs_decode_workspace_bytes(const hs_device_cache* k, uint32_t gq
     HS_CHECK_CONFIG(k != nullptr && bytes != nullptr, "decode_attention: null argument");
     int ns;
     size_t cnt, part;
-    decode_geometry(k->n_units, k->logical_blocks, gqa, splits, &ns, &cnt, &part);
+    decode_geometry(k->n_units, k->logical_blocks, gqa < 8 ? gqa : 8, splits, &ns, &cnt, &part);
     *bytes = cnt + part;
     return HS_OK;
 }
@@ -708,11 +795,14 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     HS_CHECK_CONFIG(n_kv > 0, "prefill_attention: empty key/value cache");
     HS_CHECK_CONFIG(!causal || n_kv >= n_q, "prefill_attention: causal queries exceed key sequence");
     HS_CHECK_CONFIG(tail == 0 || (k_tail != nullptr && v_tail != nullptr), "prefill_attention: null dense tail");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!specialised(k))
+        return generic_attention(q, n_q, gqa, k, v, k_tail, v_tail, tail, causal, scale, 0, k->logical_blocks, 1, out,
+                                 0, s);
     HS_CHECK_CONFIG(k->logical_blocks / 2 + 8 <= 4096,
                     "prefill_attention: %u blocks exceed the kernel's key-tile list (max 8184 blocks)",
                     k->logical_blocks);
     HS_CHECK_CONFIG(k->logical_blocks == 0 || k->slot_block != nullptr, "prefill_attention: key cache needs slot_block");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     hs::PrefillLaunch L{};
     L.bf16 = k->dtype == HS_DTYPE_BF16;
     L.n_units = k->n_units;

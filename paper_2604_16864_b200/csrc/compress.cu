@@ -200,6 +200,7 @@ struct PackArgs {
     unsigned long long* status; // SRC 1: decompress's DataErrors (status word, kernels.h reasons)
     const uint8_t* element_mask;  // mask_pack_kernel: explicit ElementMask u8 [u][rows][d]
     uint64_t mask_unit_stride;
+    int B, d;                     // block size and head dim (generic-shape kernels)
 };
 
 // One stored 2:4 group (kept pair word, 4-bit code) back to its four logical
@@ -653,6 +654,191 @@ __global__ void __launch_bounds__(kThreads) decompress_kernel(const int16_t* ind
     if (bad) record_status(status, key, kReasonCodesOrder);
 }
 
+// ---------------------------------------------------------------------------
+// Generic shapes (any block_size B and head_dim d that are multiples of 4, the
+// reference's own constraints: masks.hpp:87, pruner.hpp:172-173,
+// compressed_cache.hpp:118-126).  Same contracts as block_kernel /
+// mask_pack_kernel / decompress_kernel (bit-exact pools, losses and errors),
+// written over the canonical storage order instead of the B = 64 / d = 128
+// register tiling: one CTA per (block, unit); a thread owns whole metadata
+// words (4 consecutive groups in stored order), so every word is written once.
+// ---------------------------------------------------------------------------
+template <int AXIS>
+__device__ __forceinline__ void stored_to_logical(int sr, int sc, int& r, int& c) {
+    r = AXIS == 0 ? sr : sc;
+    c = AXIS == 0 ? sc : sr;
+}
+
+// Logical element (r, c) of input block b (decompress semantics) for any shape;
+// validity of the entry is checked by the caller.
+template <int AXIS>
+__device__ uint16_t gen_logical_in(const PackArgs& a, int u, int e, int r, int c, bool& bad) {
+    const int B = a.B, d = a.d, BE = B * d;
+    const int slot = (e > 0 ? e : -e) - 1;
+    const int scols = AXIS == 0 ? d : B;
+    const int sr = AXIS == 0 ? r : c, sc = AXIS == 0 ? c : r;
+    if (e > 0) return a.in_dense[(static_cast<uint64_t>(u) * a.in_dense_count + slot) * BE + sr * scols + sc];
+    const uint64_t sb = static_cast<uint64_t>(u) * a.in_sparse_count + slot;
+    const int gi = sr * (scols / 4) + (sc >> 2), pos = sc & 3;
+    const uint32_t code = (a.in_meta[sb * (BE / 16) + (gi >> 2)] >> (4 * (gi & 3))) & 0xFu;
+    const int p0 = code & 3, p1 = code >> 2;
+    bad |= p1 <= p0;
+    const uint16_t* nnz = a.in_nnz + sb * (BE / 2);
+    return pos == p0 ? nnz[2 * gi] : (pos == p1 ? nnz[2 * gi + 1] : static_cast<uint16_t>(0));
+}
+
+template <typename T, int AXIS, int MODE, int SRC, bool MASK>
+__global__ void __launch_bounds__(kThreads) gen_block_kernel(PackArgs a) {
+    const int b = blockIdx.x, u = blockIdx.y, t = threadIdx.x;
+    const int B = a.B, d = a.d, BE = B * d;
+    const int scols = AXIS == 0 ? d : B, gpr = scols / 4, G = BE / 4;
+    const bool from_src = SRC == 0 || b >= a.in_nb;
+    const uint16_t* blk = from_src ? unit_src(a.src, a.src_stride, u) +
+                                         static_cast<uint64_t>(b - (SRC == 0 ? 0 : a.in_nb)) * BE
+                                   : nullptr;
+    __shared__ double s_sum[kThreads / 32];
+    __shared__ int s_min[kThreads / 32];
+    const uint64_t bkey = static_cast<uint64_t>(u) * a.nb + b;
+    int in_e = 0;
+    bool in_bad = false;
+    if (SRC == 1 && !from_src) {
+        in_e = a.in_index[static_cast<int64_t>(u) * a.in_nb + b];
+        const int slot = (in_e > 0 ? in_e : -in_e) - 1;
+        if (in_e == 0 || (in_e > 0 && slot >= a.in_dense_count) || (in_e < 0 && slot >= a.in_sparse_count)) {
+            if (t == 0)
+                record_status(a.status, bkey,
+                              in_e == 0 ? kReasonZeroEntry : in_e > 0 ? kReasonDanglingDense : kReasonDanglingSparse);
+            in_e = 0;
+        }
+    }
+    auto logical = [&](int r, int c) -> uint16_t {
+        if (from_src) return blk[r * d + c];
+        if (in_e == 0) return 0;
+        return gen_logical_in<AXIS>(a, u, in_e, r, c, in_bad);
+    };
+    bool dense = false;
+    int slot = 0;
+    if (MODE != 0) {
+        const int e = a.index_map[static_cast<int64_t>(u) * a.nb + b];
+        dense = e > 0;
+        slot = (e > 0 ? e : -e) - 1;
+        if (e == 0 || slot >= (dense ? a.dense_count : a.sparse_count)) return;
+    }
+    constexpr bool kLoss = MODE != 1 && !MASK;
+    LossAcc acc;
+    if (MODE != 0 && dense) {
+        uint16_t* dst = a.dense_pool + (static_cast<uint64_t>(u) * a.dense_count + slot) * BE;
+        for (int i = t; i < BE; i += kThreads) {
+            int r, c;
+            stored_to_logical<AXIS>(i / scols, i % scols, r, c);
+            dst[i] = logical(r, c);
+        }
+    }
+    if (kLoss || (MODE != 0 && !dense)) {
+        const uint64_t sbk = static_cast<uint64_t>(u) * a.sparse_count + slot;
+        const uint8_t* mblk = MASK ? a.element_mask + static_cast<uint64_t>(u) * a.mask_unit_stride +
+                                         static_cast<uint64_t>(b) * BE
+                                   : nullptr;
+        for (int w = t; w < G / 4; w += kThreads) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int gi = 4 * w + q, sr = gi / gpr, g = gi % gpr;
+                uint32_t v[4], m = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    int r, c;
+                    stored_to_logical<AXIS>(sr, 4 * g + i, r, c);
+                    v[i] = logical(r, c);
+                    if (MASK) m |= static_cast<uint32_t>(mblk[r * d + c] != 0) << i;
+                }
+                const uint32_t lo = v[0] | (v[1] << 16), hi = v[2] | (v[3] << 16);
+                uint32_t code, kept;
+                if (MASK) {
+                    const int n = __popc(m);
+                    if (n != 2) {
+                        record_status(a.status, bkey * G + gi, n > 2 ? kReasonKeepsMore : kReasonKeepsFewer);
+                        code = kept = 0u;
+                    } else {
+                        const uint32_t p0 = __ffs(m) - 1, p1 = __ffs(m & (m - 1)) - 1;
+                        kept = __byte_perm(lo, hi, 0x1010u + p0 * 0x22u + p1 * 0x2200u);
+                        code = p0 | (p1 << 2);
+                    }
+                } else {
+                    const Sel2of4 sel = select2of4(lo, hi);
+                    code = sel.code;
+                    kept = sel.kept;
+                    if (kLoss) loss_add_pair<T>(acc, sel.pr_lo, sel.pr_hi);
+                }
+                word |= code << (4 * q);
+                if (MODE != 0 && !dense)
+                    *reinterpret_cast<uint32_t*>(a.nnz_pool + sbk * (BE / 2) + 2 * gi) = kept;
+            }
+            if (MODE != 0 && !dense) a.meta_pool[sbk * (BE / 16) + w] = static_cast<uint16_t>(word);
+        }
+    }
+    if (SRC == 1 && in_bad) record_status(a.status, bkey, kReasonCodesOrder);
+    if (kLoss) {
+        const bool exact = loss_reduce<T>(acc, s_sum, s_min, nullptr);
+        if (t == 0) {
+            double loss = acc.sum;
+            if (!exact) {
+                // block_loss (pruner.hpp:81-89) in logical row-major order
+                loss = 0.0;
+                bool dummy = false;
+                for (int r = 0; r < B; ++r)
+                    for (int c = 0; c < d; ++c) {
+                        uint32_t m[4];
+                        const int r0 = AXIS == 0 ? r : (r & ~3), c0 = AXIS == 0 ? (c & ~3) : c;
+                        for (int i = 0; i < 4; ++i)
+                            m[i] = mag16(AXIS == 0 ? logical(r0, c0 + i) : logical(r0 + i, c0));
+                        const int pos = AXIS == 0 ? (c & 3) : (r & 3);
+                        if (!((keep_mask4(m[0], m[1], m[2], m[3]) >> pos) & 1u))
+                            loss += fabs(static_cast<double>(F16Traits<T>::to_float(logical(r, c))));
+                    }
+                (void)dummy;
+            }
+            a.losses[static_cast<int64_t>(u) * a.nb + b] = loss;
+        }
+    }
+}
+
+template <int AXIS>
+__global__ void __launch_bounds__(kThreads) gen_decompress_kernel(DecompressLaunch L, int B, int d) {
+    const int b = blockIdx.x, u = blockIdx.y, t = threadIdx.x;
+    const int BE = B * d, scols = AXIS == 0 ? d : B;
+    const int e = L.index_map[static_cast<int64_t>(u) * L.nb + b];
+    const int slot = (e > 0 ? e : -e) - 1;
+    const uint64_t key = static_cast<uint64_t>(u) * L.nb + b;
+    if (e == 0 || (e > 0 && slot >= L.dense_count) || (e < 0 && slot >= L.sparse_count)) {
+        if (t == 0)
+            record_status(L.status, key, e == 0 ? kReasonZeroEntry : e > 0 ? kReasonDanglingDense : kReasonDanglingSparse);
+        return;
+    }
+    const uint16_t* dense = static_cast<const uint16_t*>(L.dense_pool);
+    const uint16_t* nnzp = static_cast<const uint16_t*>(L.nnz_pool);
+    uint16_t* out = static_cast<uint16_t*>(L.dst) + (static_cast<uint64_t>(u) * L.nb + b) * BE;
+    bool bad = false;
+    for (int i = t; i < BE; i += kThreads) {
+        const int lr = i / d, lc = i % d;
+        const int sr = AXIS == 0 ? lr : lc, sc = AXIS == 0 ? lc : lr;
+        uint16_t v;
+        if (e > 0) {
+            v = dense[(static_cast<uint64_t>(u) * L.dense_count + slot) * BE + sr * scols + sc];
+        } else {
+            const uint64_t sb = static_cast<uint64_t>(u) * L.sparse_count + slot;
+            const int gi = sr * (scols / 4) + (sc >> 2), pos = sc & 3;
+            const uint32_t code = (L.meta_pool[sb * (BE / 16) + (gi >> 2)] >> (4 * (gi & 3))) & 0xFu;
+            const int p0 = code & 3, p1 = code >> 2;
+            bad |= p1 <= p0;
+            const uint16_t* nnz = nnzp + sb * (BE / 2);
+            v = pos == p0 ? nnz[2 * gi] : (pos == p1 ? nnz[2 * gi + 1] : static_cast<uint16_t>(0));
+        }
+        out[i] = v;
+    }
+    if (bad) record_status(L.status, key, kReasonCodesOrder);
+}
+
 }  // namespace
 
 // ----------------------------------------------------------------- launchers
@@ -667,9 +853,26 @@ static void launch_block_kernel_src(int axis, int mode, const PackArgs& a, int n
     }
 #undef HS_LAUNCH
 }
+template <typename T, int SRC, bool MASK>
+static void launch_gen_src(int axis, int mode, const PackArgs& a, int n_units, cudaStream_t s) {
+    const dim3 grid(a.nb, n_units);
+#define HS_LAUNCH(AX, MD) gen_block_kernel<T, AX, MD, SRC, MASK><<<grid, kThreads, 0, s>>>(a)
+    if (axis == 0) {
+        if (mode == 0) HS_LAUNCH(0, 0); else if (mode == 1) HS_LAUNCH(0, 1); else HS_LAUNCH(0, 2);
+    } else {
+        if (mode == 0) HS_LAUNCH(1, 0); else if (mode == 1) HS_LAUNCH(1, 1); else HS_LAUNCH(1, 2);
+    }
+#undef HS_LAUNCH
+}
 template <typename T>
 static cudaError_t launch_block_kernel(int axis, int mode, const PackArgs& a, int n_units,
                                        cudaStream_t s) {
+    if (a.B != kBlock || a.d != kHeadDim) {  // generic shapes
+        if (a.element_mask) launch_gen_src<T, 0, true>(axis, 1, a, n_units, s);
+        else if (a.in_index) launch_gen_src<T, 1, false>(axis, mode, a, n_units, s);
+        else launch_gen_src<T, 0, false>(axis, mode, a, n_units, s);
+        return cudaGetLastError();
+    }
     if (a.in_index) launch_block_kernel_src<T, 1>(axis, mode, a, n_units, s);
     else launch_block_kernel_src<T, 0>(axis, mode, a, n_units, s);
     return cudaGetLastError();
@@ -695,6 +898,10 @@ cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
     a.in_nnz = static_cast<const uint16_t*>(L.in_nnz);
     a.in_meta = L.in_meta;
     a.status = L.status;
+    a.element_mask = nullptr;
+    a.mask_unit_stride = 0;
+    a.B = L.block_size;
+    a.d = L.head_dim;
     auto blocks = [&](int mode) {
         return L.bf16 ? launch_block_kernel<__nv_bfloat16>(L.axis, mode, a, L.n_units, s)
                       : launch_block_kernel<__half>(L.axis, mode, a, L.n_units, s);
@@ -709,6 +916,7 @@ cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
         if (L.element_mask) {
             a.element_mask = L.element_mask;
             a.mask_unit_stride = L.mask_unit_stride;
+            if (a.B != kBlock || a.d != kHeadDim) return blocks(1);
             if (L.axis == 0) mask_pack_kernel<0><<<dim3(L.nb, L.n_units), kThreads, 0, s>>>(a);
             else mask_pack_kernel<1><<<dim3(L.nb, L.n_units), kThreads, 0, s>>>(a);
             return cudaGetLastError();
@@ -735,6 +943,11 @@ cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
 
 cudaError_t launch_decompress(const DecompressLaunch& L, cudaStream_t s) {
     const dim3 grid(L.nb, L.n_units);
+    if (L.block_size != kBlock || L.head_dim != kHeadDim) {
+        if (L.axis == 0) gen_decompress_kernel<0><<<grid, kThreads, 0, s>>>(L, L.block_size, L.head_dim);
+        else gen_decompress_kernel<1><<<grid, kThreads, 0, s>>>(L, L.block_size, L.head_dim);
+        return cudaGetLastError();
+    }
     if (L.axis == 0)
         decompress_kernel<0><<<grid, kThreads, 0, s>>>(L.index_map, L.nb, L.dense_count, L.sparse_count,
                                                        static_cast<const uint16_t*>(L.dense_pool),

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
 
     {
         // Q^T fragments for GEMM1 (B operand, k = channel, n = query row g).
-        const T* q = static_cast<const T*>(L.q) + static_cast<int64_t>(u) * gqa * kHeadDim;
+        const T* q = static_cast<const T*>(L.q) + static_cast<int64_t>(u) * L.q_rows * kHeadDim;
         uint32_t qb[4][4];
 #pragma unroll
         for (int j = 0; j < 4; ++j)
@@ -510,9 +510,9 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
             M = mc;
         }
         if (L.out_mode == 0) {
-            L.out[(static_cast<int64_t>(u) * gqa + qq) * kHeadDim + c] = acc / lsum;
+            L.out[(static_cast<int64_t>(u) * L.q_rows + qq) * kHeadDim + c] = acc / lsum;
         } else {
-            float* po = L.out + (static_cast<int64_t>(u) * gqa + qq) * (kHeadDim + 2);
+            float* po = L.out + (static_cast<int64_t>(u) * L.q_rows + qq) * (kHeadDim + 2);
             po[c] = acc;
             if (c == 0) {
                 po[kHeadDim] = M;

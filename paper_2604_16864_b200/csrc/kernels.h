@@ -26,6 +26,7 @@ enum StatusReason : uint32_t {
 struct CompressLaunch {
     bool bf16;
     int axis;
+    int block_size = kBlock, head_dim = kHeadDim;  // != (64, 128): generic-shape kernels
     int n_units;
     int nb;
     int dense_count, sparse_count;
@@ -64,6 +65,7 @@ struct DecompressLaunch {
     const uint16_t* meta_pool;
     void* dst;
     unsigned long long* status;
+    int block_size = kBlock, head_dim = kHeadDim;
 };
 cudaError_t launch_decompress(const DecompressLaunch& L, cudaStream_t s);
 
@@ -71,9 +73,10 @@ cudaError_t launch_decompress(const DecompressLaunch& L, cudaStream_t s);
 struct DecodeLaunch {
     bool bf16;
     int n_units, nb, gqa, tail;
+    int q_rows;              // rows per unit of q / out in memory (>= gqa: GQA groups above 8 run in chunks)
     int k_dense_count, k_sparse_count, v_dense_count, v_sparse_count;
     float scale_log2;        // scale * log2(e)
-    const void* q;           // [u][gqa][d]
+    const void* q;           // [u][q_rows][d], this launch's rows first
     const int16_t* k_index;  // [u][nb]
     const int16_t* v_index;
     const uint16_t* k_meta;  // [u][sparse][512]
@@ -136,5 +139,32 @@ struct PrefillLaunch {
     CUtensorMap tm_q, tm_knnz, tm_kden, tm_vnnz, tm_vden, tm_ktail, tm_vtail, tm_vnnz2, tm_vden2;
 };
 cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s);
+
+// Attention for shapes outside the tcgen05 / mma.sp kernels' specialisation
+// (block_size != 64 or head_dim != 128): attend_range (attention.hpp:249-304)
+// per query row on CUDA cores, one warp per row, expanding 2:4 blocks from their
+// canonical metadata on the fly.  Decode, prefill (causal or not) and partials.
+struct GenericAttnLaunch {
+    bool bf16;
+    int n_units, nb, B, d, gqa, n_q, tail, causal;
+    float scale;
+    const void* q;           // [u][gqa][n_q][d]
+    const int16_t* k_index;
+    const int16_t* v_index;
+    int k_dense_count, k_sparse_count, v_dense_count, v_sparse_count;
+    const void* k_dense;
+    const void* k_nnz;
+    const uint16_t* k_meta;
+    const void* v_dense;
+    const void* v_nnz;
+    const uint16_t* v_meta;
+    const void* k_tail;      // [u][tail][d]
+    const void* v_tail;
+    int block_begin, block_end, include_tail;
+    float* out;              // out_mode 0: [u][gqa][n_q][d]; 1: SplitPartial [u][gqa][n_q][d + 2] (O, m, l)
+    int out_mode;
+};
+cudaError_t launch_generic_attention(const GenericAttnLaunch& L, cudaStream_t s);
+constexpr int kGenericMaxHeadDim = 512;
 
 }  // namespace hs

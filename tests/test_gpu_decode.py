@@ -122,7 +122,21 @@ def test_decode_rejects_invalid(hs, port):
     with pytest.raises(ConfigError):
         hs.decode_attention(q, vc, kc)          # swapped caches (test_attention.cpp:392-395)
     with pytest.raises(ConfigError):
-        hs.decode_attention(q.repeat(1, 3, 1), kc, vc)  # 12 rows > 8
+        hs.decode_attention(q[:, :, :64].contiguous(), kc, vc)  # head_dim mismatch
+
+
+def test_decode_gqa_above_eight_rows(hs, port):
+    """GQA groups above the mma.sp kernel's 8 stacked rows run in row chunks with
+    the group's strides: 12 and 16 rows against the oracle."""
+    U, L = 2, 4096
+    kx, vx, kc, vc = build_caches(hs, port, U, L, 0.5, "bf16", seed=6)
+    scale = np.float32(1.0 / math.sqrt(128))
+    for gqa in (12, 16):
+        q = decode_queries(port, U, gqa, "bf16", seed=6)
+        got = hs.decode_attention(to_torch(q, "bf16"), kc, vc, scale=float(scale)).cpu().numpy()
+        want = oracle_decode(port, kc, vc, q, scale, 1)
+        mx, mr = err_stats(got, want)
+        assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (gqa, mx, mr)
 
 
 def test_decode_fixed_splits_deterministic(hs, port):

@@ -361,3 +361,29 @@ def test_compress_with_mask_rejects_bad_groups(port, ref, kept, msg):
     # the same group in a dense block is never consulted
     for o in (port, ref):
         o.compress_with_mask(x, SparsityConfig(block_size=4), 0, em, [0, 1, 0, 0])
+
+
+def test_port_matches_small_shape_reference_fixtures(port):
+    """The port at the reference's general (B, d) shapes reproduces the fixtures the
+    compiled reference wrote (tests/golden/make_small_shapes.py)."""
+    from oracle.oracle import SparsityConfig as OCfg
+    g = np.load(os.path.join(os.path.dirname(GOLD), "small_shapes.npz"))
+    f32 = lambda b: (b.astype(np.uint32) << 16).view(np.float32)  # noqa: E731
+    for name in g["names"]:
+        name = str(name)
+        L, tail, d, B, gqa, n_q, sink, window = (int(x) for x in g[name + "_shape"])
+        s = float(g[name + "_s"][0])
+        key = f32(g[name + "_key"]).reshape(L + tail, d)
+        val = f32(g[name + "_val"]).reshape(L + tail, d)
+        cfg = OCfg(s, s, B, sink, window)
+        kc = port.prune_compress(key[:L], cfg, 0, s)
+        vc = port.prune_compress(val[:L], cfg, 1, s)
+        for c, p in ((kc, name + "_k"), (vc, name + "_v")):
+            assert (c.index_map == g[p + "_index_map"]).all(), name
+            assert c.losses.tobytes() == g[p + "_losses"].tobytes(), name
+            if c.sparse_count:
+                assert (c.meta_pool == g[p + "_meta_pool"]).all(), name
+        kt, vt = (key[L:], val[L:]) if tail else (None, None)
+        scale = np.float32(1.0 / np.sqrt(d))
+        out = port.decode(g[name + "_decode_q"], kc, vc, kt, vt, scale, 2)
+        assert np.abs(out - g[name + "_decode_out"]).max() < 1e-5, name
