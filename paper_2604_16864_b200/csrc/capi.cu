@@ -257,6 +257,7 @@ hs_status check_pair(const hs_device_cache* k, const hs_device_cache* v) {
     HS_CHECK_CONFIG(v->axis == HS_AXIS_SEQUENCE, "attention: value cache must be sequence-grouped");
     HS_CHECK_CONFIG(k->logical_blocks == v->logical_blocks, "attention: key/value block counts differ");
     HS_CHECK_CONFIG(k->block_size == v->block_size, "attention: key/value block sizes differ");
+    HS_CHECK_CONFIG(k->head_dim == v->head_dim, "attention: key/value head dims differ");
     HS_CHECK_CONFIG(k->n_units == v->n_units, "attention: key/value unit counts differ");
     HS_CHECK_CONFIG(k->dtype == v->dtype, "attention: key/value dtypes differ");
     return HS_OK;

@@ -87,12 +87,16 @@ def test_attention_argument_validation_without_gpu(lib):
     with pytest.raises(ConfigError, match="channel-grouped"):
         capi.check(rc)
     k.axis = 0
-    rc = lib.hs_decode(1, C.byref(k), C.byref(v), None, None, 0, 9, 0.1, 0, 1, None)
-    with pytest.raises(ConfigError):
+    rc = lib.hs_decode(1, C.byref(k), C.byref(v), None, None, 0, 0, 0.1, 0, 1, None)
+    with pytest.raises(ConfigError, match="no query rows"):
         capi.check(rc)
-    bad = capi.DeviceCacheC(0, 0, 64, 64, 1, 4, 0, 4, 1, None, 1, 1, None)  # head_dim 64
+    bad = capi.DeviceCacheC(0, 0, 64, 64, 1, 4, 0, 4, 1, None, 1, 1, None)  # head_dim 64 vs 128
     rc = lib.hs_decode(1, C.byref(bad), C.byref(v), None, None, 0, 4, 0.1, 0, 1, None)
-    with pytest.raises(ConfigError, match="head_dim"):
+    with pytest.raises(ConfigError, match="head dims differ"):
+        capi.check(rc)
+    odd = capi.DeviceCacheC(0, 0, 130, 64, 1, 4, 0, 4, 1, None, 1, 1, None)  # d not a multiple of 4
+    rc = lib.hs_decode(1, C.byref(odd), C.byref(v), None, None, 0, 4, 0.1, 0, 1, None)
+    with pytest.raises(ConfigError, match="m_group"):
         capi.check(rc)
 
 
