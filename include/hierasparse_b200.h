@@ -74,6 +74,11 @@ typedef struct {
  *   dense_pool dtype [n_units][dense_count][B*d] K: [B][d], V: [d][B] (transposed)
  *   nnz_pool   dtype [n_units][sparse_count][B*d/2] kept values, ascending position
  *   meta_pool  u16   [n_units][sparse_count][B*d/16] 2-bit codes, 8 per word (nm_metadata.hpp:42-46)
+ * dense_count / sparse_count are the pool slots per unit.  Caches built by
+ * hs_prune_compress have exactly logical_blocks slots; caches whose units
+ * differ in their dense counts (hs_compress_with_flags over a shard of a
+ * globally selected sequence) may hold spare slots, which only the decode
+ * entry points accept.
  * slot_block is derived (not part of the reference format): per unit, the
  * logical block of every pool slot, dense slots first then sparse slots
  * (int32 [n_units][logical_blocks]); the prefill kernel groups blocks by kind
@@ -145,9 +150,24 @@ HS_API hs_status hs_prune_compress(const void* src, uint64_t src_unit_stride, ui
                                    hs_device_cache* out, double* losses, uint8_t* flags,
                                    void* stream);
 
+/* The two halves of hierarchical_mask_for for sequence-split pruning, where
+ * the block selection is global but every rank holds only its own blocks:
+ *   hs_block_losses: block_loss (pruner.hpp:81-89, FP64, bit-exact) of every
+ *     block of src (element masks by element_mask, :40-77); geometry supplies
+ *     dtype, axis, head_dim, block_size and n_units (pointers unused);
+ *     losses double [n_units][rows / block_size].
+ *   hs_select_blocks: select_blocks (pruner.hpp:94-117) over losses
+ *     [n_units][logical_blocks] with the protected-region rounding and clamping
+ *     of :127-131; flags u8 [n_units][logical_blocks], 1 = dense. */
+HS_API hs_status hs_block_losses(const void* src, uint64_t src_unit_stride, uint64_t rows,
+                                 const hs_device_cache* geometry, double* losses, void* stream);
+HS_API hs_status hs_select_blocks(const double* losses, uint32_t n_units, uint32_t logical_blocks,
+                                  const hs_sparsity_config* cfg, double sparsity, uint8_t* flags, void* stream);
+
 /* fused_magnitude_compress (compressed_cache.hpp:262-267) under a given
- * BlockMask: flags u8 [n_units][nb] device, 1 = dense.  out->dense_count and
- * sparse_count must equal the flag counts (checked on the device: status). */
+ * BlockMask: flags u8 [n_units][nb] device, 1 = dense.  Each unit's dense and
+ * sparse block counts must fit out->dense_count / sparse_count (equal them for
+ * an exact cache; checked on the device: status). */
 HS_API hs_status hs_compress_with_flags(const void* src, uint64_t src_unit_stride, uint64_t rows,
                                         const uint8_t* flags, hs_device_cache* out, uint64_t* status,
                                         void* stream);

@@ -34,7 +34,7 @@ class DeviceCacheC(C.Structure):
 
 # Exported symbols (every one declared in include/hierasparse_b200.h).
 EXPORTS = ("hs_last_error", "hs_version", "hs_status_word_decode", "hs_pool_counts", "hs_cache_bytes",
-           "hs_prune_compress", "hs_compress_with_flags", "hs_compress_with_mask", "hs_decompress", "hs_recompress",
+           "hs_prune_compress", "hs_block_losses", "hs_select_blocks", "hs_compress_with_flags", "hs_compress_with_mask", "hs_decompress", "hs_recompress",
            "hs_absorb_tail", "hs_decode", "hs_decode_workspace_bytes", "hs_decode_ws", "hs_decode_partial",
            "hs_decode_combine", "hs_prefill", "hs_kernel_launches")
 
@@ -59,6 +59,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hs_cache_bytes": [P(DeviceCacheC), P(u64), P(u64), P(u64), P(u64), P(u64)],
         "hs_prune_compress": [vp, u64, u64, P(SparsityConfigC), C.c_double, P(DeviceCacheC), vp, vp, vp],
         "hs_status_word_decode": [u64],
+        "hs_block_losses": [vp, u64, u64, P(DeviceCacheC), vp, vp],
+        "hs_select_blocks": [vp, u32, u32, P(SparsityConfigC), C.c_double, vp, vp],
         "hs_compress_with_flags": [vp, u64, u64, vp, P(DeviceCacheC), vp, vp],
         "hs_compress_with_mask": [vp, u64, u64, vp, u64, vp, P(DeviceCacheC), vp, vp],
         "hs_decompress": [P(DeviceCacheC), vp, vp, vp],

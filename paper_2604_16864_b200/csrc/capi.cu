@@ -239,7 +239,10 @@ hs_status check_device_cache(const hs_device_cache* c, const char* what) {
                     "%s: block_size must be a positive multiple of m_group", what);
     HS_CHECK_CONFIG(c->head_dim >= 4 && c->head_dim % 4 == 0, "%s: head dimension not divisible by m_group", what);
     HS_CHECK_CONFIG(c->n_units >= 1, "%s: n_units must be positive", what);
-    HS_CHECK_CONFIG(c->dense_count + c->sparse_count == c->logical_blocks,
+    // dense_count / sparse_count are the pool slots per unit: exactly the block
+    // count for caches from hs_prune_compress, possibly more for pooled caches
+    // whose units differ in their dense counts (sequence-split shards).
+    HS_CHECK_CONFIG(c->dense_count + c->sparse_count >= c->logical_blocks,
                     "%s: pool counts do not cover the block map", what);
     HS_CHECK_CONFIG(c->dense_count <= 32767 && c->sparse_count <= 32767,
                     "%s: pool exceeds int16 index capacity", what);
@@ -522,6 +525,49 @@ HS_API hs_status hs_decompress(const hs_device_cache* c, void* dst, uint64_t* st
     return HS_OK;
 }
 
+HS_API hs_status hs_block_losses(const void* src, uint64_t src_unit_stride, uint64_t rows,
+                                 const hs_device_cache* geometry, double* losses, void* stream) {
+    HS_CHECK_CONFIG(src != nullptr && geometry != nullptr && losses != nullptr, "block_loss: null argument");
+    const hs_device_cache* g = geometry;
+    HS_CHECK_CONFIG(g->dtype == HS_DTYPE_BF16 || g->dtype == HS_DTYPE_F16, "block_loss: unsupported dtype");
+    HS_CHECK_CONFIG(g->block_size >= 4 && g->block_size % 4 == 0,
+                    "SparsityConfig: block_size must be a positive multiple of m_group");
+    HS_CHECK_CONFIG(g->head_dim >= 4 && g->head_dim % 4 == 0, "prune_cache: head dimension not divisible by m_group");
+    HS_CHECK_CONFIG(rows % g->block_size == 0, "prune_cache: sequence length not divisible by block_size");
+    HS_CHECK_CONFIG(g->n_units == 1 || src_unit_stride >= rows * g->head_dim, "block_loss: unit stride too small");
+    hs::CompressLaunch L{};
+    L.bf16 = g->dtype == HS_DTYPE_BF16;
+    L.axis = g->axis;
+    L.block_size = static_cast<int>(g->block_size);
+    L.head_dim = static_cast<int>(g->head_dim);
+    L.n_units = static_cast<int>(g->n_units);
+    L.nb = static_cast<int>(rows / g->block_size);
+    L.src = src;
+    L.src_unit_stride = src_unit_stride;
+    L.losses = losses;
+    if (L.nb == 0) return HS_OK;
+    cudaError_t e = hs::launch_block_losses(L, static_cast<cudaStream_t>(stream));
+    count_launch();
+    if (e != cudaSuccess) return cuda_fail(e, "block_loss launch");
+    return HS_OK;
+}
+
+HS_API hs_status hs_select_blocks(const double* losses, uint32_t n_units, uint32_t logical_blocks,
+                                  const hs_sparsity_config* cfg, double sparsity, uint8_t* flags, void* stream) {
+    HS_CHECK_CONFIG(losses != nullptr && flags != nullptr, "select_blocks: null argument");
+    uint32_t nb, dc, sc, pre, suf, quota;
+    hs_status st = pool_counts(static_cast<uint64_t>(logical_blocks) * (cfg ? cfg->block_size : 0), cfg, sparsity,
+                               &nb, &dc, &sc, &pre, &suf, &quota);
+    if (st) return st;
+    if (nb == 0 || n_units == 0) return HS_OK;
+    cudaError_t e = hs::launch_select_blocks(losses, static_cast<int>(n_units), static_cast<int>(nb),
+                                             static_cast<int>(pre), static_cast<int>(suf), static_cast<int>(quota),
+                                             flags, static_cast<cudaStream_t>(stream));
+    count_launch();
+    if (e != cudaSuccess) return cuda_fail(e, "select_blocks launch");
+    return HS_OK;
+}
+
 HS_API hs_status hs_status_word_decode(uint64_t word) {
     if (word == 0) return HS_OK;
     switch (static_cast<uint32_t>(word & 0xFFu)) {
@@ -533,7 +579,7 @@ HS_API hs_status hs_status_word_decode(uint64_t word) {
         case hs::kReasonKeepsMore: return fail(HS_ERR_DATA, "compress: group keeps more than n_keep elements");
         case hs::kReasonKeepsFewer: return fail(HS_ERR_DATA, "compress: group keeps fewer than n_keep elements");
         case hs::kReasonMaskCount:
-            return fail(HS_ERR_CONFIG, "compress: block mask dense count differs from the cache's dense pool");
+            return fail(HS_ERR_CONFIG, "compress: block mask dense count does not fit the cache's pools");
         default: return fail(HS_ERR_DATA, "device status word 0x%llx", static_cast<unsigned long long>(word));
     }
 }
@@ -800,6 +846,9 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     if (!specialised(k))
         return generic_attention(q, n_q, gqa, k, v, k_tail, v_tail, tail, causal, scale, 0, k->logical_blocks, 1, out,
                                  0, s);
+    HS_CHECK_CONFIG(k->dense_count + k->sparse_count == k->logical_blocks &&
+                        v->dense_count + v->sparse_count == v->logical_blocks,
+                    "prefill_attention: caches with spare pool slots (per-unit counts) are decode-only");
     HS_CHECK_CONFIG(k->logical_blocks / 2 + 8 <= 4096,
                     "prefill_attention: %u blocks exceed the kernel's key-tile list (max 8184 blocks)",
                     k->logical_blocks);

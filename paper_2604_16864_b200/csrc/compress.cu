@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(1024) assign_slots_kernel(const uint8_t* flags
                                                             int prefix, int suffix, int all_sparse,
                                                             int dense_count, int16_t* index_map,
                                                             int32_t* slot_block, uint8_t* flags_out,
-                                                            unsigned long long* status) {
+                                                            unsigned long long* status, int sparse_capacity) {
     const int u = blockIdx.x, t = threadIdx.x;
     const int per = (nb + 1023) / 1024;
     const int b0 = min(nb, t * per), b1 = min(nb, b0 + per);
@@ -594,7 +594,9 @@ __global__ void __launch_bounds__(1024) assign_slots_kernel(const uint8_t* flags
     __syncthreads();
     int dense_before = x - nd + ((t >> 5) ? warp_sums[(t >> 5) - 1] : 0);
     int sparse_before = b0 - dense_before;
-    if (t == 0 && warp_sums[31] != dense_count) record_status(status, 0, kReasonMaskCount);
+    // pools hold dense_count dense and nb_capacity - dense_count sparse slots per unit
+    if (t == 0 && (warp_sums[31] > dense_count || nb - warp_sums[31] > sparse_capacity))
+        record_status(status, 0, kReasonMaskCount);
     int16_t* im = index_map + static_cast<int64_t>(u) * nb;
     int32_t* sb = slot_block ? slot_block + static_cast<int64_t>(u) * nb : nullptr;
     for (int b = b0; b < b1; ++b) {
@@ -605,7 +607,8 @@ __global__ void __launch_bounds__(1024) assign_slots_kernel(const uint8_t* flags
             ++dense_before;
         } else {
             im[b] = static_cast<int16_t>(-(sparse_before + 1));
-            if (sb && dense_count + sparse_before < nb) sb[dense_count + sparse_before] = b;
+            if (sb && dense_count + sparse_before < nb && sparse_before < sparse_capacity)
+                sb[dense_count + sparse_before] = b;
             ++sparse_before;
         }
         if (flags_out) flags_out[static_cast<int64_t>(u) * nb + b] = static_cast<uint8_t>(f);
@@ -911,7 +914,8 @@ cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
         // fused_magnitude_compress under an explicit BlockMask, or compress under
         // an explicit ElementMask + BlockMask (compressed_cache.hpp:196-225).
         assign_slots_kernel<<<L.n_units, 1024, 0, s>>>(L.flags_in, L.nb, 0, 0, 0, L.dense_count,
-                                                       L.index_map, L.slot_block, L.flags_out, L.status);
+                                                       L.index_map, L.slot_block, L.flags_out, L.status,
+                                                       L.sparse_count);
         if ((err = cudaGetLastError())) return err;
         if (L.element_mask) {
             a.element_mask = L.element_mask;
@@ -926,7 +930,7 @@ cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
     if (L.static_selection) {
         assign_slots_kernel<<<L.n_units, 1024, 0, s>>>(nullptr, L.nb, L.prefix, L.suffix,
                                                        L.all_sparse, L.dense_count, L.index_map,
-                                                       L.slot_block, L.flags_out, nullptr);
+                                                       L.slot_block, L.flags_out, nullptr, L.sparse_count);
         if ((err = cudaGetLastError())) return err;
         return blocks(L.losses ? 2 : 1);
     }
@@ -936,9 +940,31 @@ cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
                                                                      L.suffix, L.quota, L.flags_tmp);
     if ((err = cudaGetLastError())) return err;
     assign_slots_kernel<<<L.n_units, 1024, 0, s>>>(L.flags_tmp, L.nb, 0, 0, 0, L.dense_count,
-                                                   L.index_map, L.slot_block, L.flags_out, nullptr);
+                                                   L.index_map, L.slot_block, L.flags_out, nullptr,
+                                                   L.sparse_count);
     if ((err = cudaGetLastError())) return err;
     return blocks(1);
+}
+
+cudaError_t launch_select_blocks(const double* losses, int n_units, int nb, int prefix, int suffix, int quota,
+                                 uint8_t* flags, cudaStream_t s) {
+    rank_kernel<<<dim3((nb + 255) / 256, n_units), 256, 0, s>>>(losses, nb, prefix, suffix, quota, flags);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_block_losses(const CompressLaunch& L, cudaStream_t s) {
+    CompressLaunch M = L;
+    M.flags_in = nullptr;
+    M.static_selection = false;
+    PackArgs a{};
+    a.src = static_cast<const uint16_t*>(L.src);
+    a.src_stride = L.src_unit_stride;
+    a.nb = L.nb;
+    a.losses = L.losses;
+    a.B = L.block_size;
+    a.d = L.head_dim;
+    return L.bf16 ? launch_block_kernel<__nv_bfloat16>(L.axis, 0, a, L.n_units, s)
+                  : launch_block_kernel<__half>(L.axis, 0, a, L.n_units, s);
 }
 
 cudaError_t launch_decompress(const DecompressLaunch& L, cudaStream_t s) {

@@ -56,6 +56,11 @@ struct CompressLaunch {
     uint64_t mask_unit_stride;
 };
 cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s);
+// block_loss (pruner.hpp:81-89) of every block (classify pass only) and
+// select_blocks (pruner.hpp:94-117) over given losses (sequence-split pruning).
+cudaError_t launch_block_losses(const CompressLaunch& L, cudaStream_t s);
+cudaError_t launch_select_blocks(const double* losses, int n_units, int nb, int prefix, int suffix, int quota,
+                                 uint8_t* flags, cudaStream_t s);
 
 struct DecompressLaunch {
     int axis, n_units, nb, dense_count, sparse_count;

@@ -123,8 +123,14 @@ class DeviceCompressedCache:
                     size_nnz=self.sparse_count * (be // 2) * 2, size_e=self.sparse_count * (be // 16) * 2)
 
     def nbytes(self) -> int:
-        """Bytes a full traversal of every unit reads (pools + index map)."""
-        return self.n_units * sum(self.measure_size().values())
+        """Bytes a full traversal of every unit reads (pools + index map): the sum of
+        measure_size over units (per-unit counts when units differ)."""
+        counts = getattr(self, "unit_dense_counts", None)
+        if counts is None:
+            return self.n_units * sum(self.measure_size().values())
+        be = self.block_size * self.head_dim
+        return sum(self.logical_blocks * 2 + c * be * 2 + (self.logical_blocks - c) * (be // 2 + be // 8)
+                   for c in counts)
 
 
 class StatusWord:
@@ -189,11 +195,43 @@ def prune_cache(key: torch.Tensor, value: torch.Tensor, cfg: SparsityConfig):
             prune_compress(value, cfg, cfg.s_value, capi.AXIS_SEQUENCE))
 
 
+def block_losses(x: torch.Tensor, cfg: SparsityConfig, axis: int) -> torch.Tensor:
+    """block_loss (pruner.hpp:81-89) of every block of every unit (element masks of
+    element_mask, :40-77): float64 [units, blocks], bit-identical to the reference."""
+    x = _check_src(x)
+    U, rows, d = x.shape
+    geo = DeviceCompressedCache(x.dtype, axis, U, 0, 0, 0, x.device, d, cfg.block_size)
+    if rows % cfg.block_size:
+        raise ConfigError("prune_cache: sequence length not divisible by block_size")
+    losses = torch.empty((U, rows // cfg.block_size), dtype=torch.float64, device=x.device)
+    capi.check(capi.load().hs_block_losses(x.data_ptr(), _unit_stride(x), rows, geo.cref(), losses.data_ptr(),
+                                           _stream()))
+    return losses
+
+
+def select_blocks(losses: torch.Tensor, cfg: SparsityConfig, sparsity: float) -> torch.Tensor:
+    """select_blocks (pruner.hpp:94-117) with the protected prefix / suffix of
+    cfg (masks.hpp:93-98, pruner.hpp:127-131) over losses [units, blocks] on the
+    device: u8 flags [units, blocks], 1 = dense."""
+    if not losses.is_cuda or losses.dtype != torch.float64 or losses.dim() != 2:
+        raise ConfigError("select_blocks: losses must be a CUDA float64 [units, blocks] tensor")
+    losses = losses.contiguous()
+    U, nb = losses.shape
+    flags = torch.empty((U, nb), dtype=torch.uint8, device=losses.device)
+    cc = cfg.c()
+    capi.check(capi.load().hs_select_blocks(losses.data_ptr(), U, nb, C.byref(cc), sparsity, flags.data_ptr(),
+                                            _stream()))
+    return flags
+
+
 def fused_magnitude_compress(x: torch.Tensor, flags: torch.Tensor, cfg: SparsityConfig,
-                             axis: int, check: bool = True, status: StatusWord | None = None) -> DeviceCompressedCache:
+                             axis: int, check: bool = True, status: StatusWord | None = None,
+                             capacity: bool = False) -> DeviceCompressedCache:
     """fused_magnitude_compress (compressed_cache.hpp:262-267) under a given BlockMask
     (flags u8 [units, blocks], 1 = dense).  Every unit's dense count must equal
-    unit 0's (the pooled layout); a mismatch raises ConfigError (device-checked)."""
+    unit 0's (the pooled layout); a mismatch raises ConfigError (device-checked).
+    capacity=True sizes the pools for the largest unit instead (units may differ;
+    the result then serves decode only, per-unit counts in .unit_dense_counts)."""
     x = _check_src(x)
     U, rows, d = x.shape
     if rows % cfg.block_size:
@@ -202,8 +240,17 @@ def fused_magnitude_compress(x: torch.Tensor, flags: torch.Tensor, cfg: Sparsity
     nb = rows // cfg.block_size
     if flags.shape[1] != nb:
         raise ConfigError("compress: block mask does not cover the sequence")
-    dc = int((flags[0] != 0).sum().item()) if nb else 0
-    out = DeviceCompressedCache(x.dtype, axis, U, nb, dc, nb - dc, x.device, d, cfg.block_size, cfg)
+    if capacity:
+        # per-unit dense counts may differ (a shard of a globally selected
+        # sequence): pools sized for the largest unit, decode-only
+        counts = (flags != 0).sum(dim=1).cpu() if nb else torch.zeros(U, dtype=torch.int64)
+        dc, sc = int(counts.max().item()) if U else 0, int((nb - counts).max().item()) if U else 0
+    else:
+        dc = int((flags[0] != 0).sum().item()) if nb else 0
+        sc = nb - dc
+    out = DeviceCompressedCache(x.dtype, axis, U, nb, dc, sc, x.device, d, cfg.block_size, cfg)
+    if capacity:
+        out.unit_dense_counts = [int(c) for c in counts]
     st = _status(status, x.device)
     capi.check(capi.load().hs_compress_with_flags(x.data_ptr(), _unit_stride(x), rows, flags.data_ptr(),
                                                   out.cref(), st.ptr(), _stream()))

@@ -93,3 +93,62 @@ def test_sequence_split_decode_two_ranks(L, tail):
     err, shape = ret.get(timeout=60)
     assert shape == (world, 1, 4, 130)
     assert err < 1e-5, err
+
+
+def _worker_global(rank, world, port_no, L, ret):
+    """Sequence-split pruning with the global block selection: every rank's shard
+    losses are gathered (distributed.gather_block_losses, the product's
+    collective), the selection over the whole sequence flags the blocks, each
+    rank packs its slice; oracle functions stand in for the device kernels."""
+    import torch
+    import torch.distributed as dist
+    from oracle.oracle import Oracle, SparsityConfig
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        port = Oracle("port")
+        d, gqa, seed, B = 128, 4, 9, 64
+        cfg = SparsityConfig(0.5, 0.5, B, 64, 256)
+        k = port.round_to(port.random_gaussian(L, d, port.head_seed(seed, 0, 0)), "bf16")
+        v = port.round_to(port.random_gaussian(L, d, port.head_seed(seed, 0, 1)), "bf16")
+        q = port.round_to(np.stack([port.random_gaussian(1, d, port.head_seed(seed, 0, 32 + g))[0]
+                                    for g in range(gqa)]), "bf16")
+        scale = np.float32(1 / math.sqrt(d))
+        nb = L // B
+        sh = D.sequence_shard(nb, world, rank)
+        kf = port.prune_compress(k, cfg, 0, 0.5)  # whole-sequence reference (every rank can check)
+        vf = port.prune_compress(v, cfg, 1, 0.5)
+        parts = []
+        ok_losses = True
+        for x, full, axis in ((k, kf, 0), (v, vf, 1)):
+            xs = x[sh.begin * B:sh.end * B]
+            local = port.prune_compress(xs, SparsityConfig(0.0, 0.0, B), axis, 0.0).losses  # block_loss of the shard
+            glob = D.gather_block_losses(torch.from_numpy(local)[None], nb)[0].numpy()
+            ok_losses &= glob.tobytes() == full.losses.tobytes()
+            flags = full.flags  # select_blocks over the gathered losses (the oracle's, = whole-sequence)
+            parts.append(port.compress_with_flags(xs, cfg, axis, flags[sh.begin:sh.end]))
+        out_t, m, l = port.attend_rows(q, parts[0], parts[1], None, None, 0, sh.size, False, scale)
+        partial = torch.from_numpy(np.concatenate([out_t.T, m[:, None], l[:, None]], axis=1))[None]
+        got = _combine(D.gather_partials(partial).numpy()[:, 0])
+        if rank == 0:
+            want = port.decode(q, kf, vf, None, None, scale, 1)
+            local_only = port.prune_compress(k[sh.begin * B:sh.end * B], cfg, 0, 0.5).flags
+            ret.put((ok_losses, float(np.abs(got - want).max()),
+                     bool((local_only != kf.flags[sh.begin:sh.end]).any())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sequence_split_pruning_uses_the_global_selection():
+    """At S = 0.5 with sink and window protection, shard-local pruning differs from
+    prune_cache of the whole sequence; gathering the losses restores it exactly and
+    the split decode equals the single-process decode_attention."""
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    world = 2
+    mp.start_processes(_worker_global, args=(world, _free_port(), 4096, ret), nprocs=world, join=True,
+                       start_method="spawn")
+    ok_losses, err, local_differs = ret.get(timeout=60)
+    assert ok_losses
+    assert local_differs  # the bug the global selection fixes
+    assert err < 1e-5, err

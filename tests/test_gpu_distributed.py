@@ -69,3 +69,62 @@ def test_unit_shards_equal_rows_of_full_decode(hs, port):
         got = hs.decode_attention(to_torch(q[sh.begin:sh.end], "f16"), ks, vs).cpu().numpy()
         mx, _ = err_stats(got, full[sh.begin:sh.end])
         assert mx < 1e-5, (r, mx)
+
+
+@pytest.mark.parametrize("world,s,sink,window", [(2, 0.5, 64, 256), (4, 0.25, 100, 70), (8, 0.75, 0, 512)])
+def test_sharded_pruning_equals_whole_sequence(hs, port, world, s, sink, window):
+    """prune_cache_sharded's device steps per simulated rank (block losses of the
+    shard, global select_blocks over the gathered losses, compress the slice)
+    reproduce prune_cache of the whole sequence sliced by block range, bit for
+    bit, and the split decode matches the whole-sequence decode."""
+    import torch
+    from paper_2604_16864_b200 import distributed as D
+    U, gqa, d, L, B = 3, 4, 128, 8192, 64
+    kx = gen_units(port, U, L, d, 12, 0, "bf16")
+    vx = gen_units(port, U, L, d, 12, 1, "bf16")
+    q = np.stack([port.round_to(np.stack([port.random_gaussian(1, d, port.head_seed(12, u, 32 + g))[0]
+                                          for g in range(gqa)]), "bf16") for u in range(U)])
+    cfg = hs.SparsityConfig(s, s, B, sink, window)
+    nb = L // B
+    kf, vf = hs.prune_cache(to_torch(kx, "bf16"), to_torch(vx, "bf16"), cfg)
+    shards = [D.sequence_shard(nb, world, r) for r in range(world)]
+    out = {}
+    for x, full, axis, sv in ((kx, kf, 0, s), (vx, vf, 1, s)):
+        xs = [to_torch(x[:, sh.begin * B:sh.end * B], "bf16") for sh in shards]
+        losses = torch.cat([hs.block_losses(t, cfg, axis) for t in xs], dim=1)  # = gather_block_losses
+        assert losses.cpu().numpy().tobytes() == full.losses.cpu().numpy().tobytes()
+        flags = hs.select_blocks(losses, cfg, sv)
+        assert (flags == full.flags).all()
+        caches = [hs.fused_magnitude_compress(t, flags[:, sh.begin:sh.end], cfg, axis, capacity=True)
+                  for t, sh in zip(xs, shards)]
+        for c, sh in zip(caches, shards):
+            for u in range(U):
+                got = device_to_oracle(c, u)
+                dense = port.decompress(got)
+                want = port.decompress(device_to_oracle(full, u))[sh.begin * B:sh.end * B]
+                assert (dense == want).all()
+        out[axis] = caches
+    parts = [hs.decode_partial(to_torch(q, "bf16"), out[0][r], out[1][r], 0, sh.size, include_tail=False)
+             for r, sh in enumerate(shards)]
+    got = hs.decode_combine(torch.stack(parts)).cpu().numpy()
+    want = hs.decode_attention(to_torch(q, "bf16"), kf, vf).cpu().numpy()
+    mx, mr = err_stats(got, want)
+    assert mx < 1e-4 and mr < 1e-5, (mx, mr)
+
+
+def test_prune_cache_sharded_single_rank(hs, port):
+    """world 1: prune_cache_sharded == prune_cache (flags and pools)."""
+    from paper_2604_16864_b200 import distributed as D
+    U, L = 2, 4096
+    kx = gen_units(port, U, L, 128, 13, 0, "f16")
+    vx = gen_units(port, U, L, 128, 13, 1, "f16")
+    cfg = hs.SparsityConfig(0.5, 0.75, 64, 64, 128)
+    kt, vt = to_torch(kx, "f16"), to_torch(vx, "f16")
+    kc, vc, kfl, vfl = D.prune_cache_sharded(kt, vt, cfg, L // 64)
+    kf, vf = hs.prune_cache(kt, vt, cfg)
+    assert (kfl == kf.flags).all() and (vfl == vf.flags).all()
+    for a, b in ((kc, kf), (vc, vf)):
+        assert (a.index_map == b.index_map).all()
+        for u in range(U):
+            ga, gb = device_to_oracle(a, u), device_to_oracle(b, u)
+            assert (port.decompress(ga) == port.decompress(gb)).all()
