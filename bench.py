@@ -8,15 +8,26 @@ compressed caches resident in HBM.  `value` = algorithmic bytes moved
 per second, aggregated over ranks.  N > 1: every rank decodes its own request
 (weak scaling, no data-path collective).
 
+The same JSON line carries the other BASELINE configs and legs, each measured
+in this run with device events (max over ranks):
+  config4   configs[3]  32 requests x 32K x 8 KV heads, KV heads sharded over ranks
+  config5   configs[4]  1M tokens x 8 KV heads, sequence split over ranks + NCCL
+                        all-gather of the SplitPartials (gather reported apart)
+  prefill   configs[2]  64K and 128K causal prefill, block sparsity sweep, KV heads
+                        sharded over ranks, with sampled-row parity per S
+  decode_grid           configs[1] decode at (S_K, S_V) in {0,1}^2 vs r_comp
+  compress / recompress prune_cache + fused_magnitude_compress, decode-phase re-prune
+  cpu_baseline          the reference (oracle/_ref) on this host's cores (rank 0, N = 1)
+
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
 from __future__ import annotations
 
 import argparse
-import ctypes as C
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -86,16 +97,35 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def dist_setup(n_gpus):
+# ------------------------------------------------------------ multi-rank ---
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_distributed(args) -> int:
+    """`--gpus N` without a torchrun environment: start N ranks of this script on
+    this node (torch.distributed.run, one process per GPU, 127.0.0.1 rendezvous)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dist_setup(selftest: bool = False):
     import torch
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif torch.cuda.is_available():
+        if selftest:
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available() and not selftest:
         torch.cuda.set_device(0)
     return rank, world, local
 
@@ -106,187 +136,442 @@ def barrier(world):
         dist.barrier()
 
 
-def max_over_ranks(x: float, world: int) -> float:
+def reduce_over_ranks(x: float, world: int, op: str) -> float:
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    return reduce_over_ranks(x, world, "max")
 
 
 def sum_over_ranks(x: float, world: int) -> float:
-    if world == 1:
-        return x
+    return reduce_over_ranks(x, world, "sum")
+
+
+# ------------------------------------------------------------- utilities ---
+class Flusher:
+    """L2 flush between timed steps: read (not write) a 2x-L2 buffer, so the next
+    step starts with an L2 full of clean, unrelated lines."""
+
+    def __init__(self, dev):
+        import torch
+        self.buf = torch.ones(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+        self.sink = torch.empty((), dtype=torch.float32, device=dev)
+
+    def __call__(self):
+        import torch
+        torch.sum(self.buf, dim=0, out=self.sink)
+
+
+def time_steps(step, steps: int, warmup: int, flush=None) -> list:
+    """Device time (ms) of `steps` calls of step() on the current stream, after
+    `warmup` untimed calls; L2 flushed before each timed call when given."""
+    import torch
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        if flush is not None:
+            flush()
+        a.record()
+        step()
+        b.record()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def randn16(shape, g, dev, dtype):
+    import torch
+    return torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(dtype)
+
+
+def build_decode_caches(hs, dev, g, units, ctx, cfg, dtype=None):
+    """Synthetic K/V per unit compressed on the device, in chunks of units that keep
+    the dense staging buffer below ~4 GB."""
+    import torch
+    dtype = dtype or torch.bfloat16
+    chunk = max(1, min(units, (1 << 31) // (ctx * D * 2)))
+    kcs, vcs = [], []
+    for c0 in range(0, units, chunk):
+        n = min(chunk, units - c0)
+        key, val = randn16((n, ctx, D), g, dev, dtype), randn16((n, ctx, D), g, dev, dtype)
+        kc, vc = hs.prune_cache(key, val, cfg)
+        kcs.append(kc)
+        vcs.append(vc)
+        del key, val
+    return kcs, vcs, chunk
+
+
+# ---------------------------------------------------------- headline step ---
+def build_headline(hs, dev, rank, scale):
+    import torch
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    cfg = hs.SparsityConfig(1.0, 1.0, 64)
+    kcs, vcs, _ = build_decode_caches(hs, dev, g, U, L, cfg)
+    q = randn16((U, GQA, D), g, dev, torch.bfloat16)
+    _, bytes_u = hs.flop_and_byte_count(GQA, kcs[0], vcs[0], 0, False)
+    return kcs[0], vcs[0], q, U * bytes_u
+
+
+# ------------------------------------------------------------------ legs ---
+def leg_config4(hs, D_, dev, rank, world, scale, args, flush):
+    """configs[3]: 32 requests x 32K x 8 KV heads x GQA 4, S = 1; KV heads sharded
+    over ranks (8/N heads x 32 requests per GPU), no data-path collective."""
+    import torch
+    heads = D_.heads_of_rank(8, world, rank)
+    units, ctx = 32 * heads.size, 32768
+    g = torch.Generator(device=dev).manual_seed(4000 + rank)
+    kcs, vcs, chunk = build_decode_caches(hs, dev, g, units, ctx, hs.SparsityConfig(1.0, 1.0, 64))
+    q = randn16((units, GQA, D), g, dev, torch.bfloat16)
+    plans = [hs.DecodePlan(q[i * chunk:(i + 1) * chunk], kcs[i], vcs[i], scale=scale) for i in range(len(kcs))]
+    nbytes = sum(hs.flop_and_byte_count(GQA, k, v, 0, False)[1] * k.n_units for k, v in zip(kcs, vcs))
+
+    def step():
+        for p in plans:
+            p()
+    barrier(world)
+    ms = statistics.mean(time_steps(step, args.steps, 3, flush))
+    ms_max = max_over_ranks(ms, world)
+    total = sum_over_ranks(nbytes, world)
+    hbm, _, _ = peaks()
+    out = {"workload": "configs[3]: batched decode, 32 requests x 32K ctx x 8 KV heads x GQA 4, S_K=S_V=1, "
+                       "bf16, KV heads sharded over GPUs", "n_gpus": world,
+           "parallelism": f"kv-head shards x{world} ({heads.size} heads x 32 requests = {units} units per GPU)",
+           "us_per_step": round(ms_max * 1e3, 2), "bytes_per_step": int(total),
+           "gbs": round(total / (ms_max * 1e-3) / 1e9, 1),
+           "per_gpu_frac_of_hbm": round(nbytes / (ms * 1e-3) / 1e9 / hbm, 4),
+           "kernels_per_step": sum(p.kernels_per_step for p in plans)}
+    # parity at size: a sample of units against the reference decode (rank 0)
+    if rank == 0 and not args.skip_cpu:
+        out["parity"] = decode_parity_sample(hs, plans[0].out, kcs[0], vcs[0], q[:kcs[0].n_units], scale,
+                                             [0, kcs[0].n_units // 2, kcs[0].n_units - 1])
+    del plans, kcs, vcs
+    torch.cuda.empty_cache()
+    return out
+
+
+def decode_parity_sample(hs, out, kc, vc, q, scale, units):
+    """max-abs / mean-rel of device decode outputs against the reference's
+    decode_attention (oracle/_ref, attention.hpp:360-409) on the same pools."""
+    import concurrent.futures as cf
+    from tests.helpers import device_to_oracle, err_stats
+    ref = reference_oracle()
+    qh = q.float().cpu().numpy()
+    got = out.cpu().numpy()
+
+    def one(u):
+        return ref.decode(qh[u], device_to_oracle(kc, u), device_to_oracle(vc, u), None, None,
+                          np.float32(scale), 1)
+    with cf.ThreadPoolExecutor(min(len(units), os.cpu_count() or 1)) as ex:
+        want = np.stack(list(ex.map(one, units)))
+    mx, mr = err_stats(got[units], want)
+    return {"units_checked": len(units), "max_abs": mx, "mean_rel": mr, "oracle": ref.kind,
+            "pass": bool(mx < 2e-2 and mr < 1e-3)}
+
+
+def reference_oracle():
+    from oracle.oracle import Oracle
+    ref_path = os.path.join(ROOT, "oracle", "_ref", "libhs_ref.so")
+    return Oracle("reference") if os.path.exists(ref_path) else Oracle("port")
+
+
+def leg_config5(hs, D_, dev, rank, world, scale, args, flush):
+    """configs[4]: 1M tokens x 8 KV heads x GQA 4, S = 1; the sequence split into N
+    contiguous shards (attention.hpp:380-381); step = decode partial over the
+    shard + NCCL all-gather of the packed (O, m, l) partials + LSE combine."""
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t)
-    return float(t.item())
+    nb_total = (1 << 20) // 64
+    sh = D_.sequence_shard(nb_total, world, rank)
+    g = torch.Generator(device=dev).manual_seed(5000 + rank)
+    kcs, vcs, _ = build_decode_caches(hs, dev, g, U, sh.size * 64, hs.SparsityConfig(1.0, 1.0, 64))
+    kc, vc = kcs[0], vcs[0]
+    q = randn16((U, GQA, D), g, dev, torch.bfloat16)
+    nbytes = hs.flop_and_byte_count(GQA, kc, vc, 0, False)[1] * U
+    out = {}
+
+    def partial():
+        out["p"] = hs.decode_partial(q, kc, vc, 0, kc.logical_blocks, include_tail=False, scale=scale)
+
+    def gather_combine():
+        out["o"] = hs.decode_combine(D_.gather_partials(out["p"]))
+
+    def step():
+        partial()
+        gather_combine()
+    barrier(world)
+    t_step = statistics.mean(time_steps(step, args.steps, 3, flush))
+    barrier(world)
+    t_part = statistics.mean(time_steps(partial, args.steps, 3, flush))
+    barrier(world)
+    t_gc = statistics.mean(time_steps(gather_combine, args.steps, 3, None))
+    ms = max_over_ranks(t_step, world)
+    ms_part = max_over_ranks(t_part, world)
+    ms_gc = max_over_ranks(t_gc, world)
+    total = sum_over_ranks(nbytes, world)
+    hbm, _, _ = peaks()
+    res = {"workload": "configs[4]: 1M-token decode, 8 KV heads x GQA 4, S_K=S_V=1, bf16, sequence split over "
+                       "GPUs + NCCL all-gather of the SplitPartials", "n_gpus": world,
+           "parallelism": f"sequence shards x{world} ({sh.size} blocks per GPU)",
+           "us_per_step": round(ms * 1e3, 2), "gbs": round(total / (ms * 1e-3) / 1e9, 1),
+           "partial_us": round(ms_part * 1e3, 2),
+           "partial_per_gpu_frac_of_hbm": round(nbytes / (t_part * 1e-3) / 1e9 / hbm, 4),
+           "gather_combine_us": round(ms_gc * 1e3, 2),
+           "gather_bytes_per_gpu": int(out["p"].numel() * 4), "bytes_per_step": int(total),
+           "collective": "all_gather_into_tensor (NCCL)" if world > 1 else "none (1 GPU)"}
+    if rank == 0 and not args.skip_cpu:
+        # parity at size: every head of the (rank's) shard against the reference decode
+        got = hs.decode_combine(out["p"][None])
+        res["parity_shard"] = decode_parity_sample(hs, got, kc, vc, q, scale, list(range(U)))
+    del kcs, vcs, kc, vc
+    torch.cuda.empty_cache()
+    return res
 
 
-# --------------------------------------------------------------- CPU legs ---
-def cpu_reference_decode(kc_host, vc_host, q, scale, threads):
-    """The reference's own decode_attention (oracle/_ref, compiled from the
-    reference headers) over every unit, head-parallel on `threads` cores."""
+def leg_decode_grid(hs, dev, rank, world, scale, args, flush):
+    """configs[1] decode at (S_K, S_V) in {0, 1}^2: measured speedup over the dense
+    caches against the closed form r_comp (cost_model.hpp:69-91)."""
+    import torch
+    from paper_2604_16864_b200.report import CostParams, compression_ratio
+    g = torch.Generator(device=dev).manual_seed(6000 + rank)
+    key, val = randn16((U, L, D), g, dev, torch.bfloat16), randn16((U, L, D), g, dev, torch.bfloat16)
+    q = randn16((U, GQA, D), g, dev, torch.bfloat16)
+    res = {}
+    for sk, sv in ((0.0, 0.0), (0.0, 1.0), (1.0, 0.0), (1.0, 1.0)):
+        kc, vc = hs.prune_cache(key, val, hs.SparsityConfig(sk, sv, 64))
+        plan = hs.DecodePlan(q, kc, vc, scale=scale)
+        ms = max_over_ranks(statistics.mean(time_steps(plan, args.steps, 3, flush)), world)
+        nbytes = hs.flop_and_byte_count(GQA, kc, vc, 0, False)[1] * U
+        res[f"{sk:g},{sv:g}"] = {"us": round(ms * 1e3, 2), "bytes": int(nbytes),
+                                 "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1)}
+        del plan, kc, vc
+    base = res["0,0"]["us"]
+    for k, v in res.items():
+        sk, sv = (float(x) for x in k.split(","))
+        v["speedup_vs_dense"] = round(base / v["us"], 3)
+        v["r_comp_closed_form"] = round(compression_ratio(CostParams(L, D, 64, sk, sv), exact=True), 3)
+    del key, val
+    torch.cuda.empty_cache()
+    return {"workload": "configs[1] shape (8 KV heads x 128K x GQA 4, bf16), decode µs per (S_K,S_V)",
+            "by_s_key_s_value": res}
+
+
+def leg_prefill(hs, D_, dev, rank, world, args):
+    """configs[2]: Llama-3.1-8B prefill attention, causal, hierarchical mixed
+    dense / 2:4 blocks at block sparsity S_K = S_V in {0, .25, .5, .75} (+1), fp16
+     at 64K and 128K, bf16 at 64K; KV heads sharded over ranks.
+    TFLOPS counts flop_and_byte_count flops (sparse blocks at half).  Parity:
+    sampled query rows through the reference's attend_range with explicit
+    positions (attention.hpp:249-253) on rank 0."""
+    import torch
+    _, dense_peak, peak_kind = peaks()
+    heads = D_.heads_of_rank(8, world, rank)
+    Up, G = heads.size, 4
+    res = {}
+    sweeps = [(args.prefill_ctx, torch.float16, (0.0, 0.25, 0.5, 0.75, 1.0))]
+    if not args.quick:
+        sweeps += [(2 * args.prefill_ctx, torch.float16, (0.0, 0.25, 0.5, 0.75, 1.0)),
+                   (args.prefill_ctx, torch.bfloat16, (0.0, 0.5, 1.0))]
+    for Lp, dt, levels in sweeps:
+        tag = f"{Lp // 1024}K_{'fp16' if dt == torch.float16 else 'bf16'}"
+        g = torch.Generator(device=dev).manual_seed(99 + rank)
+        q = randn16((Up, G, Lp, D), g, dev, dt)
+        out = torch.empty((Up, G, Lp, D), dtype=torch.float32, device=dev)
+        by = {}
+        for s in levels:
+            key, val = randn16((Up, Lp, D), g, dev, dt), randn16((Up, Lp, D), g, dev, dt)
+            kc, vc = hs.prune_cache(key, val, hs.SparsityConfig(s, s, 64))
+            flops = sum(hs.flop_and_byte_count(Lp, kc, vc, 0, True, unit=u)[0] for u in range(Up)) * G
+            barrier(world)
+            times = time_steps(lambda: hs.prefill_attention(q, kc, vc, causal=True, out=out), args.prefill_steps, 1)
+            ms = max_over_ranks(statistics.median(times), world)
+            total = sum_over_ranks(flops, world)
+            tflops = total / (ms * 1e-3) / 1e12
+            entry = {"ms": round(ms, 3), "counted_tflops": round(tflops, 1), "frac": round(tflops / dense_peak, 4),
+                     "counted_flops": int(total)}
+            if rank == 0 and not args.skip_cpu and Lp <= 2 * args.prefill_ctx:
+                entry["parity"] = prefill_parity(hs, q, out, kc, vc, key, val, dt,
+                                                 rows=64 if Lp > args.prefill_ctx else 96,
+                                                 heads=[(0, 0), (Up - 1, G - 1)] if Lp <= args.prefill_ctx
+                                                 else [(0, 1)])
+            by[str(s)] = entry
+            del kc, vc, key, val
+        res[tag] = by
+        del q, out
+        torch.cuda.empty_cache()
+    f16 = res[f"{args.prefill_ctx // 1024}K_fp16"]
+    s0, s1 = f16["0.0"]["ms"], f16["1.0"]["ms"]
+    return {"workload": f"configs[2]: Llama-3.1-8B prefill, 32 q / 8 kv heads, d=128, causal; {args.prefill_ctx} "
+                        f"(+{2 * args.prefill_ctx}) ctx; KV heads sharded over GPUs ({heads.size}/GPU)",
+            "metric": "counted TFLOPS (flop_and_byte_count; sparse blocks at half) / dense bf16 peak",
+            "peak": dense_peak, "peak_kind": peak_kind, "by_block_sparsity": f16, "sweeps": res,
+            "speedup_s1_vs_s0": round(s0 / s1, 3), "ideal_speedup_s1_vs_s0": 2.0,
+            "kernel": "hs::prefill_kernel (tcgen05.mma.sp, TMEM accumulators)", "n_gpus": world}
+
+
+def prefill_parity(hs, q, out, kc, vc, key, val, dt, rows, heads):
+    """Sampled rows of the device prefill against the reference's attend_range over
+    the whole cache with explicit query positions (attention.hpp:249-253) and
+    finalize_rows (:309-317): rows 0, B-1, B, block boundaries, L-1 and a
+    uniform spread; max-abs / mean-rel over all sampled rows."""
     import concurrent.futures as cf
-    from oracle.oracle import Oracle
-    ref = Oracle("reference") if os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libhs_ref.so")) \
-        else Oracle("port")
+    from tests.helpers import device_to_oracle, err_stats
+    ref = reference_oracle()
+    n_q = q.shape[2]
+    pick = sorted(set([0, 63, 64, 127, 128, n_q // 2, n_q - 65, n_q - 64, n_q - 1] +
+                      list(np.linspace(0, n_q - 1, rows).astype(int))))
+    scale = np.float32(1.0 / math.sqrt(D))
+    got_all, want_all = [], []
+    for u, h in heads:
+        kh, vh = device_to_oracle(kc, u), device_to_oracle(vc, u)
+        qh = q[u, h, pick].float().cpu().numpy()
+        pos = np.array(pick, np.int64)
+        chunks = np.array_split(np.arange(len(pick)), min(16, os.cpu_count() or 1))
+
+        def one(idx):
+            o_t, m, l = ref.attend_rows(qh[idx], kh, vh, None, None, 0, kh.logical_blocks, False, scale, pos[idx])
+            return o_t.T / l[:, None]
+        with cf.ThreadPoolExecutor(len(chunks)) as ex:
+            want = np.concatenate(list(ex.map(one, chunks)))
+        got_all.append(out[u, h, pick].cpu().numpy())
+        want_all.append(want)
+    mx, mr = err_stats(np.concatenate(got_all), np.concatenate(want_all))
+    return {"rows": len(pick) * len(heads), "heads": [list(x) for x in heads], "max_abs": mx, "mean_rel": mr,
+            "oracle": ref.kind, "pass": bool(mx < 2e-2 and mr < 1e-3)}
+
+
+def leg_compress(hs, dev, rank, world, args, flush):
+    """prune_cache + fused_magnitude_compress of configs[1] K+V (8 x 128K x 128 bf16)
+    into preallocated pools (no allocation in the timed region), static (S = 1) and
+    loss-driven (S = 0.5) selection; the fused decode-phase re-prune 0.5 -> 1."""
+    import torch
+    hbm, _, _ = peaks()
+    g = torch.Generator(device=dev).manual_seed(7000 + rank)
+    key, val = randn16((U, L, D), g, dev, torch.bfloat16), randn16((U, L, D), g, dev, torch.bfloat16)
+    res = {}
+    for s in (1.0, 0.5):
+        cfg = hs.SparsityConfig(s, s, 64)
+        outp = hs.prune_cache(key, val, cfg)
+        ms = max_over_ranks(min(time_steps(lambda: hs.prune_cache(key, val, cfg, out=outp), args.steps, 3, flush)),
+                            world)
+        nbytes = 2 * key.numel() * 2 + outp[0].nbytes() + outp[1].nbytes() + 2 * U * outp[0].logical_blocks * (8 + 1 + 4)
+        res[f"prune_cache_s{s:g}"] = {"ms": round(ms, 4), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
+                                      "frac_of_hbm": round(nbytes / (ms * 1e-3) / 1e9 / hbm, 4), "bytes": int(nbytes),
+                                      "selection": "static" if s == 1.0 else "loss-driven (classify, rank, pack)"}
+    kp, vp = hs.prune_cache(key, val, hs.SparsityConfig(0.5, 0.5, 64))
+    dec = hs.SparsityConfig(1.0, 1.0, 64)
+    k2, v2 = hs.recompress(kp, dec, 1.0), hs.recompress(vp, dec, 1.0)
+    st = hs.StatusWord(dev)
+
+    def rc():
+        hs.recompress(kp, dec, 1.0, check=False, status=st)
+        hs.recompress(vp, dec, 1.0, check=False, status=st)
+    ms = max_over_ranks(min(time_steps(rc, args.steps, 3, flush)), world)
+    st.check()
+    nbytes = kp.nbytes() + vp.nbytes() + k2.nbytes() + v2.nbytes() + 2 * U * k2.logical_blocks * (8 + 1 + 4)
+    res["recompress_s0.5_to_1"] = {"ms": round(ms, 4), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
+                                   "frac_of_hbm": round(nbytes / (ms * 1e-3) / 1e9 / hbm, 4), "bytes": int(nbytes),
+                                   "call": "hierasparse.recompress x2 (hs_recompress, one pass, no host sync)"}
+    del key, val, kp, vp, k2, v2
+    torch.cuda.empty_cache()
+    return res
+
+
+# ------------------------------------------------------------ CPU baseline ---
+def cpu_baselines(hs, kc, vc, q, scale, step_bytes):
+    """The reference's own CPU implementation (oracle/_ref, compiled from the
+    reference headers with its Release flags) on this host, bounded samples of
+    the BASELINE workloads: decode 1 core as shipped and
+    head-parallel; prefill per head extrapolated from sampled rows; compression."""
+    import concurrent.futures as cf
+    from oracle.oracle import SparsityConfig as OCfg
+    from tests.helpers import device_to_oracle
+    ref = reference_oracle()
+    nproc = os.cpu_count() or 1
+    kch = [device_to_oracle(kc, u) for u in range(U)]
+    vch = [device_to_oracle(vc, u) for u in range(U)]
+    qh = q.float().cpu().numpy()
+    sc = np.float32(scale)
+    # decode: one unit on one core (as shipped), then the whole step head-parallel
+    t0 = time.perf_counter()
+    ref.decode(qh[0], kch[0], vch[0], None, None, sc, 1)
+    t_one = time.perf_counter() - t0
+    threads = min(U, nproc)
     t0 = time.perf_counter()
     with cf.ThreadPoolExecutor(threads) as ex:
-        outs = list(ex.map(lambda u: ref.decode(q[u], kc_host[u], vc_host[u], None, None, scale, 1),
-                           range(len(kc_host))))
-    return time.perf_counter() - t0, np.stack(outs), ref.kind
-
-
-def host_caches(dev, units):
-    from tests.helpers import device_to_oracle
-    return [device_to_oracle(dev, u) for u in units]
+        outs = list(ex.map(lambda u: ref.decode(qh[u], kch[u], vch[u], None, None, sc, 1), range(U)))
+    t_par = time.perf_counter() - t0
+    decode = {"value": round(step_bytes / t_par / 1e9, 4), "unit": "GB/s", "cores": threads, "nproc": nproc,
+              "kind": ref.kind, "seconds_per_step": round(t_par, 3),
+              "one_core_seconds_per_step": round(t_one * U, 3),
+              "one_core_value": round(step_bytes / (t_one * U) / 1e9, 4),
+              "sample": f"configs[1] decode step ({U} KV heads x {L} tokens, GQA {GQA}): all {U} units on "
+                        f"{threads} threads (one unit per thread, the reference is single-threaded); 1-core "
+                        f"figure = one unit timed alone x {U}"}
+    # prefill: the reference's attend_range over a full 64K cache for sampled rows,
+    # extrapolated to a head by visible keys and x32 heads (labelled)
+    import torch
+    Lp = 65536
+    g = torch.Generator().manual_seed(11)
+    kx = torch.randn((Lp, D), generator=g).to(torch.float16).float().numpy()
+    vx = torch.randn((Lp, D), generator=g).to(torch.float16).float().numpy()
+    qx = torch.randn((Lp, D), generator=g).to(torch.float16).float().numpy()
+    cfg = OCfg(0.5, 0.5, 64)
+    kref = ref.prune_compress(kx, cfg, 0, 0.5)
+    vref = ref.prune_compress(vx, cfg, 1, 0.5)
+    rows = np.linspace(0, Lp - 1, 48).astype(np.int64)
+    t0 = time.perf_counter()
+    ref.attend_rows(qx[rows], kref, vref, None, None, 0, kref.logical_blocks, False, sc, rows)
+    t_rows = time.perf_counter() - t0
+    visible_sample = float((rows + 1).sum())
+    visible_head = Lp * (Lp + 1) / 2.0
+    per_head = t_rows * visible_head / visible_sample
+    prefill = {"seconds_per_head_extrapolated": round(per_head, 1), "seconds_32_heads_extrapolated":
+               round(per_head * 32, 1), "cores": 1, "kind": ref.kind,
+               "sample": f"attend_range over a full 64K causal S=0.5 cache for {len(rows)} query rows "
+                         f"({t_rows:.2f} s), extrapolated to one head by visible keys, x32 heads"}
+    # compression of one 128K KV head (K + V): prune_cache (fused) and the two-phase compress
+    kx1 = torch.randn((L, D), generator=g).to(torch.bfloat16).float().numpy()
+    vx1 = torch.randn((L, D), generator=g).to(torch.bfloat16).float().numpy()
+    cfg1 = OCfg(0.5, 0.5, 64)
+    t0 = time.perf_counter()
+    ck = ref.prune_compress(kx1, cfg1, 0, 0.5, fused=True)
+    ref.prune_compress(vx1, cfg1, 1, 0.5, fused=True)
+    t_prune = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ref.compress_with_flags(kx1, cfg1, 0, ck.flags)
+    t_fused = time.perf_counter() - t0
+    compress = {"prune_cache_kv_one_head_s": round(t_prune, 3),
+                "fused_magnitude_compress_k_one_head_s": round(t_fused, 3), "cores": 1, "kind": ref.kind,
+                "sample": "one 128K KV head, S=0.5 (loss-driven): prune_cache + fused_magnitude_compress of K "
+                          "and V; fused_magnitude_compress of K under the resulting BlockMask"}
+    return decode, prefill, compress, np.stack(outs)
 
 
 # ---------------------------------------------------------------- our arm ---
-def build_workload(args, hs, dev, rank, world, scale):
-    """The decode workload this rank runs (synthetic bf16 K/V, compressed on device):
-
-    config2 (headline, BASELINE configs[1]): this rank's own request, 8 KV heads x
-        GQA 4 x 128K, S_K=S_V=1 — weak scaling over ranks, no collective.
-    config4 (configs[3]): 32 requests x 32K x 8 KV heads, KV heads sharded over the
-        ranks (each rank: 8/N heads x 32 requests = 256/N units) — strong scaling.
-    config5 (configs[4]): 1 request x 1M tokens x 8 KV heads, the sequence split
-        into N contiguous shards (distributed.sequence_shard); each step = decode
-        partial over the shard + NCCL all-gather of the (O, m, l) partials +
-        LSE combine — strong scaling."""
-    import torch
-    from paper_2604_16864_b200 import distributed as Dd
-    cfg = hs.SparsityConfig(1.0, 1.0, 64)
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    if args.workload == "config2":
-        units, L_ctx, blocks = U, L, L // 64
-        desc = {"workload": "configs[1]: Llama-3.1-8B GQA decode, 32 q / 8 kv heads, d=128, 128K ctx, batch 1 "
-                            "per GPU, S_K=S_V=1 (2:4 K+V)", "kv_heads": U, "gqa": GQA, "context": L,
-                "block_size": 64, "s_key": 1.0, "s_value": 1.0, "parallelism": f"request-per-GPU x{world}"}
-        scaling = "weak"
-    elif args.workload == "config4":
-        heads = Dd.heads_of_rank(8, world, rank)
-        units, L_ctx, blocks = 32 * heads.size, 32768, 32768 // 64
-        desc = {"workload": "configs[3]: batched decode, 32 requests x 32K ctx x 8 KV heads x GQA 4, S_K=S_V=1, "
-                            "KV heads sharded over GPUs", "requests": 32, "kv_heads": 8, "gqa": GQA,
-                "context": 32768, "parallelism": f"kv-head shards x{world} ({heads.size} heads/GPU)"}
-        scaling = "strong"
-    elif args.workload == "config5":
-        sh = Dd.sequence_shard(1 << 14, world, rank)
-        units, L_ctx, blocks = U, sh.size * 64, sh.size
-        desc = {"workload": "configs[4]: 1M-token decode, 8 KV heads x GQA 4, S_K=S_V=1, sequence split over "
-                            "GPUs + NCCL all-gather of partials", "kv_heads": U, "gqa": GQA, "context": 1 << 20,
-                "parallelism": f"sequence shards x{world} ({sh.size} blocks/GPU)"}
-        scaling = "strong"
-    else:
-        raise SystemExit(f"unknown workload {args.workload}")
-    # compress in chunks of units to bound the dense staging buffer (<= 4 GB)
-    chunk = max(1, min(units, (1 << 31) // (L_ctx * D * 2)))
-    kcs, vcs = [], []
-    comp_ms = []
-    comp_bytes = 0
-    rc_ms, rc_bytes = [], 0
-    for c0 in range(0, units, chunk):
-        n = min(chunk, units - c0)
-        key = torch.randn((n, L_ctx, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
-        val = torch.randn((n, L_ctx, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
-        if c0 == 0:  # compression (prune_cache + fused_magnitude_compress) timed on the first chunk
-            for _ in range(3):
-                torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                kc0, vc0 = hs.prune_cache(key, val, cfg)
-                e1.record()
-                torch.cuda.synchronize()
-                comp_ms.append(e0.elapsed_time(e1))
-            comp_bytes = 2 * key.numel() * 2 + kc0.nbytes() + vc0.nbytes() + 2 * n * kc0.logical_blocks * (8 + 1 + 4)
-            # decode-phase re-prune (pipeline.hpp:227-240) of prefill-sparsity caches
-            # (S = 0.5) to the decode sparsity, fused over the compressed pools
-            kp, vp = hs.prune_cache(key, val, hs.SparsityConfig(0.5, 0.5, 64))
-            for _ in range(3):
-                torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                k2, v2 = hs.recompress(kp, cfg, cfg.s_key), hs.recompress(vp, cfg, cfg.s_value)
-                e1.record()
-                torch.cuda.synchronize()
-                rc_ms.append(e0.elapsed_time(e1))
-            rc_bytes = (kp.nbytes() + vp.nbytes() + k2.nbytes() + v2.nbytes() +
-                        2 * n * k2.logical_blocks * (8 + 1 + 4))
-            del kp, vp, k2, v2
-            kcs.append(kc0)
-            vcs.append(vc0)
-        else:
-            kc0, vc0 = hs.prune_cache(key, val, cfg)
-            kcs.append(kc0)
-            vcs.append(vc0)
-        del key, val
-    q = torch.randn((units, GQA, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
-    _, bytes_u = hs.flop_and_byte_count(GQA, kcs[0], vcs[0], 0, False)
-    step_bytes = units * bytes_u
-    wl = {"kc": kcs[0], "vc": vcs[0], "q": q, "bytes": step_bytes, "config": desc, "scaling": scaling,
-          "comp_ms": comp_ms, "comp_bytes": comp_bytes, "rc_ms": rc_ms, "rc_bytes": rc_bytes, "plan": None}
-    if args.workload == "config5":
-        last = rank == world - 1
-
-        def call(qd):
-            return Dd.sequence_split_decode(qd, kcs[0], vcs[0], is_last=last, scale=scale)
-        wl["step"] = lambda: call(q)
-        wl["e2e_call"] = call
-        wl["e2e_name"] = "distributed.sequence_split_decode (decode_partial + all-gather + decode_combine)"
-        return wl
-    # one CUDA graph per chunk of units (the decode step of every unit of this rank)
-    plans = [hs.DecodePlan(q[i * chunk:(i + 1) * chunk], kcs[i], vcs[i], scale=scale) for i in range(len(kcs))]
-
-    class MultiPlan:
-        kernels_per_step = sum(p.kernels_per_step for p in plans)
-        out = plans[0].out
-
-        def __call__(self):
-            for p in plans:
-                p()
-    wl["plan"] = MultiPlan()
-    wl["step"] = wl["plan"]
-    outs = [torch.empty((kc.n_units, GQA, D), dtype=torch.float32, device=dev) for kc in kcs]
-
-    def call(qd):
-        for i in range(len(kcs)):
-            hs.decode_attention(qd[i * chunk:(i + 1) * chunk], kcs[i], vcs[i], scale=scale, out=outs[i])
-        return outs[0] if len(outs) == 1 else torch.cat(outs)
-    wl["e2e_call"] = call
-    wl["e2e_name"] = "hierasparse.decode_attention"
-    return wl
-
-
 def run_ours(args):
     import torch
     from paper_2604_16864_b200 import capi
+    from paper_2604_16864_b200 import distributed as D_
     from paper_2604_16864_b200 import hierasparse as hs
 
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup()
     dev = torch.device("cuda", torch.cuda.current_device())
     hbm_peak, _, peak_kind = peaks()
     scale = 1.0 / math.sqrt(D)
-    wl = build_workload(args, hs, dev, rank, world, scale)
-    kc, vc, q, step_bytes = wl["kc"], wl["vc"], wl["q"], wl["bytes"]
-    comp_ms, comp_bytes = wl["comp_ms"], wl["comp_bytes"]
-    # L2 flush between timed steps: read (not write) a 2x-L2 buffer, so the next
-    # step starts with an L2 full of clean, unrelated lines (a write flush would
-    # charge ~126 MB of dirty-line writebacks to the timed kernel).
-    flush = torch.ones(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
-    flush_sink = torch.empty((), dtype=torch.float32, device=dev)
-
-    def flush_l2():
-        torch.sum(flush, dim=0, out=flush_sink)
-
-    plan = wl["plan"]
-    step = wl["step"]
+    kc, vc, q, step_bytes = build_headline(hs, dev, rank, scale)
+    flush = Flusher(dev)
+    plan = hs.DecodePlan(q, kc, vc, scale=scale)
     for _ in range(args.warmup):
-        step()
+        plan()
     torch.cuda.synchronize()
 
     # ---- timed region: K decode steps (device events), L2 flushed between steps
@@ -298,9 +583,9 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         t_wall = time.perf_counter()
         for i in range(args.steps):
-            flush_l2()
+            flush()
             starts[i].record()
-            step()
+            plan()
             stops[i].record()
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
@@ -309,10 +594,10 @@ def run_ours(args):
         t_soak = time.perf_counter()
         while not args.profile and time.perf_counter() - t_soak < 1.5:
             for _ in range(50):
-                step()
+                plan()
             torch.cuda.synchronize()
     barrier(world)
-    launches = capi.kernel_launches() - launches0 + (args.steps * plan.kernels_per_step if plan else 0)
+    launches = capi.kernel_launches() - launches0 + args.steps * plan.kernels_per_step
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, stops)]
     ms = statistics.mean(step_ms)
     ms_max = max_over_ranks(ms, world)
@@ -322,51 +607,46 @@ def run_ours(args):
     # ---- e2e: host queries in (pinned), decode through the public API, result out
     q_host = q.cpu().pin_memory()
     q_dev = torch.empty_like(q)
-    e2e_call = wl["e2e_call"]
-    out = e2e_call(q_dev)
-    out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
-    for _ in range(max(3, args.warmup)):
+    out_dev = torch.empty((U, GQA, D), dtype=torch.float32, device=dev)
+    out_host = torch.empty(out_dev.shape, dtype=torch.float32).pin_memory()
+
+    def e2e_step():
         q_dev.copy_(q_host, non_blocking=True)
-        out = e2e_call(q_dev)
-        out_host.copy_(out, non_blocking=True)
-    torch.cuda.synchronize()
-    e_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    e_t = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        hs.decode_attention(q_dev, kc, vc, scale=scale, out=out_dev)
+        out_host.copy_(out_dev, non_blocking=True)
     barrier(world)
-    for i in range(args.steps):
-        flush_l2()
-        e_s[i].record()
-        q_dev.copy_(q_host, non_blocking=True)
-        out = e2e_call(q_dev)
-        out_host.copy_(out, non_blocking=True)
-        e_t[i].record()
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in zip(e_s, e_t)), world)
+    e2e_ms = max_over_ranks(statistics.mean(time_steps(e2e_step, args.steps, max(3, args.warmup), flush)), world)
     e2e_value = total_bytes / (e2e_ms * 1e-3) / 1e9
 
-    # ---- prefill (configs[2]): 32 q / 8 kv heads, 64K causal, S in {0,.25,.5,.75}
-    prefill = None if (args.no_prefill or args.workload != "config2") else run_prefill(hs, dev, rank, args)
+    # ---- the other BASELINE configs and legs (same run, device events, max over ranks)
+    legs = {}
+    if not args.headline_only:
+        legs["config4"] = leg_config4(hs, D_, dev, rank, world, scale, args, flush)
+        legs["config5"] = leg_config5(hs, D_, dev, rank, world, scale, args, flush)
+        if not args.no_prefill:
+            legs["prefill"] = leg_prefill(hs, D_, dev, rank, world, args)
+        if not args.quick:
+            legs["decode_grid"] = leg_decode_grid(hs, dev, rank, world, scale, args, flush)
+        legs["compress"] = leg_compress(hs, dev, rank, world, args, flush)
 
-    # ---- CPU baseline: the reference's decode on this host's cores (rank 0, N=1)
+    # ---- CPU baseline: the reference on this host's cores (rank 0, N = 1)
     cpu = None
-    if rank == 0 and world == 1 and args.workload == "config2" and not (args.skip_cpu or args.profile):
-        threads = min(16, os.cpu_count() or 1)
-        units = list(range(U))
-        kch, vch = host_caches(kc, units), host_caches(vc, units)
-        qh = q.float().cpu().numpy()
-        secs, ref_out, kind = cpu_reference_decode(kch, vch, qh, np.float32(scale), threads)
+    extra_cpu = {}
+    if rank == 0 and world == 1 and not (args.skip_cpu or args.profile):
+        dec, pre, comp, ref_out = cpu_baselines(hs, kc, vc, q, scale, step_bytes)
         got = plan.out.cpu().numpy()
-        err = float(np.abs(got - ref_out).max())
-        cpu = {"value": round(step_bytes / secs / 1e9, 4), "unit": "GB/s", "cores": threads,
-               "kind": kind, "seconds": round(secs, 3), "max_abs_vs_gpu": err,
-               "sample": f"one full configs[1] decode step ({U} KV heads x {L} tokens, GQA {GQA}) "
-                         f"head-parallel on {threads} threads"}
+        from tests.helpers import err_stats
+        mx, mr = err_stats(got, ref_out)
+        dec.update(max_abs_vs_gpu=mx, mean_rel_vs_gpu=mr)
+        cpu = dec
+        extra_cpu = {"cpu_prefill": pre, "cpu_compress": comp}
 
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "decode_traffic.json")
+    traffic, traffic_src = None, None
+    tf = os.path.join(ROOT, "profiles", "r02_decode_traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("bytes_per_launch")
+            tj = json.load(open(tf))
+            traffic, traffic_src = tj.get("bytes_per_launch"), tj.get("source")
         except Exception:  # noqa: BLE001
             traffic = None
 
@@ -380,30 +660,28 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms_max, 5),
         "higher_is_better": True,
-        "scaling": wl["scaling"],
+        "scaling": "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (torch.randn, bf16), random-init; pools compressed on device",
-        "config": dict(wl["config"], bytes_per_step_per_gpu=step_bytes,
-                       l2="flushed between timed steps (read of a 252 MB buffer)"),
+        "config": {"workload": "configs[1]: Llama-3.1-8B GQA decode, 32 q / 8 kv heads, d=128, 128K ctx, batch 1 "
+                               "per GPU, S_K=S_V=1 (2:4 K+V)", "kv_heads": U, "gqa": GQA, "context": L,
+                   "block_size": 64, "s_key": 1.0, "s_value": 1.0, "parallelism": f"request-per-GPU x{world}",
+                   "bytes_per_step_per_gpu": step_bytes,
+                   "l2": "flushed between timed steps (read of a 252 MB buffer)"},
         "decode_us": round(ms_max * 1e3, 2),
         "roofline": {"bound": "hbm", "achieved": round(per_gpu_gbs, 2), "peak": hbm_peak, "unit": "GB/s",
-                     "frac": round(per_gpu_gbs / hbm_peak, 4), "traffic": traffic,
-                     "peak_kind": peak_kind, "kernel": "hs::decode_kernel (+fused split combine)"}
-        if args.workload == "config2" else None,
+                     "frac": round(per_gpu_gbs / hbm_peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind, "kernel": "hs::decode_kernel (+fused split combine)",
+                     "algorithmic_bytes_per_launch": step_bytes},
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "ms_per_step": round(e2e_ms, 5),
-                "h2d_bytes_per_step": int(q.numel() * 2), "d2h_bytes_per_step": int(out.numel() * 4),
-                "call": wl["e2e_name"]},
-        "compress": {"ms": round(min(comp_ms), 4), "gbs": round(comp_bytes / (min(comp_ms) * 1e-3) / 1e9, 2),
-                     "bytes": int(comp_bytes)},
-        "recompress": {"from_s": 0.5, "to_s": 1.0, "ms": round(min(wl["rc_ms"]), 4),
-                       "gbs": round(wl["rc_bytes"] / (min(wl["rc_ms"]) * 1e-3) / 1e9, 2),
-                       "bytes": int(wl["rc_bytes"]), "call": "hierasparse.recompress x2 (hs_recompress, one pass)"}
-        if wl.get("rc_ms") else None,
+                "h2d_bytes_per_step": int(q.numel() * 2), "d2h_bytes_per_step": int(out_dev.numel() * 4),
+                "call": "hierasparse.decode_attention"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
-        "prefill": prefill,
+        **extra_cpu,
+        **legs,
         "wall_s": round(t_wall, 4),
     }
     if rank == 0:
@@ -413,43 +691,32 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_prefill(hs, dev, rank, args):
-    """configs[2]: Llama-3.1-8B prefill attention at 64K context, causal,
-    hierarchical mixed dense/2:4 blocks at block sparsity S_K = S_V in
-    {0, .25, .5, .75}; fp16 (P in fp16 meets the 1e-3 bar).
-    TFLOPS counts flop_and_byte_count flops (sparse blocks at half)."""
+# ------------------------------------------------------ distributed selftest ---
+def run_selftest(args):
+    """CPU / gloo check of the multi-rank wiring bench.py uses on GPUs: rank
+    spawning (--gpus N), barrier + max/sum over ranks, the configs[4] step's
+    all-gather of SplitPartials in rank order (distributed.gather_partials) and
+    the combine of the gathered partials, against a single-process reference
+    combine of the same partials.  No device kernels run (test infrastructure)."""
     import torch
-    _, dense_peak, peak_kind = peaks()
-    Lp, Up, G = args.prefill_ctx, 8, 4
-    g = torch.Generator(device=dev).manual_seed(99 + rank)
-    q = torch.randn((Up, G, Lp, D), generator=g, device=dev, dtype=torch.float32).half()
-    out = torch.empty((Up, G, Lp, D), dtype=torch.float32, device=dev)
-    res = {}
-    for s in (0.0, 0.25, 0.5, 0.75, 1.0):
-        key = torch.randn((Up, Lp, D), generator=g, device=dev, dtype=torch.float32).half()
-        val = torch.randn((Up, Lp, D), generator=g, device=dev, dtype=torch.float32).half()
-        kc, vc = hs.prune_cache(key, val, hs.SparsityConfig(s, s, 64))
-        del key, val
-        flops = sum(hs.flop_and_byte_count(Lp, kc, vc, 0, True, unit=u)[0] for u in range(Up)) * G
-        hs.prefill_attention(q, kc, vc, causal=True, out=out)
-        torch.cuda.synchronize()
-        times = []
-        for _ in range(args.prefill_steps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            hs.prefill_attention(q, kc, vc, causal=True, out=out)
-            e1.record()
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-        ms = statistics.median(times)
-        tflops = flops / (ms * 1e-3) / 1e12
-        res[str(s)] = {"ms": round(ms, 3), "counted_tflops": round(tflops, 1),
-                       "frac": round(tflops / dense_peak, 4), "counted_flops": flops}
-        del kc, vc
-    return {"workload": f"configs[2]: Llama-3.1-8B prefill, 32 q / 8 kv heads, d=128, {Lp} ctx, causal, fp16",
-            "metric": "counted TFLOPS (flop_and_byte_count; sparse blocks at half) / dense bf16 peak",
-            "peak": dense_peak, "peak_kind": peak_kind, "by_block_sparsity": res,
-            "kernel": "hs::prefill_kernel (tcgen05.mma.sp, TMEM accumulators)"}
+    from paper_2604_16864_b200 import distributed as D_
+    rank, world, _ = dist_setup(selftest=True)
+    nb = (1 << 20) // 64
+    sh = D_.sequence_shard(nb, world, rank)
+    g = torch.Generator().manual_seed(7)
+    all_parts = torch.randn((world, U, GQA, D + 2), generator=g, dtype=torch.float32)
+    gathered = D_.gather_partials(all_parts[rank])
+    order_ok = bool(torch.equal(gathered, all_parts))
+    t = max_over_ranks(float(rank + 1), world)
+    total = sum_over_ranks(float(sh.size), world)
+    barrier(world)
+    if rank == 0:
+        print(json.dumps({"selftest": "ok" if order_ok and t == world and total == nb else "FAILED",
+                          "n_gpus": world, "gather_order_ok": order_ok, "max_over_ranks": t,
+                          "blocks_covered": int(total), "blocks_total": nb}), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 # ---------------------------------------------------------- reference arm ---
@@ -462,10 +729,9 @@ def run_reference(args):
         return
     from oracle.oracle import Oracle, SparsityConfig
     import concurrent.futures as cf
-    ref_path = os.path.join(ROOT, "oracle", "_ref", "libhs_ref.so")
-    ref = Oracle("reference") if os.path.exists(ref_path) else Oracle("port")
+    ref = reference_oracle()
     port = Oracle("port")
-    threads = min(16, os.cpu_count() or 1)
+    threads = min(U, os.cpu_count() or 1)
     rng = np.random.default_rng(1234)
     cfg = SparsityConfig(1.0, 1.0, 64)
 
@@ -500,11 +766,12 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (bf16-rounded inputs)",
         "data": "synthetic (numpy normal, bf16-rounded)",
-        "config": {"workload": "configs[1]: Llama-3.1-8B GQA decode, 8 kv heads x GQA 4, d=128, 128K ctx, "
-                               "S_K=S_V=1", "bytes_per_step": step_bytes},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": ref.kind,
-                         "sample": f"full configs[1] decode step ({U} KV heads) per step, head-parallel on "
-                                   f"{threads} threads"},
+        "config": {"workload": "configs[1]: Llama-3.1-8B GQA decode, 32 q / 8 kv heads, d=128, 128K ctx, batch 1 "
+                               "per GPU, S_K=S_V=1 (2:4 K+V)", "bytes_per_step": step_bytes},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "nproc": os.cpu_count(),
+                         "kind": ref.kind,
+                         "sample": f"full configs[1] decode step ({U} KV heads) per step, one unit per thread on "
+                                   f"{threads} threads (the reference itself is single-threaded)"},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -515,17 +782,22 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--skip-cpu", action="store_true", help="skip the CPU-baseline leg")
+    ap.add_argument("--skip-cpu", action="store_true", help="skip the CPU-baseline and parity-sample legs")
     ap.add_argument("--profile", action="store_true", help="profiling run: no CPU leg, no clock soak")
     ap.add_argument("--no-prefill", action="store_true", help="skip the configs[2] prefill leg")
+    ap.add_argument("--quick", action="store_true", help="64K fp16 prefill only, no decode grid")
+    ap.add_argument("--headline-only", action="store_true", help="only the configs[1] headline decode")
     ap.add_argument("--prefill-ctx", type=int, default=65536)
     ap.add_argument("--prefill-steps", type=int, default=3)
-    ap.add_argument("--workload", default="config2", choices=["config2", "config4", "config5"],
-                    help="config2 (headline) | config4 batched KV-head sharding | config5 1M sequence split")
+    ap.add_argument("--selftest", action="store_true", help="CPU/gloo check of the multi-rank wiring")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args))
+    if args.selftest:
+        run_selftest(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -177,22 +177,27 @@ def prune_compress(x: torch.Tensor, cfg: SparsityConfig, sparsity: float, axis: 
     nb, dc, sc, _, _ = pool_counts(rows, cfg, sparsity)
     if out is None:
         out = DeviceCompressedCache(x.dtype, axis, U, nb, dc, sc, x.device, d, cfg.block_size, cfg)
+    elif (out.n_units, out.logical_blocks, out.dense_count, out.sparse_count, out.dtype, out.axis, out.head_dim) != \
+            (U, nb, dc, sc, x.dtype, axis, d):
+        raise ConfigError("prune_cache: the output cache's geometry does not match")
     lib = capi.load()
-    c, cc = out.c(), cfg.c()
-    capi.check(lib.hs_prune_compress(x.data_ptr(), _unit_stride(x), rows, C.byref(cc), sparsity, C.byref(c),
+    cc = cfg.c()
+    capi.check(lib.hs_prune_compress(x.data_ptr(), _unit_stride(x), rows, C.byref(cc), sparsity, out.cref(),
                                      out.losses.data_ptr(), out.flags.data_ptr(), _stream()))
     return out
 
 
-def prune_cache(key: torch.Tensor, value: torch.Tensor, cfg: SparsityConfig):
+def prune_cache(key: torch.Tensor, value: torch.Tensor, cfg: SparsityConfig, out=None):
     """prune_cache (pruner.hpp:165-176) followed by compression of both caches:
-    key along channels at S_K, value along the sequence at S_V."""
+    key along channels at S_K, value along the sequence at S_V.  out: an earlier
+    (key, value) result of the same geometry to overwrite (no allocation)."""
     if key.shape[-2] != value.shape[-2]:
         raise ConfigError("prune_cache: key/value sequence lengths differ")
     if key.shape[-1] % 4:
         raise ConfigError("prune_cache: head dimension not divisible by m_group")
-    return (prune_compress(key, cfg, cfg.s_key, capi.AXIS_CHANNEL),
-            prune_compress(value, cfg, cfg.s_value, capi.AXIS_SEQUENCE))
+    ko, vo = out if out is not None else (None, None)
+    return (prune_compress(key, cfg, cfg.s_key, capi.AXIS_CHANNEL, ko),
+            prune_compress(value, cfg, cfg.s_value, capi.AXIS_SEQUENCE, vo))
 
 
 def block_losses(x: torch.Tensor, cfg: SparsityConfig, axis: int) -> torch.Tensor:

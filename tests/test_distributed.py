@@ -152,3 +152,18 @@ def test_sequence_split_pruning_uses_the_global_selection():
     assert ok_losses
     assert local_differs  # the bug the global selection fixes
     assert err < 1e-5, err
+
+
+def test_bench_spawns_ranks_and_reports_n_gpus():
+    """`bench.py --gpus 2` without torchrun starts two ranks itself; the selftest
+    mode drives its multi-rank wiring (all-gather order of the configs[4]
+    partials, max / sum over ranks) on gloo and reports n_gpus: 2."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--selftest"],
+                         capture_output=True, text=True, timeout=240, cwd=root)
+    line = [x for x in out.stdout.splitlines() if x.startswith("{")][-1]
+    rec = json.loads(line)
+    assert rec["selftest"] == "ok" and rec["n_gpus"] == 2, rec
