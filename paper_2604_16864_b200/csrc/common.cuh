@@ -297,11 +297,16 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 constexpr uint32_t kLayoutNone = 0, kLayoutSW128 = 2, kLayoutSW64 = 4, kLayoutSW32 = 6;
 
 // Instruction descriptor for kind::f16 (fp32 accumulate).
+__host__ __device__ constexpr uint32_t umma_idesc_f16x(bool a_bf16, bool b_bf16, int M, int N, bool a_mn, bool b_mn,
+                                                       bool sparse) {
+    // kind::f16 carries separate A (bits 7-9) and B (bits 10-12) formats: F16 = 0, BF16 = 1
+    return (sparse ? (1u << 2) : 0u) | (1u << 4) /*F32 accum*/ | ((a_bf16 ? 1u : 0u) << 7) |
+           ((b_bf16 ? 1u : 0u) << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+           (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
 __host__ __device__ constexpr uint32_t umma_idesc_f16(bool bf16, int M, int N, bool a_mn, bool b_mn,
                                                       bool sparse) {
-    return (sparse ? (1u << 2) : 0u) | (1u << 4) /*F32 accum*/ | ((bf16 ? 1u : 0u) << 7) |
-           ((bf16 ? 1u : 0u) << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-           (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+    return umma_idesc_f16x(bf16, bf16, M, N, a_mn, b_mn, sparse);
 }
 
 __device__ __forceinline__ void tmem_alloc(uint32_t* smem_dst, uint32_t ncols) {

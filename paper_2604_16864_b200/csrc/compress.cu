@@ -282,6 +282,55 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
     constexpr bool kLoss = MODE != 1;
     LossAcc acc;
 
+    if (SRC == 1 && in_e < 0 && (MODE == 0 || !dense)) {
+        // A stored 2:4 block re-pruned (decode-phase re-prune): expanded, every
+        // group holds its two kept values and two zeros, so its pruned terms are
+        // zeros (loss exactly 0.0, pruner.hpp:85-87) and top-2-of-4 keeps the
+        // same positions unless a kept value is itself zero (then the tie rule may
+        // move a code).  Such blocks are copied stored-to-stored (nnz + metadata,
+        // 9 KB) instead of expanded and re-selected; the metadata is still
+        // validated like unpack_metadata (nm_metadata.hpp:107).
+        constexpr int kNnzVec = kBlock * kHeadDim / 2 / 8, kMetaVec = kBlock * kHeadDim / 16 / 8;  // uint4 counts
+        const uint4* sn = reinterpret_cast<const uint4*>(in_nnz);
+        const uint4* sm = reinterpret_cast<const uint4*>(in_meta);
+        bool bad_codes = false, zero_kept = false;
+        uint4 nv[kNnzVec / kThreads], mv = make_uint4(0u, 0u, 0u, 0u);
+        auto has_zero = [](uint32_t w) { return (w & 0x7FFFu) == 0u || (w & 0x7FFF0000u) == 0u; };
+        auto codes_bad = [](uint32_t w) {
+            bool bad = false;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t nib = (w >> (4 * i)) & 0xFu;
+                bad |= (nib >> 2) <= (nib & 3u);
+            }
+            return bad;
+        };
+        if (t < kMetaVec) {
+            mv = sm[t];
+            bad_codes = codes_bad(mv.x) || codes_bad(mv.y) || codes_bad(mv.z) || codes_bad(mv.w);
+        }
+        if (MODE != 0) {
+#pragma unroll
+            for (int i = 0; i < kNnzVec / kThreads; ++i) {
+                nv[i] = sn[t + i * kThreads];
+                zero_kept |= has_zero(nv[i].x) || has_zero(nv[i].y) || has_zero(nv[i].z) || has_zero(nv[i].w);
+            }
+        }
+        if (!__syncthreads_or(zero_kept)) {
+            if (MODE != 0) {
+                const uint64_t sb = static_cast<uint64_t>(u) * a.sparse_count + slot;
+                uint4* dn = reinterpret_cast<uint4*>(a.nnz_pool + sb * (kBlock * kHeadDim / 2));
+                uint4* dm = reinterpret_cast<uint4*>(a.meta_pool + sb * (kBlock * kHeadDim / 16));
+#pragma unroll
+                for (int i = 0; i < kNnzVec / kThreads; ++i) dn[t + i * kThreads] = nv[i];
+                if (t < kMetaVec) dm[t] = mv;
+            }
+            if (bad_codes) record_status(a.status, static_cast<uint64_t>(u) * a.nb + b, kReasonCodesOrder);
+            if (kLoss && t == 0) a.losses[static_cast<int64_t>(u) * a.nb + b] = 0.0;
+            return;
+        }
+    }
+
     if (AXIS == 0) {
         // Key cache: groups of 4 channels along a token row, stored layout = logical.
         const int c = t & 15;  // 16-byte chunk: channels 8c..8c+7 (groups 2c, 2c+1)

@@ -785,12 +785,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             const TileInfo ti = s_tiles[t];
             mbar_wait_dbg(&bar_sfull[sb], (t >> 1) & 1, dbgp, 21);
             tc_fence_after();
+            const bool tr0 = DBG && lane == 0 && wq == 0 && ch == 0;  // one tracing thread per group
+            if (tr0) trace(L, t, 0);
             float x[64];
             tmem_ld16_f(tS0 + 128 * sb + lane_off + c0, x);
             tmem_ld16_f(tS0 + 128 * sb + lane_off + c0 + 16, x + 16);
             tmem_ld16_f(tS0 + 128 * sb + lane_off + c0 + 32, x + 32);
             tmem_ld16_f(tS0 + 128 * sb + lane_off + c0 + 48, x + 48);
             tmem_ld_wait();
+            if (tr0) trace(L, t, 1);
             int c_first = 0;
             bool fast = true;
             if (ti.dblk >= 0 || ti.ve1 == 0) {
@@ -820,7 +823,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     max3f(max3f(m8[0], m8[1], m8[2]), max3f(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
                 slow = !(xmax <= kTau);
             }
-            if (bar_red_or(bar_id, slow)) {
+            const bool slow_q = bar_red_or(bar_id, slow);
+            if (tr0) trace(L, t, 2);
+            if (slow_q) {
                 if (DBG && dbgp && r == 0) atomicAdd(dbgp + 8, 1);
                 // ---- slow path (quad): x is relative to m_used[grp]
 #pragma unroll
@@ -872,6 +877,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_sempty[sb]);  // S^T[sb] consumed
             if (t >= 2) mbar_wait_dbg(&bar_pempty[sb], ((t >> 1) - 1) & 1, dbgp, 22);  // P^T[sb] free (GEMM2(t-2) done)
+            if (tr0) trace(L, t, 3);
             uint8_t* const pbuf = pbuf0 + sb * lay.p_bytes;
 #pragma unroll
             for (int g8 = 0; g8 < 8; ++g8) {
@@ -904,6 +910,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     *reinterpret_cast<uint4*>(pbuf + 32768 + pto) = lo;
                 }
             }
+            if (tr0) trace(L, t, 12);
             // ---- publish the m this tile used; O^T / l to it when tile t-1 used another
             // (between GEMM2(t-1) and GEMM2(t)).  Per-column compare of exact values:
             // a version match alone does not imply equal values across the groups.
@@ -927,6 +934,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     }
                 }
                 __syncwarp();
+                if (tr0) trace(L, t, 13);
                 if (r < 64) need = s_mt[pg][ps][c0 + r] != s_mused[grp][c0 + r];
             }
             need = bar_red_or(bar_id, need);  // also: this quad's s_mt values are all stored
@@ -966,6 +974,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_pfull[sb]);
+            if (tr0) trace(L, t, 14);
         }
         // ---- epilogue: O^T / l after the last GEMM2 (l from the row-sum accumulator),
         // by the group of the last tile: it already waited on that P^T buffer's

@@ -360,6 +360,34 @@ def test_fused_recompress_equals_decompress_then_compress(hs, port, dtype, s_pre
             assert torch.equal(a.losses, b.losses)
 
 
+@pytest.mark.parametrize("s_pre,s_dec", [(1.0, 1.0), (0.5, 1.0), (1.0, 0.5)])
+def test_recompress_with_kept_zeros(hs, port, s_pre, s_dec):
+    """Inputs with exact zeros (a third of the values): stored 2:4 groups keep
+    zeros, so re-pruning may move their codes by the tie rule -- the blocks the
+    stored-to-stored copy must not take.  Fused == the oracle chain, bit for bit."""
+    import torch
+    from oracle.oracle import SparsityConfig as OCfg
+    rng = np.random.default_rng(77)
+    U, L = 2, 2048
+    kx = gen_units(port, U, L, 128, 34, 0, "bf16")
+    vx = gen_units(port, U, L, 128, 34, 1, "bf16")
+    for x in (kx, vx):
+        x[rng.random(x.shape) < 0.35] = 0.0
+        x[:, 640:704] = 0.0  # one all-zero block
+    pre = hs.SparsityConfig(s_pre, s_pre, 64)
+    kc, vc = hs.prune_cache(to_torch(kx, "bf16"), to_torch(vx, "bf16"), pre)
+    dec = hs.SparsityConfig(s_dec, s_dec, 64)
+    for c in (kc, vc):
+        got = hs.recompress(c, dec, s_dec)
+        for u in range(U):
+            want = port.prune_compress(port.decompress(device_to_oracle(c, u)), OCfg(s_dec, s_dec, 64), c.axis, s_dec)
+            g = device_to_oracle(got, u)
+            for f in ("index_map", "dense_pool", "nnz_pool", "meta_pool"):
+                assert (getattr(g, f) == getattr(want, f)).all(), (u, f)
+            assert g.losses.tobytes() == want.losses.tobytes()
+    del torch
+
+
 def test_recompress_rejects_corrupt_input(hs, port):
     """A zero index entry or non-increasing codes in the input: decompress's DataError."""
     U, L = 1, 512
