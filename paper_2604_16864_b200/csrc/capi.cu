@@ -765,15 +765,15 @@ static hs_status decode_common_rows(const void* q, const hs_device_cache* k, con
     static long long* times = nullptr;
     const char* tpath = getenv("HS_DECODE_TIMES");  // tools: per-CTA timeline dump
     if (tpath) {
-        if (!times) cudaMalloc(&times, 65536 * 8 * sizeof(long long));
-        cudaMemsetAsync(times, 0, 65536 * 8 * sizeof(long long), s);
+        if (!times) cudaMalloc(&times, 65536 * 16 * sizeof(long long));
+        cudaMemsetAsync(times, 0, 65536 * 16 * sizeof(long long), s);
         L.cta_times = times;
     }
     cudaError_t e = hs::launch_decode(L, s);
     count_launch();
     if (e != cudaSuccess) return cuda_fail(e, "decode launch");
     if (tpath) {
-        const size_t n = static_cast<size_t>(L.n_units) * ns * 8;
+        const size_t n = static_cast<size_t>(L.n_units) * ns * 16;
         std::vector<long long> host(n);
         cudaStreamSynchronize(s);
         cudaMemcpy(host.data(), times, n * sizeof(long long), cudaMemcpyDeviceToHost);
@@ -879,12 +879,24 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
         const size_t kb = static_cast<size_t>(k->n_units) * k->sparse_count * 1024;
         const size_t vb = static_cast<size_t>(v->n_units) * v->sparse_count * 2048;
         const size_t tb = static_cast<size_t>(k->n_units) * L.n_tail_blocks * hs::kBlock * hs::kHeadDim * 2;
-        uint8_t* ws = static_cast<uint8_t*>(workspace(s, kb + vb + 2 * tb + 256, kWsPrefill, &st));
+        // bf16 caches: fp16 copy of the V pools for the ping-pong kernel (PrefillLaunch::v16)
+        L.v16 = L.bf16 && getenv("HS_PREFILL_BF16_HILO") == nullptr;
+        const size_t vd16 = L.v16 ? static_cast<size_t>(v->n_units) * v->dense_count * hs::kBlock * hs::kHeadDim * 2 : 0;
+        const size_t vn16 = L.v16 ? static_cast<size_t>(v->n_units) * v->sparse_count * hs::kBlock * hs::kHeadDim : 0;
+        const size_t a256 = 256;
+        uint8_t* ws = static_cast<uint8_t*>(
+            workspace(s, kb + vb + 2 * tb + vd16 + vn16 + 4 * a256, kWsPrefill, &st));
         if (st) return st;
         L.k_meta_hw = reinterpret_cast<uint16_t*>(ws);
         L.v_meta_hw = reinterpret_cast<uint16_t*>(ws + kb);
         L.k_tail_ws = reinterpret_cast<uint16_t*>(ws + kb + vb);
         L.v_tail_ws = reinterpret_cast<uint16_t*>(ws + kb + vb + tb);
+        uint8_t* p16 = ws + ((kb + vb + 2 * tb + a256 - 1) / a256) * a256;
+        L.v16_dense = reinterpret_cast<uint16_t*>(p16);
+        L.v16_nnz = reinterpret_cast<uint16_t*>(p16 + vd16);
+        L.v16_scale = reinterpret_cast<int*>(p16 + vd16 + vn16);
+        L.v_dense_src = v->dense_pool;
+        L.v_nnz_src = v->nnz_pool;
     }
     L.out = out;
     static long long* trace = nullptr;
@@ -907,10 +919,14 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     // tile's second half is masked in the kernel (and zero-filled past the pool).
     ok &= make_map(&L.tm_knnz, k->nnz_pool, 64, U * k->sparse_count * 64, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     ok &= make_map_halves(&L.tm_kden, k->dense_pool, U * k->dense_count * 64, 128);
-    ok &= make_map(&L.tm_vnnz, v->nnz_pool, 32, U * v->sparse_count * 128, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
-    ok &= make_map(&L.tm_vden, v->dense_pool, 64, U * v->dense_count * 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-    ok &= make_map(&L.tm_vnnz2, v->nnz_pool, 32, U * v->sparse_count * 128, 32, 256, CU_TENSOR_MAP_SWIZZLE_64B);
-    ok &= make_map(&L.tm_vden2, v->dense_pool, 64, U * v->dense_count * 128, 64, 256, CU_TENSOR_MAP_SWIZZLE_128B);
+    const void* vnnz = L.v16 ? static_cast<const void*>(L.v16_nnz) : v->nnz_pool;
+    const void* vden = L.v16 ? static_cast<const void*>(L.v16_dense) : v->dense_pool;
+    if (L.v16 && v->sparse_count == 0) vnnz = nullptr;
+    if (L.v16 && v->dense_count == 0) vden = nullptr;
+    ok &= make_map(&L.tm_vnnz, vnnz, 32, U * v->sparse_count * 128, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
+    ok &= make_map(&L.tm_vden, vden, 64, U * v->dense_count * 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_map(&L.tm_vnnz2, vnnz, 32, U * v->sparse_count * 128, 32, 256, CU_TENSOR_MAP_SWIZZLE_64B);
+    ok &= make_map(&L.tm_vden2, vden, 64, U * v->dense_count * 128, 64, 256, CU_TENSOR_MAP_SWIZZLE_128B);
     const uint64_t ntb = static_cast<uint64_t>(L.n_tail_blocks);
     ok &= make_map_halves(&L.tm_ktail, ntb ? L.k_tail_ws : nullptr, U * ntb * 64, 128);
     ok &= make_map(&L.tm_vtail, ntb ? L.v_tail_ws : nullptr, 64, U * ntb * 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -919,6 +935,7 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     count_launch();
     count_launch();  // metadata atom-order pass + the attention kernel
     if (L.n_tail_blocks > 0) count_launch();  // dense-tail layout pass
+    if (L.v16) count_launch(2);               // fp16 V copy: scale + convert
     if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
     if (L.trace) {
         static std::vector<long long> host(4096 * 16);

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int split = blockIdx.x, u = blockIdx.y;
-    long long* const ct = L.cta_times ? L.cta_times + 8 * (static_cast<int64_t>(u) * gridDim.x + split) : nullptr;
+    long long* const ct = L.cta_times ? L.cta_times + 16 * (static_cast<int64_t>(u) * gridDim.x + split) : nullptr;
     if (ct && threadIdx.x == 0) ct[0] = globaltimer();
     const int gqa = L.gqa;
     // Block range of this CTA (attention.hpp:380-381 partition of [begin, end)).
@@ -137,8 +137,11 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     int d_cur = -1, d_cur_ke = 0, d_cur_ve = 0;  // block being computed (lane 0)
     int d_nxt = -1, d_nxt_ke = 0, d_nxt_ve = 0;  // next block: entries in flight
     int d_claim = -1;                            // block after next: claim in flight
+    // The first block of every warp is static (warp w of split s: block s*NW + w),
+    // so the first TMA needs no atomic round trip; later claims start past them.
+    const int first_static = L.nsplit * NW;
     auto claim = [&]() {
-        const int b = atomicAdd(ctr, 1);
+        const int b = first_static + atomicAdd(ctr, 1);
         return b < span_dyn ? b : -1;
     };
     // L2 prefetch of a future block of this warp (pools are contiguous per slot).
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
             prefetch_tmap(&L.tm_vnnz);
         }
         if (dyn) {
-            d_cur = claim();
+            d_cur = split * NW + warp < span_dyn ? split * NW + warp : -1;
             if (d_cur >= 0) {
                 d_cur_ke = kidx_g[d_cur];
                 d_cur_ve = vidx_g[d_cur];
@@ -476,47 +479,64 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     if (L.out == nullptr) return;
 
     // ---------------- combine the unit's splits (attention.hpp:387-407) ----------------
-    // Streaming LSE merge in chunks of 32 splits: every load of a chunk (m, l and
-    // the O column of each split) is independent, so a chunk costs one L2 round
-    // trip (configs[1] has 18 splits per unit: one chunk).
+    // Two rounds of independent L2 loads: the (m, l) of every split and row go to
+    // shared memory once per CTA (weights exp(m_s - M) and the merged l computed
+    // once), then each output column loads its nsplit O values and sums them.
     const float* P = L.partial + static_cast<int64_t>(u) * L.nsplit * stride_p;
-    auto merge = [&](int idx) {
+    float* s_wt = reinterpret_cast<float*>(base_ptr);  // [nsplit][gqa] weights (the ring is free)
+    float* s_M = s_wt + L.nsplit * kMaxGqa;             // [gqa] merged max (natural-log units)
+    float* s_L = s_M + kMaxGqa;                         // [gqa] merged l
+    auto combine_slice = [&](int lo, int hi) {
         constexpr float kLog2e = 1.4426950408889634f;
-        const int qq = idx / kHeadDim, c = idx % kHeadDim;
-        const float* pq = P + qq * (kHeadDim + 2);
-        float M = -INFINITY, lsum = 0.f, acc = 0.f;
-        for (int sp0 = 0; sp0 < L.nsplit; sp0 += 32) {
-            float mv[32], lv[32], ov[32];
-#pragma unroll
-            for (int x = 0; x < 32; ++x) {
-                const bool ok = sp0 + x < L.nsplit;
-                const float* ps = pq + static_cast<int64_t>(sp0 + x) * stride_p;
-                mv[x] = ok ? __ldcg(ps + kHeadDim) : -INFINITY;
-                lv[x] = ok ? __ldcg(ps + kHeadDim + 1) : 0.f;
-                ov[x] = ok ? __ldcg(ps + c) : 0.f;
-            }
-            float mc = M;
-#pragma unroll
-            for (int x = 0; x < 32; ++x) mc = fmaxf(mc, mv[x]);
-            const float a = (M == -INFINITY) ? 0.f : fast_exp2((M - mc) * kLog2e);
-            lsum *= a;
-            acc *= a;
-#pragma unroll
-            for (int x = 0; x < 32; ++x) {
-                const float wt = mv[x] == -INFINITY ? 0.f : fast_exp2((mv[x] - mc) * kLog2e);
-                lsum += lv[x] * wt;
-                acc += ov[x] * wt;
-            }
-            M = mc;
+        const int nsg = L.nsplit * gqa;
+        for (int i = threadIdx.x; i < nsg; i += nthr) {
+            const float* ps = P + static_cast<int64_t>(i / gqa) * stride_p + (i % gqa) * (kHeadDim + 2);
+            s_wt[i] = __ldcg(ps + kHeadDim);  // m_s, then the weight
+            s_wt[nsg + i] = __ldcg(ps + kHeadDim + 1);  // l_s (scratch past the weights)
         }
-        if (L.out_mode == 0) {
-            L.out[(static_cast<int64_t>(u) * L.q_rows + qq) * kHeadDim + c] = acc / lsum;
-        } else {
-            float* po = L.out + (static_cast<int64_t>(u) * L.q_rows + qq) * (kHeadDim + 2);
-            po[c] = acc;
-            if (c == 0) {
-                po[kHeadDim] = M;
-                po[kHeadDim + 1] = lsum;
+        __syncthreads();
+        if (ct && threadIdx.x == 0) ct[8] = globaltimer();
+        if (threadIdx.x < gqa) {
+            const int qq = threadIdx.x;
+            float M = -INFINITY;
+            for (int sp = 0; sp < L.nsplit; ++sp) M = fmaxf(M, s_wt[sp * gqa + qq]);
+            float lsum = 0.f;
+            for (int sp = 0; sp < L.nsplit; ++sp) {
+                const float m = s_wt[sp * gqa + qq];
+                lsum += m == -INFINITY ? 0.f : s_wt[nsg + sp * gqa + qq] * fast_exp2((m - M) * kLog2e);
+            }
+            s_M[qq] = M;
+            s_L[qq] = lsum;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nsg; i += nthr) {
+            const float m = s_wt[i];
+            s_wt[i] = m == -INFINITY ? 0.f : fast_exp2((m - s_M[i % gqa]) * kLog2e);
+        }
+        __syncthreads();
+        if (ct && threadIdx.x == 0) ct[9] = globaltimer();
+        for (int idx = lo + threadIdx.x; idx < hi; idx += nthr) {
+            const int qq = idx / kHeadDim, c = idx % kHeadDim;
+            const float* pq = P + qq * (kHeadDim + 2) + c;
+            float acc = 0.f;
+            for (int sp0 = 0; sp0 < L.nsplit; sp0 += 16) {
+                float ov[16];
+#pragma unroll
+                for (int x = 0; x < 16; ++x)
+                    ov[x] = sp0 + x < L.nsplit ? __ldcg(pq + static_cast<int64_t>(sp0 + x) * stride_p) : 0.f;
+#pragma unroll
+                for (int x = 0; x < 16; ++x)
+                    if (sp0 + x < L.nsplit) acc += ov[x] * s_wt[(sp0 + x) * gqa + qq];
+            }
+            if (L.out_mode == 0) {
+                L.out[(static_cast<int64_t>(u) * L.q_rows + qq) * kHeadDim + c] = acc / s_L[qq];
+            } else {
+                float* po = L.out + (static_cast<int64_t>(u) * L.q_rows + qq) * (kHeadDim + 2);
+                po[c] = acc;
+                if (c == 0) {
+                    po[kHeadDim] = s_M[qq];
+                    po[kHeadDim + 1] = s_L[qq];
+                }
             }
         }
     };
@@ -538,7 +558,8 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
         const int n = gqa * kHeadDim;
         const int lo = static_cast<int>(static_cast<int64_t>(n) * split / L.nsplit);
         const int hi = static_cast<int>(static_cast<int64_t>(n) * (split + 1) / L.nsplit);
-        for (int idx = lo + threadIdx.x; idx < hi; idx += nthr) merge(idx);
+        combine_slice(lo, hi);
+        if (ct && threadIdx.x == 0) ct[10] = globaltimer();
         __syncthreads();
         if (threadIdx.x == 0 && atomicAdd(done, 1) == L.nsplit - 1) {
             *arrive = 0;  // every CTA of the unit is past its spin: safe to re-arm
@@ -555,7 +576,7 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     if (ct && threadIdx.x == 0) ct[5] = globaltimer();
     __threadfence();
     if (ct && threadIdx.x == 0) ct[6] = globaltimer();
-    for (int idx = threadIdx.x; idx < gqa * kHeadDim; idx += nthr) merge(idx);
+    combine_slice(0, gqa * kHeadDim);
     if (threadIdx.x == 0) {
         L.counters[u] = 0;
         if (dyn) *ctr = 0;  // last CTA of the unit: every warp has finished claiming

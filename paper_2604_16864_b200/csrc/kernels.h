@@ -135,6 +135,16 @@ struct PrefillLaunch {
     int n_tail_blocks;       // ceil(tail / 64): the tail enters as dense blocks nb, nb+1, ...
     uint16_t* k_tail_ws;     // workspace: [u][n_tail_blocks * 64][d], zero padded
     uint16_t* v_tail_ws;     // workspace: [u][n_tail_blocks][d][64] (transposed, zero padded)
+    // bf16 caches on the ping-pong path: GEMM2 runs in fp16 (P^T fp16 keeps 11
+    // mantissa bits; kind::f16 needs A and B of one format), over an fp16 copy of
+    // the V pools scaled by 2^-v_exp (exact for every value in fp16's normal range
+    // after scaling); the epilogue multiplies by 2^v_exp.
+    bool v16;
+    const void* v_dense_src;  // the bf16 V pools the copy is made from
+    const void* v_nnz_src;
+    uint16_t* v16_dense;      // workspace: fp16 V pools (same layouts); the V maps point here
+    uint16_t* v16_nnz;
+    int* v16_scale;           // workspace: [0] = max bf16 magnitude bits, [1] = v_exp
     float* out;
     int* dbg;                // optional pipeline watchdog record (debug)
     int mode;                // tools only: 1 = softmax skipped, 2 = MMAs skipped, 3 = both

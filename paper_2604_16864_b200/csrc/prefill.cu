@@ -78,7 +78,7 @@ struct PPNone {
 #define HS_PREFILL_G2FIRST 0  // measured: +1.5% at S=1, -2% at S=0 (64K); off
 #endif
 constexpr bool kG2First = HS_PREFILL_G2FIRST != 0;  // issue GEMM2(t-2) before GEMM1(t)
-constexpr uint32_t kBiasBytes = 3 * 2048;  // ones + bias[2] GEMM1 operands (16-byte rows)
+constexpr uint32_t kBiasBytes = 4 * 2048;  // ones + bias[2] GEMM1 operands + fp16 ones for the l MMA (16-byte rows)
 constexpr float kTau = 8.0f;      // lazy-rescale threshold (log2 units): P <= 2^8
 
 // One key tile = one or two 64-token blocks of the same K kind.  8 bytes:
@@ -321,19 +321,68 @@ __global__ void __launch_bounds__(128) meta_atom_kernel(const uint16_t* __restri
 // K rows copied token-major ([B][d], the dense K block layout), V transposed to
 // [d][B] (the dense V^T block layout), both zero padded to whole blocks.  One CTA
 // per (tail block, unit); 128 threads = one token row (K) / one channel (V).
+// bf16 magnitude bits -> fp16 bits of x * 2^-e (round to nearest even).
+__device__ __forceinline__ uint16_t bf16_to_f16_scaled(uint16_t b, int e) {
+    const float f = ldexpf(__uint_as_float(static_cast<uint32_t>(b) << 16), -e);
+    return __half_as_ushort(__float2half_rn(f));
+}
+
 __global__ void __launch_bounds__(128) tail_prep_kernel(const uint16_t* __restrict__ k_tail,
                                                         const uint16_t* __restrict__ v_tail, int tail, int ntb,
-                                                        uint16_t* __restrict__ k_ws, uint16_t* __restrict__ v_ws) {
+                                                        uint16_t* __restrict__ k_ws, uint16_t* __restrict__ v_ws,
+                                                        const int* __restrict__ v16_scale) {
     const int tb = blockIdx.x, u = blockIdx.y, c = threadIdx.x;
     const uint16_t* kt = k_tail + static_cast<int64_t>(u) * tail * kHeadDim;
     const uint16_t* vt = v_tail + static_cast<int64_t>(u) * tail * kHeadDim;
     uint16_t* kw = k_ws + (static_cast<int64_t>(u) * ntb + tb) * kBlock * kHeadDim;
     uint16_t* vw = v_ws + (static_cast<int64_t>(u) * ntb + tb) * kBlock * kHeadDim;
+    const int e = v16_scale ? v16_scale[1] : 0;
     for (int i = 0; i < kBlock; ++i) {
         const int tok = tb * kBlock + i;
         const bool in = tok < tail;
         kw[i * kHeadDim + c] = in ? kt[static_cast<int64_t>(tok) * kHeadDim + c] : uint16_t(0);
-        vw[c * kBlock + i] = in ? vt[static_cast<int64_t>(tok) * kHeadDim + c] : uint16_t(0);
+        const uint16_t vb = in ? vt[static_cast<int64_t>(tok) * kHeadDim + c] : uint16_t(0);
+        vw[c * kBlock + i] = v16_scale ? bf16_to_f16_scaled(vb, e) : vb;  // V^T of the tail (fp16 on the v16 path)
+    }
+}
+
+// The v16 path's scale: the largest bf16 magnitude of the V pools and tail
+// (integer order of the low 15 bits is magnitude order).
+__global__ void __launch_bounds__(256) v16_absmax_kernel(const uint32_t* __restrict__ a, int64_t na,
+                                                         const uint32_t* __restrict__ b, int64_t nb,
+                                                         const uint16_t* __restrict__ tail, int64_t nt, int* scale) {
+    uint32_t m = 0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < na + nb + nt; i += stride) {
+        uint32_t w;
+        if (i < na) w = a[i];
+        else if (i < na + nb) w = b[i - na];
+        else w = tail[i - na - nb];
+        m = max(m, max(w & 0x7FFFu, (w >> 16) & 0x7FFFu));
+    }
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(reinterpret_cast<unsigned*>(scale), m);
+}
+
+// fp16 copy of the bf16 V pools scaled by 2^-e, e chosen so the largest magnitude
+// lands in [2^14, 2^15): every value in fp16's normal range after scaling
+// converts exactly (bf16 has 8 significant bits, fp16 11); values more than 2^28
+// below the largest round at 2^-25 of it.  Inf / NaN: e = 0.
+__global__ void __launch_bounds__(256) v16_convert_kernel(const uint32_t* __restrict__ a, uint32_t* __restrict__ a16,
+                                                          int64_t na, const uint32_t* __restrict__ b,
+                                                          uint32_t* __restrict__ b16, int64_t nb, int* scale) {
+    const uint32_t mb = static_cast<uint32_t>(scale[0]);
+    const int ex = static_cast<int>(mb >> 7);
+    const int e = (mb == 0 || ex >= 0xFF) ? 0 : (ex == 0 ? -126 : ex - 127) - 14;
+    if (blockIdx.x == 0 && threadIdx.x == 0) scale[1] = e;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < na + nb; i += stride) {
+        const bool first = i < na;
+        const uint32_t w = first ? a[i] : b[i - na];
+        const uint32_t r = bf16_to_f16_scaled(static_cast<uint16_t>(w & 0xFFFFu), e) |
+                           (static_cast<uint32_t>(bf16_to_f16_scaled(static_cast<uint16_t>(w >> 16), e)) << 16);
+        if (first) a16[i] = r;
+        else b16[i - na] = r;
     }
 }
 
@@ -344,6 +393,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     // switches); the production instantiation compiles all of it out.
     int* const dbgp = DBG ? L.dbg : nullptr;
     const int mode = DBG ? L.mode : 0;
+    // bf16 caches on the ping-pong path: GEMM2 (and the l MMA) in fp16 over the
+    // fp16 V^T copy, P^T in fp16 (PrefillLaunch::v16)
+    constexpr bool V16 = PP && std::is_same<T, __nv_bfloat16>::value;
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bar_q, bar_kfull[4], bar_kempty[4];
     __shared__ __align__(8) uint64_t bar_vfull[4], bar_vempty[4];
@@ -467,8 +519,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         // B[sb] row c = 8 copies of -m_c / (16 scale log2e) (m unset: 0).
         uint4* ob = reinterpret_cast<uint4*>(base_ptr + lay.off_bias);
         const uint32_t one = F16Traits<T>::pack(1.f, 1.f);
-        for (int i = tid; i < 3 * 128; i += 32 * kSoftWarps)
-            ob[i] = i < 128 ? make_uint4(one, one, one, one) : make_uint4(0u, 0u, 0u, 0u);
+        const uint32_t one16 = F16Traits<__half>::pack(1.f, 1.f);  // the l MMA's B operand (fp16 P^T)
+        for (int i = tid; i < 4 * 128; i += 32 * kSoftWarps)
+            ob[i] = i < 128 ? make_uint4(one, one, one, one)
+                            : i >= 384 ? make_uint4(one16, one16, one16, one16) : make_uint4(0u, 0u, 0u, 0u);
         if (tid < 128) {
             s_mused[0][tid] = PP ? -INFINITY : 0.f;
             s_mused[1][tid] = PP ? -INFINITY : 0.f;
@@ -617,10 +671,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         // buffer vs V / P^T), so neither stalls the other's issue.  Each
         // tcgen05.commit tracks the MMAs of its own thread only.
         const bool bf = std::is_same<T, __nv_bfloat16>::value;
+        const bool bf2 = bf && !V16;  // GEMM2 / l MMA format (fp16 on the v16 path)
         const uint32_t id_g1_sp = umma_idesc_f16(bf, 128, 128, false, false, true);
         const uint32_t id_g1_de = umma_idesc_f16(bf, 128, 128, false, false, false);
-        const uint32_t id_g2_sp = umma_idesc_f16(bf, 128, 128, false, true, true);
-        const uint32_t id_g2_de = umma_idesc_f16(bf, 128, 128, false, true, false);
+        const uint32_t id_g2_sp = umma_idesc_f16(bf2, 128, 128, false, true, true);
+        const uint32_t id_g2_de = umma_idesc_f16(bf2, 128, 128, false, true, false);
         mbar_wait_dbg(&bar_q, 0, dbgp, 1);
         tc_fence_after();
         // Descriptor bases (start address in 16-byte units in the low 14 bits:
@@ -636,6 +691,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         // rows); LBO 0 aliases the two 8-element K halves (the rows are constant)
         const uint32_t sBias = base + lay.off_bias;
         const uint64_t dOnes = umma_desc(sBias, 0, 128, kLayoutNone);
+        const uint64_t dOnesL = V16 ? umma_desc(sBias + 3 * 2048, 0, 128, kLayoutNone) : dOnes;  // l MMA ones
         const uint64_t dBias = umma_desc(sBias + 2048, 0, 128, kLayoutNone);
         const uint32_t kst16 = lay.k_stage >> 4, vst16 = lay.v_stage >> 4, vblk16 = lay.vblk >> 4;
         bool o_started = false;
@@ -678,13 +734,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 umma_commit(&bar_vempty[s]);  // V stage free once the O^T MMAs are done
 #ifndef HS_PREFILL_XP_NO_LMMA
                 {   // row sums l[q] += sum_k P^T[q][k]: P^T as an MN-major A operand, ones as B (N = 16)
-                    const uint32_t id_l = umma_idesc_f16(bf, 128, 16, true, false, false);
+                    const uint32_t id_l = umma_idesc_f16(bf2, 128, 16, true, false, false);
                     const uint64_t pa = dP + (pbuf_of(tp) * lay.p_bytes) / 16;
 #pragma unroll
                     for (int pass = 0; pass < (HILO ? 2 : 1); ++pass)
 #pragma unroll
                         for (int kk = 0; kk < 8; ++kk)
-                            umma_f16(tmem + 416u, pa + pass * 2048 + 128 * kk, dOnes, id_l, tp > 0 || pass > 0 || kk > 0);
+                            umma_f16(tmem + 416u, pa + pass * 2048 + 128 * kk, dOnesL, id_l, tp > 0 || pass > 0 || kk > 0);
                 }
 #endif
                 umma_commit(&bar_pempty[pbuf_of(tp)]);  // P^T buffer free; O^T and l through tile tp final
@@ -890,8 +946,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     p[k + 1] = x[8 * g8 + k + 1];
                     exp2_fma2(p[k], p[k + 1]);
                 }
-                const uint4 hi = make_uint4(F16Traits<T>::pack(p[0], p[1]), F16Traits<T>::pack(p[2], p[3]),
-                                            F16Traits<T>::pack(p[4], p[5]), F16Traits<T>::pack(p[6], p[7]));
+                using PT = typename std::conditional<V16, __half, T>::type;  // P^T element type
+                const uint4 hi = make_uint4(F16Traits<PT>::pack(p[0], p[1]), F16Traits<PT>::pack(p[2], p[3]),
+                                            F16Traits<PT>::pack(p[4], p[5]), F16Traits<PT>::pack(p[6], p[7]));
                 const uint32_t pto = pt_base_h + ((static_cast<uint32_t>(g8) ^ r7) << 4);
 #ifdef HS_PREFILL_XP_NO_PSTORE
                 if (hi.x == 0x7fff7fffu)  // experiment: keep the math, drop the P^T stores
@@ -994,6 +1051,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             }
             named_bar(5, 256);  // the epilogue group only (ids 1-4 are the quads' barriers)
             float* out = L.out + (static_cast<int64_t>(u * L.gqa + h) * L.n_q + q0) * kHeadDim;
+            const int v_exp = V16 ? L.v16_scale[1] : 0;  // O^T was accumulated over V * 2^-v_exp
 #pragma unroll 1
             for (int k16 = 0; k16 < 64; k16 += 16) {
                 float v[16];
@@ -1002,7 +1060,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
 #pragma unroll
                 for (int k = 0; k < 16; ++k) {
                     const int c = c0 + k16 + k;
-                    if (c < rows_q) out[c * kHeadDim + r] = ntiles > 0 ? v[k] * s_alpha[c] : 0.f;
+                    const float o = v[k] * s_alpha[c];
+                    if (c < rows_q) out[c * kHeadDim + r] = ntiles > 0 ? (V16 ? ldexpf(o, v_exp) : o) : 0.f;
                 }
             }
         }
@@ -1273,7 +1332,7 @@ int prefill_tile_cap(int nb, int ntb) { return nb / 2 + ntb / 2 + 10; }
 
 cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
     PrefillLayout lay;
-    const bool hilo = L.bf16;
+    const bool hilo = L.bf16 && !L.v16;
     // K stage: dense 128x128 tile, or 128x64 nnz + 2 KB metadata + 2 KB E atom.
     const bool kden = L.k_dense_count > 0 || L.n_tail_blocks > 0, vden = L.v_dense_count > 0 || L.n_tail_blocks > 0;
     lay.k_meta = 0;  // unused: the metadata atoms come prepared (meta_atom_kernel)
@@ -1349,10 +1408,27 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
             if (e != cudaSuccess) return e;
         }
     }
+    if (L.v16) {
+        if (!pp) return cudaErrorInvalidConfiguration;  // the fp16 V copy serves the ping-pong kernel only
+        const int64_t na = static_cast<int64_t>(L.n_units) * L.v_dense_count * kBlock * kHeadDim / 2;
+        const int64_t nb = static_cast<int64_t>(L.n_units) * L.v_sparse_count * kBlock * kHeadDim / 4;
+        const int64_t nt = static_cast<int64_t>(L.n_units) * L.tail * kHeadDim;
+        cudaError_t e = cudaMemsetAsync(L.v16_scale, 0, 2 * sizeof(int), s);
+        if (e != cudaSuccess) return e;
+        const int grid = 148 * 8;
+        v16_absmax_kernel<<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(L.v_dense_src), na,
+                                               static_cast<const uint32_t*>(L.v_nnz_src), nb,
+                                               static_cast<const uint16_t*>(L.v_tail), nt, L.v16_scale);
+        v16_convert_kernel<<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(L.v_dense_src),
+                                                reinterpret_cast<uint32_t*>(L.v16_dense), na,
+                                                static_cast<const uint32_t*>(L.v_nnz_src),
+                                                reinterpret_cast<uint32_t*>(L.v16_nnz), nb, L.v16_scale);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     if (L.n_tail_blocks > 0) {
         tail_prep_kernel<<<dim3(L.n_tail_blocks, L.n_units), 128, 0, s>>>(
             static_cast<const uint16_t*>(L.k_tail), static_cast<const uint16_t*>(L.v_tail), L.tail, L.n_tail_blocks,
-            L.k_tail_ws, L.v_tail_ws);
+            L.k_tail_ws, L.v_tail_ws, L.v16 ? L.v16_scale : nullptr);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -1365,7 +1441,13 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
         return cudaSuccess;
     };
     cudaError_t e;
-    if (L.bf16)
+    if (L.bf16 && L.v16 && !kden && !vden)
+        e = dbg ? launch(prefill_kernel<__nv_bfloat16, false, true, true, 2>)
+                : launch(prefill_kernel<__nv_bfloat16, false, false, true, 2>);
+    else if (L.bf16 && L.v16)
+        e = dbg ? launch(prefill_kernel<__nv_bfloat16, false, true, true, 0>)
+                : launch(prefill_kernel<__nv_bfloat16, false, false, true, 0>);
+    else if (L.bf16)
         e = dbg ? launch(prefill_kernel<__nv_bfloat16, true, true, false>)
                 : launch(prefill_kernel<__nv_bfloat16, true, false, false>);
     else if (pp && !kden && !vden)  // softmax-bound: a quarter of the exponentials on the FMA pipe

@@ -43,7 +43,7 @@ torch.sum(flush, dim=0, out=sink)
 os.environ["HS_DECODE_TIMES"] = "/tmp/dtimes.bin"
 hs.decode_attention(q, kc, vc, out=out)
 torch.cuda.synchronize()
-t = np.fromfile("/tmp/dtimes.bin", dtype=np.int64).reshape(-1, 8).astype(np.float64)
+t = np.fromfile("/tmp/dtimes.bin", dtype=np.int64).reshape(-1, 16).astype(np.float64)
 t0 = t[:, 0].min()
 t = np.where(t > 0, t - t0, np.nan)
 t /= 1000.0  # us
@@ -52,5 +52,6 @@ print(f"CTAs {len(t)}  start: min {t[:,0].min():.1f} max {t[:,0].max():.1f} us |
       f"max {t[:,2].max():.1f} | partial written: max {np.nanmax(t[:,3]):.1f} | combine done: max {np.nanmax(t[:,4]):.1f} us")
 print("loop-end percentiles (10/25/50/75/90/100):", np.percentile(t[:, 2], [10, 25, 50, 75, 90, 100]).round(1))
 last = ~np.isnan(t[:, 4])
-for row in t[last]:
-    print(f"combine CTA: partial {row[3]:.1f} fence1 {row[7]:.1f} ticket {row[5]:.1f} fence2 {row[6]:.1f} done {row[4]:.1f}")
+for row in t[last][:12]:
+    print(f"combine CTA: loop end {row[2]:.1f} partial {row[3]:.1f} fence1 {row[7]:.1f} ticket {row[5]:.1f} "
+          f"m/l loaded {row[8]:.1f} weights {row[9]:.1f} O summed {row[10]:.1f} done {row[4]:.1f}")
