@@ -2,7 +2,7 @@
 # One GPU-box pass: parity tests, smoke, bench (both arms), ncu launch list and
 # full captures of the decode / prefill / compress kernels.  Outputs -> gpurun_out/.
 # Usage: bash tools/gpu_round.sh [tag]
-TAG=${1:-r01}
+TAG=${1:-r02}
 O=gpurun_out/$TAG
 mkdir -p $O
 nvidia-smi > $O/smi.txt 2>&1
@@ -12,8 +12,6 @@ timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo 
 timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "rc=$?" >> $O/bench.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
-timeout 600 python bench.py --workload config4 --skip-cpu > $O/bench_config4.json 2> $O/bench_config4.err
-timeout 600 python bench.py --workload config5 --skip-cpu > $O/bench_config5.json 2> $O/bench_config5.err
 NCU=/usr/local/cuda/bin/ncu
 timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
    python bench.py --steps 2 --warmup 3 --profile --prefill-steps 1 > $O/ncu_launch_bench.log 2>&1
