@@ -884,8 +884,9 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
         const size_t vd16 = L.v16 ? static_cast<size_t>(v->n_units) * v->dense_count * hs::kBlock * hs::kHeadDim * 2 : 0;
         const size_t vn16 = L.v16 ? static_cast<size_t>(v->n_units) * v->sparse_count * hs::kBlock * hs::kHeadDim : 0;
         const size_t a256 = 256;
+        const size_t nredo = static_cast<size_t>((n_q + 127) / 128) * gqa * k->n_units * sizeof(int);
         uint8_t* ws = static_cast<uint8_t*>(
-            workspace(s, kb + vb + 2 * tb + vd16 + vn16 + 4 * a256, kWsPrefill, &st));
+            workspace(s, kb + vb + 2 * tb + vd16 + vn16 + nredo + 5 * a256, kWsPrefill, &st));
         if (st) return st;
         L.k_meta_hw = reinterpret_cast<uint16_t*>(ws);
         L.v_meta_hw = reinterpret_cast<uint16_t*>(ws + kb);
@@ -895,6 +896,7 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
         L.v16_dense = reinterpret_cast<uint16_t*>(p16);
         L.v16_nnz = reinterpret_cast<uint16_t*>(p16 + vd16);
         L.v16_scale = reinterpret_cast<int*>(p16 + vd16 + vn16);
+        L.redo = reinterpret_cast<int*>(p16 + ((vd16 + vn16 + 2 * sizeof(int) + a256 - 1) / a256) * a256);
         L.v_dense_src = v->dense_pool;
         L.v_nnz_src = v->nnz_pool;
     }
@@ -931,11 +933,9 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     ok &= make_map_halves(&L.tm_ktail, ntb ? L.k_tail_ws : nullptr, U * ntb * 64, 128);
     ok &= make_map(&L.tm_vtail, ntb ? L.v_tail_ws : nullptr, 64, U * ntb * 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     if (!ok) return fail(HS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    cudaError_t e = hs::launch_prefill(L, s);
-    count_launch();
-    count_launch();  // metadata atom-order pass + the attention kernel
-    if (L.n_tail_blocks > 0) count_launch();  // dense-tail layout pass
-    if (L.v16) count_launch(2);               // fp16 V copy: scale + convert
+    int n_kernels = 0;
+    cudaError_t e = hs::launch_prefill(L, s, &n_kernels);
+    count_launch(n_kernels);
     if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
     if (L.trace) {
         static std::vector<long long> host(4096 * 16);

@@ -146,6 +146,10 @@ struct PrefillLaunch {
     uint16_t* v16_nnz;
     int* v16_scale;           // workspace: [0] = max bf16 magnitude bits, [1] = v_exp
     float* out;
+    // workspace, one int per CTA (zeroed by launch_prefill): the ping-pong kernel
+    // flags a CTA whose output rows came out non-finite; a second SAFE pass
+    // recomputes exactly those CTAs with the race-free running-max exchange
+    int* redo;
     int* dbg;                // optional pipeline watchdog record (debug)
     int mode;                // tools only: 1 = softmax skipped, 2 = MMAs skipped, 3 = both
     long long* trace;        // optional per-tile event clocks of CTA (0,0,0) (tools)
@@ -153,7 +157,8 @@ struct PrefillLaunch {
     // tm_vnnz2 / tm_vden2 box two consecutive V pool slots (256 rows).
     CUtensorMap tm_q, tm_knnz, tm_kden, tm_vnnz, tm_vden, tm_ktail, tm_vtail, tm_vnnz2, tm_vden2;
 };
-cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s);
+// *n_kernels: kernels launched (prep passes, the attention kernel, the SAFE pass)
+cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s, int* n_kernels);
 
 // Attention for shapes outside the tcgen05 / mma.sp kernels' specialisation
 // (block_size != 64 or head_dim != 128): attend_range (attention.hpp:249-304)

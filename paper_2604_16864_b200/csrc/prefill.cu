@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(256) v16_convert_kernel(const uint32_t* __rest
     }
 }
 
-template <typename T, bool HILO, bool DBG, bool PP, int POLY = kPolyPer8>
+template <typename T, bool HILO, bool DBG, bool PP, int POLY = kPolyPer8, bool SAFE = false>
 __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_constant__ PrefillLaunch L,
                                                                PrefillLayout lay) {
     // DBG: tools-only instrumentation (per-tile trace, watchdog waits, mode
@@ -406,8 +406,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     __shared__ float s_delta[128], s_alpha[128], s_mrun[128], s_mused[2][128];
     __shared__ uint16_t s_bq[128];
     __shared__ int s_g2_issued;  // GEMM2 tiles issued (kG2First ordering)
+    __shared__ int s_bad;        // ping-pong: some output row of this CTA came out non-finite
     __shared__ typename std::conditional<PP, PPShared, PPNone>::type pps;  // ping-pong softmax state
 
+    if constexpr (SAFE) {  // only the CTAs the fast pass flagged
+        if (L.redo[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] == 0) return;
+    }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     const int n_tiles_q = (L.n_q + 127) / 128;
     const int qt = n_tiles_q - 1 - static_cast<int>(blockIdx.x);  // heaviest causal tiles first
@@ -429,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     if (warp == kWarpMma) tmem_alloc(&s_tmem, 512);
     if (tid == 0) {
         s_g2_issued = 0;
+        s_bad = 0;
         mbar_init(&bar_q, 1);
         for (int s = 0; s < nk; ++s) {
             mbar_init(&bar_kfull[s], 1);
@@ -968,11 +973,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 }
             }
             if (tr0) trace(L, t, 12);
+            bool need = false;
+            if constexpr (!SAFE) {
             // ---- publish the m this tile used; O^T / l to it when tile t-1 used another
             // (between GEMM2(t-1) and GEMM2(t)).  Per-column compare of exact values:
             // a version match alone does not imply equal values across the groups.
             if (r < 64) s_mt[grp][slot][c0 + r] = s_mused[grp][c0 + r];
-            bool need = false;
+            need = false;
             if (t >= 1) {
                 const int pg = grp ^ 1, ps = ((t - 1) >> 1) & 1;
                 if (lane == 0) {
@@ -996,17 +1003,71 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             }
             need = bar_red_or(bar_id, need);  // also: this quad's s_mt values are all stored
             if (r == 0) st_release(&s_tdone[grp][slot][ch], t);
+            } else {
+            // ---- SAFE pass: the tile's m is m_t = max(m_used, m_{t-1}) per column, so
+            // O^T / l are only ever rescaled by exp2(m_{t-1} - m_t) <= 1 (between
+            // GEMM2(t-1) and GEMM2(t)).  When the other group grew a column after this
+            // group's snapshot (m_{t-1} > m_used; this group's next tile sees the
+            // version bump), the P^T values just stored are lowered to m_t instead.
+            if (t >= 1) {
+                const int pg = grp ^ 1, ps = ((t - 1) >> 1) & 1;
+                if (lane == 0) {
+                    while (ld_acquire_cta(&s_tdone[pg][ps][ch]) != t - 1) __nanosleep(32);
+                }
+                __syncwarp();
+                if (r < 64) {
+                    const int c = c0 + r;
+                    const float mp = s_mt[pg][ps][c], mu = s_mused[grp][c];
+                    // mu = -inf: every logit of the column so far is masked (P = 0)
+                    const float me = mu == -INFINITY ? mp : fmaxf(mu, mp);
+                    const float pscale = (mu != -INFINITY && me > mu) ? fast_exp2(mu - me) : 1.f;
+                    const float al = (mp == -INFINITY || me == mp) ? 1.f : fast_exp2(mp - me);
+                    s_mt[grp][slot][c] = me;
+                    // P^T factor in the slow path's scratch (every read of it is behind
+                    // the slow path's last quad barrier)
+                    s_red2[grp][0][c] = pscale;
+                    s_al[grp][c] = al;
+                    need = pscale != 1.f || al != 1.f;
+                }
+            } else if (r < 64) {
+                s_mt[grp][slot][c0 + r] = s_mused[grp][c0 + r];
+            }
+            need = bar_red_or(bar_id, need);  // also: this quad's s_mt / P^T factors / s_al values are all stored
+            if (r == 0) st_release(&s_tdone[grp][slot][ch], t);
+            }
             if (need) {
                 if (DBG && dbgp && r == 0) atomicAdd(dbgp + 9, 1);
+                if constexpr (SAFE) {  // P^T of this tile to m_t (this thread's own chunks; 1 where unchanged)
+                    uint8_t* const pbuf = pbuf0 + sb * lay.p_bytes;
+                    using PT = typename std::conditional<V16, __half, T>::type;
+#pragma unroll 1
+                    for (int g8 = 0; g8 < 8; ++g8) {
+                        uint4* const pp = reinterpret_cast<uint4*>(pbuf + pt_base_h + ((static_cast<uint32_t>(g8) ^ r7) << 4));
+                        uint4 w = *pp;
+                        uint32_t* wv = &w.x;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float a = F16Traits<PT>::to_float(static_cast<uint16_t>(wv[k] & 0xFFFF)) *
+                                            s_red2[grp][0][c0 + 8 * g8 + 2 * k];
+                            const float b = F16Traits<PT>::to_float(static_cast<uint16_t>(wv[k] >> 16)) *
+                                            s_red2[grp][0][c0 + 8 * g8 + 2 * k + 1];
+                            wv[k] = F16Traits<PT>::pack(a, b);
+                        }
+                        *pp = w;
+                    }
+                }
                 const int pg = grp ^ 1, ps = ((t - 1) >> 1) & 1;
                 mbar_wait_dbg(&bar_pempty[pg], ((t - 1) >> 1) & 1, dbgp, 23);  // GEMM2(t-1) complete
                 tc_fence_after();
-                if (r < 64) {
-                    const int c = c0 + r;
-                    const float mp = s_mt[pg][ps][c], mt = s_mused[grp][c];
-                    s_al[grp][c] = (mp == -INFINITY || mt == -INFINITY) ? 1.f : fast_exp2(mp - mt);
+                if constexpr (!SAFE) {
+                    if (r < 64) {
+                        const int c = c0 + r;
+                        const float mp = s_mt[pg][ps][c], mt = s_mused[grp][c];
+                        s_al[grp][c] = (mp == -INFINITY || mt == -INFINITY) ? 1.f : fast_exp2(mp - mt);
+                    }
+                    named_bar(bar_id, 128);
                 }
-                named_bar(bar_id, 128);
+                (void)ps;
 #pragma unroll 1
                 for (int k8 = 0; k8 < 64; k8 += 8) {
                     uint32_t v[8];
@@ -1052,6 +1113,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             named_bar(5, 256);  // the epilogue group only (ids 1-4 are the quads' barriers)
             float* out = L.out + (static_cast<int64_t>(u * L.gqa + h) * L.n_q + q0) * kHeadDim;
             const int v_exp = V16 ? L.v16_scale[1] : 0;  // O^T was accumulated over V * 2^-v_exp
+            bool bad = false;  // a non-finite row: flag this CTA for the SAFE pass
 #pragma unroll 1
             for (int k16 = 0; k16 < 64; k16 += 16) {
                 float v[16];
@@ -1061,9 +1123,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 for (int k = 0; k < 16; ++k) {
                     const int c = c0 + k16 + k;
                     const float o = v[k] * s_alpha[c];
+                    bad |= c < rows_q && !(fabsf(o) <= 3.4e38f);
                     if (c < rows_q) out[c * kHeadDim + r] = ntiles > 0 ? (V16 ? ldexpf(o, v_exp) : o) : 0.f;
                 }
             }
+            if (!SAFE && bad) s_bad = 1;  // published to L.redo after the final barrier
         }
     } else {
         // ------------------------------------------------------- softmax WGs
@@ -1324,14 +1388,16 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     tc_fence_before();
     __syncthreads();
     if (warp == kWarpMma) tmem_dealloc(tmem, 512);
+    if (PP && !SAFE && tid == 0 && s_bad) L.redo[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = 1;
 }
 
 }  // namespace
 
 int prefill_tile_cap(int nb, int ntb) { return nb / 2 + ntb / 2 + 10; }
 
-cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
+cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s, int* n_kernels) {
     PrefillLayout lay;
+    *n_kernels = 0;
     const bool hilo = L.bf16 && !L.v16;
     // K stage: dense 128x128 tile, or 128x64 nnz + 2 KB metadata + 2 KB E atom.
     const bool kden = L.k_dense_count > 0 || L.n_tail_blocks > 0, vden = L.v_dense_count > 0 || L.n_tail_blocks > 0;
@@ -1404,6 +1470,7 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
         const int kb = L.n_units * L.k_sparse_count, vb = L.n_units * L.v_sparse_count;
         if (kb + vb > 0) {
             meta_atom_kernel<<<kb + vb, 128, 0, s>>>(L.k_meta, kb, L.v_meta, vb, L.k_meta_hw, L.v_meta_hw);
+            ++*n_kernels;
             cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) return e;
         }
@@ -1423,12 +1490,14 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
                                                 reinterpret_cast<uint32_t*>(L.v16_dense), na,
                                                 static_cast<const uint32_t*>(L.v_nnz_src),
                                                 reinterpret_cast<uint32_t*>(L.v16_nnz), nb, L.v16_scale);
+        *n_kernels += 2;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (L.n_tail_blocks > 0) {
         tail_prep_kernel<<<dim3(L.n_tail_blocks, L.n_units), 128, 0, s>>>(
             static_cast<const uint16_t*>(L.k_tail), static_cast<const uint16_t*>(L.v_tail), L.tail, L.n_tail_blocks,
             L.k_tail_ws, L.v_tail_ws, L.v16 ? L.v16_scale : nullptr);
+        ++*n_kernels;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -1438,22 +1507,39 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e) return e;
         kern<<<grid, kThreads, smem, s>>>(L, lay);
+        ++*n_kernels;
         return cudaSuccess;
+    };
+    // Ping-pong launches: the fast pass, then the SAFE pass over the CTAs it flagged
+    // (every other CTA of the SAFE grid exits at once; a few microseconds).
+    auto launch_pp = [&](auto fast, auto safe) -> cudaError_t {
+        cudaError_t e = cudaMemsetAsync(L.redo, 0, sizeof(int) * grid.x * grid.y * grid.z, s);
+        if (e) return e;
+        if ((e = launch(fast)) != cudaSuccess) return e;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if (getenv("HS_PREFILL_NO_SAFE")) return cudaSuccess;  // tools: timing of the fast pass alone
+        if (getenv("HS_PREFILL_FORCE_SAFE"))  // tests: every CTA recomputed by the SAFE pass
+            if ((e = cudaMemsetAsync(L.redo, 1, sizeof(int) * grid.x * grid.y * grid.z, s)) != cudaSuccess) return e;
+        return launch(safe);
     };
     cudaError_t e;
     if (L.bf16 && L.v16 && !kden && !vden)
         e = dbg ? launch(prefill_kernel<__nv_bfloat16, false, true, true, 2>)
-                : launch(prefill_kernel<__nv_bfloat16, false, false, true, 2>);
+                : launch_pp(prefill_kernel<__nv_bfloat16, false, false, true, 2>,
+                            prefill_kernel<__nv_bfloat16, false, false, true, 2, true>);
     else if (L.bf16 && L.v16)
         e = dbg ? launch(prefill_kernel<__nv_bfloat16, false, true, true, 0>)
-                : launch(prefill_kernel<__nv_bfloat16, false, false, true, 0>);
+                : launch_pp(prefill_kernel<__nv_bfloat16, false, false, true, 0>,
+                            prefill_kernel<__nv_bfloat16, false, false, true, 0, true>);
     else if (L.bf16)
         e = dbg ? launch(prefill_kernel<__nv_bfloat16, true, true, false>)
                 : launch(prefill_kernel<__nv_bfloat16, true, false, false>);
     else if (pp && !kden && !vden)  // softmax-bound: a quarter of the exponentials on the FMA pipe
-        e = dbg ? launch(prefill_kernel<__half, false, true, true, 2>) : launch(prefill_kernel<__half, false, false, true, 2>);
+        e = dbg ? launch(prefill_kernel<__half, false, true, true, 2>)
+                : launch_pp(prefill_kernel<__half, false, false, true, 2>, prefill_kernel<__half, false, false, true, 2, true>);
     else if (pp)  // ring-bound (dense stages): every exponential on the SFU (2.5% faster than a quarter)
-        e = dbg ? launch(prefill_kernel<__half, false, true, true, 0>) : launch(prefill_kernel<__half, false, false, true, 0>);
+        e = dbg ? launch(prefill_kernel<__half, false, true, true, 0>)
+                : launch_pp(prefill_kernel<__half, false, false, true, 0>, prefill_kernel<__half, false, false, true, 0, true>);
     else
         e = dbg ? launch(prefill_kernel<__half, false, true, false>) : launch(prefill_kernel<__half, false, false, false>);
     if (e) return e;

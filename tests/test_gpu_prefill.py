@@ -216,3 +216,48 @@ def test_prefill_random_shapes(hs, port, seed):
         want = np.stack(parallel(one, range(U * gqa))).reshape(U, gqa, n_q, 128)
         mx, mr = err_stats(got, want)
         assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (L, n_q, s, sink, window, causal, U, gqa, mx, mr)
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("s", [1.0, 0.5])
+def test_prefill_safe_pass(hs, port, dtype, s, monkeypatch):
+    """The SAFE pass (race-free running-max exchange, every CTA recomputed) on
+    growing scores and random shapes: the ping-pong kernel re-runs the CTAs whose
+    rows came out non-finite through it, so it must match the oracle on its own."""
+    monkeypatch.setenv("HS_PREFILL_FORCE_SAFE", "1")
+    test_prefill_growing_scores(hs, port, dtype, s, True)
+    kc, vc, q = setup(hs, port, 2, 1024, s, dtype, 2, 700, 64, 128, seed=5)
+    scale = np.float32(1.0 / math.sqrt(128))
+    got = hs.prefill_attention(to_torch(q, dtype), kc, vc, causal=True, scale=float(scale)).cpu().numpy()
+
+    def one(ug):
+        u, g = divmod(ug, 2)
+        return port.prefill(q[u, g], device_to_oracle(kc, u), device_to_oracle(vc, u), None, None, True, scale, 64)
+    want = np.stack(parallel(one, range(4))).reshape(2, 2, 700, 128)
+    mx, mr = err_stats(got, want)
+    assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_prefill_extreme_jumps(hs, port, dtype):
+    """Column maxima that jump by hundreds of log2 units late in the sequence
+    (hot key blocks scaled far above the rest): whichever group sees the jump
+    first, the result (fast pass plus the SAFE pass it may trigger) matches."""
+    U, gqa, L, n_q = 1, 2, 2048, 2048
+    kx = np.stack([port.random_gaussian(L, 128, port.head_seed(21, u, 0)) for u in range(U)])
+    for b0 in (640, 1216, 1792):
+        kx[:, b0:b0 + 64] *= 48.0
+    kx = port.round_to(kx.astype(np.float32), dtype)
+    vx = gen_units(port, U, L, 128, 21, 1, dtype)
+    kc, vc = hs.prune_cache(to_torch(kx, dtype), to_torch(vx, dtype), hs.SparsityConfig(1.0, 1.0, 64))
+    q = np.stack([np.stack([port.round_to(port.random_gaussian(n_q, 128, port.head_seed(21, u, 2 + g)) * 6.0, dtype)
+                            for g in range(gqa)]) for u in range(U)])
+    scale = np.float32(1.0 / math.sqrt(128))
+    got = hs.prefill_attention(to_torch(q, dtype), kc, vc, causal=True, scale=float(scale)).cpu().numpy()
+    assert np.isfinite(got).all()
+
+    def one(g):
+        return port.prefill(q[0, g], device_to_oracle(kc, 0), device_to_oracle(vc, 0), None, None, True, scale, 64)
+    want = np.stack(parallel(one, range(gqa)))[None]
+    mx, mr = err_stats(got, want)
+    assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)

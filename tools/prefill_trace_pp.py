@@ -42,6 +42,7 @@ print("MMA: GEMM1 issue->S full e0-e4 %.0f | check(t)->GEMM1(t+2) issue e4(t+2)-
       % (gap(4, 0), med(tr[st + 2, 4] - tr[st, 2]), gap(14, 6), med(tr[st + 2, 3] - tr[st, 6])))
 print("K: K(t) TMA issue -> landed e10-e7 %.0f | MMA top->K landed wait e10-e11 %.0f"
       % (gap(7, 10), gap(11, 10)))
+print("median event offsets from e0(t):", " ".join(f"e{e}={med(tr[st, e] - tr[st, 0]):+.0f}" for e in (11, 7, 10, 4, 0, 1, 2, 13, 12, 3, 14, 5, 6)))
 for t in (n // 2, n // 2 + 1, n // 2 + 2, n // 2 + 3):
     b = tr[t, 0]
     print(t, " ".join(f"e{e}={tr[t, e] - b:+d}" for e in (11, 7, 10, 4, 0, 1, 2, 3, 12, 13, 14, 5, 6) if tr[t, e] > 0))
