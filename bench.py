@@ -53,6 +53,17 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+def sustained_tflops():
+    """MEASURED_PEAKS.json's sustained dense bf16 figure (cuBLAS back to back for
+    seconds, power-capped clocks): the denominator for kernels timed inside long
+    runs, beside the burst figure (B200_PROFILING.md)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops_sustained"])
+    except Exception:  # noqa: BLE001
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -373,6 +384,7 @@ def leg_prefill(hs, D_, dev, rank, world, args):
     positions (attention.hpp:249-253) on rank 0."""
     import torch
     _, dense_peak, peak_kind = peaks()
+    sustained_peak = sustained_tflops()
     heads = D_.heads_of_rank(8, world, rank)
     Up, G = heads.size, 4
     res = {}
@@ -391,15 +403,18 @@ def leg_prefill(hs, D_, dev, rank, world, args):
             kc, vc = hs.prune_cache(key, val, hs.SparsityConfig(s, s, 64))
             flops = sum(hs.flop_and_byte_count(Lp, kc, vc, 0, True, unit=u)[0] for u in range(Up)) * G
             barrier(world)
-            times = time_steps(lambda: hs.prefill_attention(q, kc, vc, causal=True, out=out), args.prefill_steps, 1)
+            with ClockSampler(dev.index or 0) as cs:
+                times = time_steps(lambda: hs.prefill_attention(q, kc, vc, causal=True, out=out),
+                                   args.prefill_steps, 3)
             ms = max_over_ranks(statistics.median(times), world)
             total = sum_over_ranks(flops, world)
             tflops = total / (ms * 1e-3) / 1e12
             entry = {"ms": round(ms, 3), "counted_tflops": round(tflops, 1), "frac": round(tflops / dense_peak, 4),
-                     "counted_flops": int(total)}
+                     "frac_of_sustained": round(tflops / sustained_peak, 4) if sustained_peak else None,
+                     "counted_flops": int(total), "clocks": cs.summary()}
             if rank == 0 and not args.skip_cpu and Lp <= 2 * args.prefill_ctx:
                 entry["parity"] = prefill_parity(hs, q, out, kc, vc, key, val, dt,
-                                                 rows=64 if Lp > args.prefill_ctx else 96,
+                                                 rows=64 if Lp > args.prefill_ctx else 256,
                                                  heads=[(0, 0), (Up - 1, G - 1)] if Lp <= args.prefill_ctx
                                                  else [(0, 1)])
             by[str(s)] = entry
