@@ -19,6 +19,9 @@ namespace hs {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef HS_COMPRESS_MINB
+#define HS_COMPRESS_MINB 8  // 32 registers: 8 CTAs per SM (+4% at S = 1 against 6)
+#endif
 
 // Top-2-of-4 by magnitude with the stable-sort tie rule (pruner.hpp:53-74):
 // element i is kept iff #{j: |x_j|>|x_i|} + #{j<i: |x_j|==|x_i|} < 2.
@@ -241,7 +244,7 @@ __device__ double sequential_loss_in(const PackArgs& a, int u, int b) {
 }
 
 template <typename T, int AXIS, int MODE, int SRC>
-__global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
+__global__ void __launch_bounds__(kThreads, HS_COMPRESS_MINB) block_kernel(PackArgs a) {
     const int b = blockIdx.x, u = blockIdx.y, t = threadIdx.x;
     // SRC 1: blocks past the input cache come from the dense source (a tail's
     // full blocks absorbed into the cache)
@@ -251,6 +254,20 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
                                    : nullptr;
     __shared__ double s_sum[kThreads / 32];
     __shared__ int s_min[kThreads / 32];
+    // SRC 0: the 16 KB source block lands in shared memory by one bulk copy issued
+    // first thing (no registers hold in-flight data, so the 32-register budget
+    // keeps 8 CTAs per SM while every CTA's block is in flight at once)
+    __shared__ __align__(128) uint16_t tile[kBlock * kHeadDim];
+    __shared__ __align__(8) uint64_t s_bar;
+    if (SRC == 0) {
+        if (t == 0) {
+            mbar_init(&s_bar, 1);
+            fence_barrier_init();
+            mbar_arrive_expect_tx(&s_bar, kBlock * kHeadDim * 2);
+            tma_bulk_g2s(tile, blk, kBlock * kHeadDim * 2, &s_bar);
+        }
+        __syncthreads();  // barrier initialised before anyone waits on it
+    }
     // SRC 1: the input block (dense slot or nnz + metadata of a sparse slot)
     int in_e = 0;
     const uint16_t *in_den = nullptr, *in_nnz = nullptr, *in_meta = nullptr;
@@ -280,8 +297,12 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
         slot = (e > 0 ? e : -e) - 1;
         // a block mask whose dense count differs from the pool capacity was
         // reported by assign_slots_kernel; never write past a pool
-        if (e == 0 || slot >= (dense ? a.dense_count : a.sparse_count)) return;
+        if (e == 0 || slot >= (dense ? a.dense_count : a.sparse_count)) {
+            if (SRC == 0) mbar_wait(&s_bar, 0);  // no bulk copy may outlive the CTA
+            return;
+        }
     }
+    if (SRC == 0) mbar_wait(&s_bar, 0);
     constexpr bool kLoss = MODE != 1;
     LossAcc acc;
 
@@ -343,7 +364,9 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
         for (int p = 0; p < 4; ++p) {
             const int r = p * 16 + (t >> 4);
             uint4& v = vr[p];
-            if (from_src) {
+            if (SRC == 0) {
+                v = *reinterpret_cast<const uint4*>(tile + r * kHeadDim + c * 8);
+            } else if (from_src) {
                 v = *reinterpret_cast<const uint4*>(blk + r * kHeadDim + c * 8);
             } else if (in_e > 0) {
                 v = *reinterpret_cast<const uint4*>(in_den + r * kHeadDim + c * 8);
@@ -382,10 +405,11 @@ __global__ void __launch_bounds__(kThreads) block_kernel(PackArgs a) {
         }
     } else {
         // Value cache: groups of 4 tokens down a channel; stored transposed [d][B].
-        __shared__ __align__(16) uint16_t tile[kBlock * kHeadDim];
         const int c = t & 127;  // channel
         const int h = t >> 7;   // token half: groups 8h..8h+7
-        if (from_src) {
+        if (SRC == 0) {
+            // staged by the bulk copy
+        } else if (from_src) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int chunk = t + i * kThreads;  // 1024 chunks of 8 elements
