@@ -121,6 +121,21 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 // 3-D view of a row-major [outer][128] 16-bit array as [2 halves][outer][64]
 // (half stride 128 B): one box {64, box_outer, 2} lands as the two SW128
 // column-half tiles [half][row][64] a K-major UMMA operand of K = 128 expects.
+// 4-D view of the queries [unit*gqa + head][n_q][128] as [half][head][query][64]:
+// one box {64, qt, hg, 2} is the SW128 K-major B operand of a GEMM1 over hg
+// stacked heads (hg * qt = 128 rows); queries past n_q are zero-filled.
+bool make_map_q(CUtensorMap* m, const void* ptr, uint64_t n_q, uint64_t heads, uint32_t qt, uint32_t hg) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {64, n_q, heads, 2};
+    cuuint64_t strides[3] = {256, 256 * n_q, 128};
+    cuuint32_t box[4] = {64, qt, hg, 2};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(ptr), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map_halves(CUtensorMap* m, const void* ptr, uint64_t outer, uint32_t box_outer) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
@@ -859,6 +874,14 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     L.nb = k->logical_blocks;
     L.gqa = gqa;
     L.n_q = n_q;
+    // GQA stacking: hg heads of one KV head per CTA, 128 / hg queries
+    // each, so a K/V tile is staged once for hg query heads
+    L.hg = gqa % 4 == 0 ? 4 : gqa % 2 == 0 ? 2 : 1;
+    if (const char* env = getenv("HS_PREFILL_HG")) {  // tools: A/B of the stacking factor
+        const int g = atoi(env);
+        if ((g == 1 || g == 2 || g == 4) && gqa % g == 0) L.hg = g;
+    }
+    L.qt = 128 / L.hg;
     L.tail = static_cast<int>(tail);
     L.n_tail_blocks = static_cast<int>((tail + hs::kBlock - 1) / hs::kBlock);
     L.k_tail = k_tail;
@@ -884,7 +907,7 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
         const size_t vd16 = L.v16 ? static_cast<size_t>(v->n_units) * v->dense_count * hs::kBlock * hs::kHeadDim * 2 : 0;
         const size_t vn16 = L.v16 ? static_cast<size_t>(v->n_units) * v->sparse_count * hs::kBlock * hs::kHeadDim : 0;
         const size_t a256 = 256;
-        const size_t nredo = static_cast<size_t>((n_q + 127) / 128) * gqa * k->n_units * sizeof(int);
+        const size_t nredo = static_cast<size_t>((n_q + L.qt - 1) / L.qt) * (gqa / L.hg) * k->n_units * sizeof(int);
         uint8_t* ws = static_cast<uint8_t*>(
             workspace(s, kb + vb + 2 * tb + vd16 + vn16 + nredo + 5 * a256, kWsPrefill, &st));
         if (st) return st;
@@ -916,7 +939,7 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     L.mode = 0;
     if (const char* env = getenv("HS_PREFILL_MODE")) L.mode = atoi(env);
     const uint64_t U = k->n_units;
-    bool ok = make_map(&L.tm_q, q, 128, U * gqa * n_q, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    bool ok = make_map_q(&L.tm_q, q, n_q, U * gqa, static_cast<uint32_t>(L.qt), static_cast<uint32_t>(L.hg));
     // K tiles are two consecutive pool slots (128 rows) per TMA; a single-block
     // tile's second half is masked in the kernel (and zero-filled past the pool).
     ok &= make_map(&L.tm_knnz, k->nnz_pool, 64, U * k->sparse_count * 64, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);

@@ -179,6 +179,15 @@ __device__ __forceinline__ void tma_tile3_g2s(void* dst, const CUtensorMap* map,
         : "memory");
 }
 
+__device__ __forceinline__ void tma_tile4_g2s(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                              int32_t c2, int32_t c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // L2 prefetch of a contiguous global range (no shared memory involved).
 __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");

@@ -479,63 +479,52 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     if (L.out == nullptr) return;
 
     // ---------------- combine the unit's splits (attention.hpp:387-407) ----------------
-    // Two rounds of independent L2 loads: the (m, l) of every split and row go to
-    // shared memory once per CTA (weights exp(m_s - M) and the merged l computed
-    // once), then each output column loads its nsplit O values and sums them.
+    // One thread per output column, registers only: the (m, l, O) of every split
+    // are independent L2 loads issued together (chunks of 16 splits, online LSE
+    // across chunks), so the combine costs about one L2 round trip and no CTA
+    // barriers (the former shared-memory weight table took ~5 us at configs[1]).
     const float* P = L.partial + static_cast<int64_t>(u) * L.nsplit * stride_p;
-    float* s_wt = reinterpret_cast<float*>(base_ptr);  // [nsplit][gqa] weights (the ring is free)
-    float* s_M = s_wt + L.nsplit * kMaxGqa;             // [gqa] merged max (natural-log units)
-    float* s_L = s_M + kMaxGqa;                         // [gqa] merged l
     auto combine_slice = [&](int lo, int hi) {
         constexpr float kLog2e = 1.4426950408889634f;
-        const int nsg = L.nsplit * gqa;
-        for (int i = threadIdx.x; i < nsg; i += nthr) {
-            const float* ps = P + static_cast<int64_t>(i / gqa) * stride_p + (i % gqa) * (kHeadDim + 2);
-            s_wt[i] = __ldcg(ps + kHeadDim);  // m_s, then the weight
-            s_wt[nsg + i] = __ldcg(ps + kHeadDim + 1);  // l_s (scratch past the weights)
-        }
-        __syncthreads();
-        if (ct && threadIdx.x == 0) ct[8] = globaltimer();
-        if (threadIdx.x < gqa) {
-            const int qq = threadIdx.x;
-            float M = -INFINITY;
-            for (int sp = 0; sp < L.nsplit; ++sp) M = fmaxf(M, s_wt[sp * gqa + qq]);
-            float lsum = 0.f;
-            for (int sp = 0; sp < L.nsplit; ++sp) {
-                const float m = s_wt[sp * gqa + qq];
-                lsum += m == -INFINITY ? 0.f : s_wt[nsg + sp * gqa + qq] * fast_exp2((m - M) * kLog2e);
-            }
-            s_M[qq] = M;
-            s_L[qq] = lsum;
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < nsg; i += nthr) {
-            const float m = s_wt[i];
-            s_wt[i] = m == -INFINITY ? 0.f : fast_exp2((m - s_M[i % gqa]) * kLog2e);
-        }
-        __syncthreads();
-        if (ct && threadIdx.x == 0) ct[9] = globaltimer();
         for (int idx = lo + threadIdx.x; idx < hi; idx += nthr) {
             const int qq = idx / kHeadDim, c = idx % kHeadDim;
-            const float* pq = P + qq * (kHeadDim + 2) + c;
-            float acc = 0.f;
+            const float* pq = P + qq * (kHeadDim + 2);
+            float M = -INFINITY, acc = 0.f, lsum = 0.f;
             for (int sp0 = 0; sp0 < L.nsplit; sp0 += 16) {
-                float ov[16];
+                float mv[16], lv[16], ov[16];
 #pragma unroll
-                for (int x = 0; x < 16; ++x)
-                    ov[x] = sp0 + x < L.nsplit ? __ldcg(pq + static_cast<int64_t>(sp0 + x) * stride_p) : 0.f;
+                for (int x = 0; x < 16; ++x) {
+                    const bool in = sp0 + x < L.nsplit;
+                    const float* ps = pq + static_cast<int64_t>(sp0 + x) * stride_p;
+                    mv[x] = in ? __ldcg(ps + kHeadDim) : -INFINITY;
+                    lv[x] = in ? __ldcg(ps + kHeadDim + 1) : 0.f;
+                    ov[x] = in ? __ldcg(ps + c) : 0.f;
+                }
+                float Mc = M;
 #pragma unroll
-                for (int x = 0; x < 16; ++x)
-                    if (sp0 + x < L.nsplit) acc += ov[x] * s_wt[(sp0 + x) * gqa + qq];
+                for (int x = 0; x < 16; ++x) Mc = fmaxf(Mc, mv[x]);
+                if (Mc == -INFINITY) continue;  // every split so far empty
+                if (M != Mc) {
+                    const float r = M == -INFINITY ? 0.f : fast_exp2((M - Mc) * kLog2e);
+                    acc *= r;
+                    lsum *= r;
+                    M = Mc;
+                }
+#pragma unroll
+                for (int x = 0; x < 16; ++x) {
+                    const float wt = mv[x] == -INFINITY ? 0.f : fast_exp2((mv[x] - M) * kLog2e);
+                    acc = fmaf(ov[x], wt, acc);
+                    lsum = fmaf(lv[x], wt, lsum);
+                }
             }
             if (L.out_mode == 0) {
-                L.out[(static_cast<int64_t>(u) * L.q_rows + qq) * kHeadDim + c] = acc / s_L[qq];
+                L.out[(static_cast<int64_t>(u) * L.q_rows + qq) * kHeadDim + c] = acc / lsum;
             } else {
                 float* po = L.out + (static_cast<int64_t>(u) * L.q_rows + qq) * (kHeadDim + 2);
                 po[c] = acc;
                 if (c == 0) {
-                    po[kHeadDim] = s_M[qq];
-                    po[kHeadDim + 1] = s_L[qq];
+                    po[kHeadDim] = M;
+                    po[kHeadDim + 1] = lsum;
                 }
             }
         }

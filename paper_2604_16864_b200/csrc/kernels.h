@@ -120,6 +120,9 @@ cudaError_t launch_combine(const float* partials, int n_parts, int n_units, int 
 struct PrefillLaunch {
     bool bf16;
     int n_units, nb, gqa, n_q, tail, causal;
+    // GQA stacking: one CTA covers hg query heads of a KV head x qt queries each
+    // (hg * qt = 128 columns), so every K/V tile is staged once for hg heads.
+    int hg, qt;
     int k_dense_count, k_sparse_count, v_dense_count, v_sparse_count;
     float scale_log2;
     const void* q;
@@ -153,6 +156,8 @@ struct PrefillLaunch {
     int* dbg;                // optional pipeline watchdog record (debug)
     int mode;                // tools only: 1 = softmax skipped, 2 = MMAs skipped, 3 = both
     long long* trace;        // optional per-tile event clocks of CTA (0,0,0) (tools)
+    // tm_q is a 4-D view [half][unit*gqa + head][query][64]: one box {64, qt, hg, 2}
+    // lands as the stacked 128-column Q tile (rows past n_q zero-filled).
     // tm_kden / tm_ktail are 3-D views ([half][row][64]: one box per 128x128 tile);
     // tm_vnnz2 / tm_vden2 box two consecutive V pool slots (256 rows).
     CUtensorMap tm_q, tm_knnz, tm_kden, tm_vnnz, tm_vden, tm_ktail, tm_vtail, tm_vnnz2, tm_vden2;

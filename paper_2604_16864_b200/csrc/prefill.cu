@@ -413,13 +413,20 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         if (L.redo[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] == 0) return;
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-    const int n_tiles_q = (L.n_q + 127) / 128;
+    // Columns: hg stacked query heads x QT queries (column c = head h0 + c / QT,
+    // query q0 + c % QT; QT a power of two, QT * hg = 128)
+    const int QT = L.qt, qmask = L.qt - 1;
+    const int n_tiles_q = (L.n_q + QT - 1) / QT;
     const int qt = n_tiles_q - 1 - static_cast<int>(blockIdx.x);  // heaviest causal tiles first
-    const int h = blockIdx.y, u = blockIdx.z;
-    const int q0 = qt * 128;
+    const int h0 = blockIdx.y * L.hg, u = blockIdx.z;
+    const int q0 = qt * QT;
     const int n_kv = L.nb * kBlock + L.tail;  // blocked prefix + dense tail
     const int off = n_kv - L.n_q;
-    const int rows_q = min(128, L.n_q - q0);
+    const int rows_q = min(QT, L.n_q - q0);
+    // output row of column c (valid iff (c & qmask) < rows_q)
+    auto out_row = [&](int c) {
+        return L.out + (static_cast<int64_t>(u * L.gqa + h0 + c / QT) * L.n_q + q0 + (c & qmask)) * kHeadDim;
+    };
 
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -570,10 +577,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             prefetch_tmap(&L.tm_q);
             prefetch_tmap(&L.tm_knnz);
             prefetch_tmap(&L.tm_kden);
-            const int qrow = (u * L.gqa + h) * L.n_q + q0;
-            mbar_arrive_expect_tx(&bar_q, 32768);
-            tma_tile_g2s(base_ptr + lay.off_q, &L.tm_q, 0, qrow, &bar_q);
-            tma_tile_g2s(base_ptr + lay.off_q + 16384, &L.tm_q, 64, qrow, &bar_q);
+            mbar_arrive_expect_tx(&bar_q, 32768);  // [half][hg heads x QT queries][64]
+            tma_tile4_g2s(base_ptr + lay.off_q, &L.tm_q, 0, q0, u * L.gqa + h0, 0, &bar_q);
         }
 #ifndef HS_PREFILL_SPLIT_PRODUCER
         if (elect_one()) {
@@ -861,14 +866,14 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 const int key_pos = ti.dblk * kBlock + r;
                 const bool row_valid = (r < 64 || ti.ve1 != 0) && (ti.dblk < 0 || key_pos < n_kv);
                 c_first = row_valid ? ((L.causal && ti.dblk >= 0) ? key_pos - off - q0 : 0) : 1 << 30;
-                fast = __all_sync(0xffffffffu, c_first <= c0);
+                fast = __all_sync(0xffffffffu, c_first <= (QT > 64 ? (c0 & qmask) : 0));
             }
 #pragma unroll
             for (int k = 0; k < 64; k += 2) ffma2(x[k], x[k + 1], sl2, 0.f, 0.f);  // s*scale*log2e - m_used
             if (!fast) {
 #pragma unroll
                 for (int k = 0; k < 64; ++k)
-                    if (c0 + k < c_first) x[k] = -INFINITY;
+                    if (((c0 + k) & qmask) < c_first) x[k] = -INFINITY;
             }
             bool slow = pending || *reinterpret_cast<volatile int*>(&s_ver[ch]) != bver;
             if (!slow) {
@@ -1111,7 +1116,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 s_alpha[r] = l > 0.f ? 1.f / l : 0.f;
             }
             named_bar(5, 256);  // the epilogue group only (ids 1-4 are the quads' barriers)
-            float* out = L.out + (static_cast<int64_t>(u * L.gqa + h) * L.n_q + q0) * kHeadDim;
             const int v_exp = V16 ? L.v16_scale[1] : 0;  // O^T was accumulated over V * 2^-v_exp
             bool bad = false;  // a non-finite row: flag this CTA for the SAFE pass
 #pragma unroll 1
@@ -1123,8 +1127,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 for (int k = 0; k < 16; ++k) {
                     const int c = c0 + k16 + k;
                     const float o = v[k] * s_alpha[c];
-                    bad |= c < rows_q && !(fabsf(o) <= 3.4e38f);
-                    if (c < rows_q) out[c * kHeadDim + r] = ntiles > 0 ? (V16 ? ldexpf(o, v_exp) : o) : 0.f;
+                    const bool cv = (c & qmask) < rows_q;
+                    bad |= cv && !(fabsf(o) <= 3.4e38f);
+                    if (cv) out_row(c)[r] = ntiles > 0 ? (V16 ? ldexpf(o, v_exp) : o) : 0.f;
                 }
             }
             if (!SAFE && bad) s_bad = 1;  // published to L.redo after the final barrier
@@ -1197,7 +1202,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 // column c (query q0 + c at position off + q0 + c) sees this key iff c >= c_first
                 c_first = row_valid ? ((L.causal && ti.dblk >= 0) ? key_pos - off - q0 : 0) : 1 << 30;
                 // warp-uniform fast path: every (row, column) of this warp visible
-                fast = __all_sync(0xffffffffu, c_first <= c0);
+                fast = __all_sync(0xffffffffu, c_first <= (QT > kCols ? (c0 & qmask) : 0));
             }
             // S^T holds s + bias[sb] = s - m_used/(scale log2e), so x = S^T * scale log2e
             // = s*scale*log2e - m_used: no per-column operand in the steady state
@@ -1206,7 +1211,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             if (!fast) {
 #pragma unroll
                 for (int k = 0; k < kCols; ++k)
-                    if (c0 + k < c_first) x[k] = -INFINITY;
+                    if (((c0 + k) & qmask) < c_first) x[k] = -INFINITY;
             }
             bool slow = pending || ((dirty >> sb) & 1u);
             if (!slow) {
@@ -1373,7 +1378,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             s_alpha[c0 + r] = lsum > 0.f ? 1.f / lsum : 0.f;
         }
         named_bar(bar_id, 128);
-        float* out = L.out + (static_cast<int64_t>(u * L.gqa + h) * L.n_q + q0) * kHeadDim;
         {
             uint32_t v[kCols];
             tmem_ld_cols<kCols>(tO + lane_off + c0, v);
@@ -1381,7 +1385,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
 #pragma unroll
             for (int k = 0; k < kCols; ++k) {
                 const int c = c0 + k;
-                if (c < rows_q) out[c * kHeadDim + r] = __uint_as_float(v[k]) * s_alpha[c];
+                if ((c & qmask) < rows_q) out_row(c)[r] = __uint_as_float(v[k]) * s_alpha[c];
             }
         }
     }
@@ -1501,7 +1505,9 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s, int* n_kernel
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    const dim3 grid((L.n_q + 127) / 128, L.gqa, L.n_units);
+    if (L.hg < 1 || L.hg > 4 || (L.hg & (L.hg - 1)) || L.gqa % L.hg || L.qt * L.hg != 128)
+        return cudaErrorInvalidValue;
+    const dim3 grid((L.n_q + L.qt - 1) / L.qt, L.gqa / L.hg, L.n_units);
     const bool dbg = L.trace != nullptr || L.dbg != nullptr || L.mode != 0;
     auto launch = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
