@@ -874,10 +874,13 @@ HS_API hs_status hs_prefill(const void* q, uint32_t n_q, uint32_t gqa, const hs_
     L.nb = k->logical_blocks;
     L.gqa = gqa;
     L.n_q = n_q;
-    // GQA stacking: hg heads of one KV head per CTA, 128 / hg queries
-    // each, so a K/V tile is staged once for hg query heads
-    L.hg = gqa % 4 == 0 ? 4 : gqa % 2 == 0 ? 2 : 1;
-    if (const char* env = getenv("HS_PREFILL_HG")) {  // tools: A/B of the stacking factor
+    // GQA stacking: hg heads of one KV head per CTA x 128 / hg queries
+    // each.  At N = 128 columns per CTA the K/V traffic per column is the same for
+    // every hg (a CTA stages the tiles its own 128 columns see), so hg = 1 is the
+    // default; measured neutral to -4% at 64K.  Stacking that
+    // shares tiles needs N > 128, which TMEM (two S^T buffers + O^T) cannot hold.
+    L.hg = 1;
+    if (const char* env = getenv("HS_PREFILL_HG")) {  // tests / tools: the stacked layouts
         const int g = atoi(env);
         if ((g == 1 || g == 2 || g == 4) && gqa % g == 0) L.hg = g;
     }

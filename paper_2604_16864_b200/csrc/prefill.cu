@@ -851,6 +851,14 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             const TileInfo ti = s_tiles[t];
             mbar_wait_dbg(&bar_sfull[sb], (t >> 1) & 1, dbgp, 21);
             tc_fence_after();
+            if (DBG && (mode & 1)) {  // tools: the TMA + MMA pipeline without the softmax
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_sempty[sb]);
+                if (t >= 2) mbar_wait_dbg(&bar_pempty[sb], ((t >> 1) - 1) & 1, dbgp, 22);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_pfull[sb]);
+                continue;
+            }
             const bool tr0 = DBG && lane == 0 && wq == 0 && ch == 0;  // one tracing thread per group
             if (tr0) trace(L, t, 0);
             float x[64];
@@ -1463,6 +1471,9 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s, int* n_kernel
             pp = pp && a == 2;
         }
     }
+    if (getenv("HS_PREFILL_VERBOSE"))  // tools
+        fprintf(stderr, "prefill plan: pp %d pbuf %u nk %u (stage %u) nv %u (stage %u) hg %d\n", (int)pp, lay.n_pbuf,
+                lay.nk, lay.k_stage, lay.nv, lay.v_stage, L.hg);
     lay.off_k = lay.off_p + lay.n_pbuf * lay.p_bytes;
     lay.off_v = lay.off_k + lay.nk * lay.k_stage;
     lay.off_tiles = lay.off_v + lay.nv * lay.v_stage;

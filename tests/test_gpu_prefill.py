@@ -54,6 +54,29 @@ def test_prefill_matches_oracle(hs, port, dtype, L, n_q, s, sink, window, causal
     assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
 
 
+@pytest.mark.parametrize("hg", [2, 4])
+@pytest.mark.parametrize("dtype,L,n_q,s,causal", [
+    ("f16", 1024, 1024, 1.0, True),
+    ("f16", 1024, 300, 0.5, True),    # partial query tiles of every stacked head
+    ("bf16", 768, 256, 0.25, False),
+])
+def test_prefill_gqa_stacked(hs, port, monkeypatch, hg, dtype, L, n_q, s, causal):
+    """hg query heads of one KV head per CTA (HS_PREFILL_HG): column c of the
+    128-column tile is head c / (128 / hg), query c % (128 / hg)."""
+    monkeypatch.setenv("HS_PREFILL_HG", str(hg))
+    U, gqa = 2, 4
+    kc, vc, q = setup(hs, port, U, L, s, dtype, gqa, n_q)
+    scale = np.float32(1.0 / math.sqrt(128))
+    got = hs.prefill_attention(to_torch(q, dtype), kc, vc, causal=causal, scale=float(scale)).cpu().numpy()
+
+    def one(ug):
+        u, g = divmod(ug, gqa)
+        return port.prefill(q[u, g], device_to_oracle(kc, u), device_to_oracle(vc, u), None, None, causal, scale, 64)
+    want = np.stack(parallel(one, range(U * gqa))).reshape(U, gqa, n_q, 128)
+    mx, mr = err_stats(got, want)
+    assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
+
+
 @pytest.mark.parametrize("s", [1.0, 0.5])
 def test_prefill_sampled_rows_8k(hs, port, s):
     """8K causal prefill; 96 sampled query rows per head (block boundaries,
