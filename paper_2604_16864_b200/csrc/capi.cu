@@ -732,6 +732,7 @@ static hs_status decode_common_rows(const void* q, const hs_device_cache* k, con
     L.prefetch_distance = 0;  // measured: L2 prefetch ahead of the TMA ring costs 3% (tools/tune_decode.py)
     if (const char* env = getenv("HS_DECODE_PF")) L.prefetch_distance = atoi(env);
     if (const char* env = getenv("HS_DECODE_DEBUG_STREAM_ONLY")) L.debug_stream_only = atoi(env);
+    if (const char* env = getenv("HS_DECODE_XP_TAIL")) L.debug_tail = atoi(env);
     L.k_tail = k_tail;
     L.v_tail = v_tail;
     L.block_begin = block_begin;

@@ -188,6 +188,16 @@ __device__ __forceinline__ void tma_tile4_g2s(void* dst, const CUtensorMap* map,
         : "memory");
 }
 
+// Asynchronous 4- / 8-byte global -> shared copies (LDGSTS; completion by
+// cp_async_wait_all in the issuing thread).
+__device__ __forceinline__ void cp_async_4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // L2 prefetch of a contiguous global range (no shared memory involved).
 __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -273,6 +283,19 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+// Device-scope atomics with release / acquire-release ordering (a CTA barrier
+// before a release makes every thread's earlier stores part of it).
+__device__ __forceinline__ int atom_add_release_gpu(int* p, int v) {
+    int r;
+    asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+    return r;
+}
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+    int r;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+    return r;
 }
 
 __device__ __forceinline__ long long globaltimer() {

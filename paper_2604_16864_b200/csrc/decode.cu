@@ -479,44 +479,64 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     if (L.out == nullptr) return;
 
     // ---------------- combine the unit's splits (attention.hpp:387-407) ----------------
-    // One thread per output column, registers only: the (m, l, O) of every split
-    // are independent L2 loads issued together (chunks of 16 splits, online LSE
-    // across chunks), so the combine costs about one L2 round trip and no CTA
-    // barriers (the former shared-memory weight table took ~5 us at configs[1]).
+    // Latency-bound (it runs once, after the stream): G lanes per output column
+    // each fold a strided subset of the splits (their (m, l, O) loads issued
+    // together, online LSE over groups of 4), then the G partial (M, acc, l) merge
+    // by a butterfly of shuffles -- a handful of dependent steps instead of one
+    // thread walking every split (measured ~2 us of the configs[1] step).
     const float* P = L.partial + static_cast<int64_t>(u) * L.nsplit * stride_p;
     auto combine_slice = [&](int lo, int hi) {
         constexpr float kLog2e = 1.4426950408889634f;
-        for (int idx = lo + threadIdx.x; idx < hi; idx += nthr) {
-            const int qq = idx / kHeadDim, c = idx % kHeadDim;
+        const int ncols = hi - lo;
+        int G = 8;  // lanes per column (a power of two within a warp)
+        while (G > 1 && ncols * G > nthr) G >>= 1;
+        const int j = threadIdx.x / G, r = threadIdx.x % G, per_round = nthr / G;
+        const int rounds = (ncols + per_round - 1) / per_round;
+        for (int it = 0; it < rounds; ++it) {
+            const int idx = lo + it * per_round + j;
+            const bool valid = idx < hi;
+            const int qq = valid ? idx / kHeadDim : 0, c = valid ? idx % kHeadDim : 0;
             const float* pq = P + qq * (kHeadDim + 2);
             float M = -INFINITY, acc = 0.f, lsum = 0.f;
-            for (int sp0 = 0; sp0 < L.nsplit; sp0 += 16) {
-                float mv[16], lv[16], ov[16];
+            for (int sp0 = r; valid && sp0 < L.nsplit; sp0 += 4 * G) {
+                float mv[4], lv[4], ov[4];
 #pragma unroll
-                for (int x = 0; x < 16; ++x) {
-                    const bool in = sp0 + x < L.nsplit;
-                    const float* ps = pq + static_cast<int64_t>(sp0 + x) * stride_p;
-                    mv[x] = in ? __ldcg(ps + kHeadDim) : -INFINITY;
-                    lv[x] = in ? __ldcg(ps + kHeadDim + 1) : 0.f;
-                    ov[x] = in ? __ldcg(ps + c) : 0.f;
+                for (int x = 0; x < 4; ++x) {
+                    const int sp = sp0 + x * G;
+                    const float* ps = pq + static_cast<int64_t>(sp) * stride_p;
+                    // weak loads: ordered after the producers' release by the acquire
+                    // (and its L1 invalidation) plus the CTA barrier
+                    mv[x] = sp < L.nsplit ? ps[kHeadDim] : -INFINITY;
+                    lv[x] = sp < L.nsplit ? ps[kHeadDim + 1] : 0.f;
+                    ov[x] = sp < L.nsplit ? ps[c] : 0.f;
                 }
-                float Mc = M;
-#pragma unroll
-                for (int x = 0; x < 16; ++x) Mc = fmaxf(Mc, mv[x]);
+                const float Mc = fmaxf(fmaxf(M, fmaxf(mv[0], mv[1])), fmaxf(mv[2], mv[3]));
                 if (Mc == -INFINITY) continue;  // every split so far empty
                 if (M != Mc) {
-                    const float r = M == -INFINITY ? 0.f : fast_exp2((M - Mc) * kLog2e);
-                    acc *= r;
-                    lsum *= r;
+                    const float sc = M == -INFINITY ? 0.f : fast_exp2((M - Mc) * kLog2e);
+                    acc *= sc;
+                    lsum *= sc;
                     M = Mc;
                 }
 #pragma unroll
-                for (int x = 0; x < 16; ++x) {
+                for (int x = 0; x < 4; ++x) {
                     const float wt = mv[x] == -INFINITY ? 0.f : fast_exp2((mv[x] - M) * kLog2e);
                     acc = fmaf(ov[x], wt, acc);
                     lsum = fmaf(lv[x], wt, lsum);
                 }
             }
+            for (int o = 1; o < G; o <<= 1) {  // merge the G lanes' partial sums
+                const float Mo = __shfl_xor_sync(0xffffffffu, M, o);
+                const float ao = __shfl_xor_sync(0xffffffffu, acc, o);
+                const float lo2 = __shfl_xor_sync(0xffffffffu, lsum, o);
+                const float Mn = fmaxf(M, Mo);
+                const float w1 = M == -INFINITY ? 0.f : fast_exp2((M - Mn) * kLog2e);
+                const float w2 = Mo == -INFINITY ? 0.f : fast_exp2((Mo - Mn) * kLog2e);
+                acc = acc * w1 + ao * w2;
+                lsum = lsum * w1 + lo2 * w2;
+                M = Mn;
+            }
+            if (!valid || r != 0) continue;
             if (L.out_mode == 0) {
                 L.out[(static_cast<int64_t>(u) * L.q_rows + qq) * kHeadDim + c] = acc / lsum;
             } else {
@@ -529,9 +549,11 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
             }
         }
     };
-    __threadfence();
-    if (ct && threadIdx.x == 0) ct[7] = globaltimer();
+    // Publication: the CTA barrier orders every thread's partial stores before
+    // thread 0's release atomic on the unit's counter (no device-wide SC fence
+    // in all 256 threads, ~0.5 us here); readers acquire the counter.
     __syncthreads();
+    if (ct && threadIdx.x == 0) ct[7] = globaltimer();
     if (L.coop_combine) {
         // Whole grid resident (host-checked): every CTA of the unit waits for the
         // unit's last partial, then merges its own slice of the gqa x d outputs, so
@@ -539,15 +561,15 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
         int* arrive = &L.counters[u];
         int* done = &L.counters[L.n_units + u];
         if (threadIdx.x == 0) {
-            atomicAdd(arrive, 1);
-            while (ld_acquire(arrive) < L.nsplit) __nanosleep(64);
+            atom_add_release_gpu(arrive, 1);
+            while (L.debug_tail < 2 && ld_acquire(arrive) < L.nsplit) __nanosleep(64);
         }
         __syncthreads();
         if (ct && threadIdx.x == 0) ct[5] = globaltimer();
         const int n = gqa * kHeadDim;
         const int lo = static_cast<int>(static_cast<int64_t>(n) * split / L.nsplit);
         const int hi = static_cast<int>(static_cast<int64_t>(n) * (split + 1) / L.nsplit);
-        combine_slice(lo, hi);
+        if (L.debug_tail == 0) combine_slice(lo, hi);
         if (ct && threadIdx.x == 0) ct[10] = globaltimer();
         __syncthreads();
         if (threadIdx.x == 0 && atomicAdd(done, 1) == L.nsplit - 1) {
@@ -559,7 +581,7 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
         return;
     }
     // Otherwise the last CTA of the unit to arrive merges everything.
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&L.counters[u], 1);
+    if (threadIdx.x == 0) s_ticket = atom_add_acq_rel_gpu(&L.counters[u], 1);
     __syncthreads();
     if (s_ticket != L.nsplit - 1) return;
     if (ct && threadIdx.x == 0) ct[5] = globaltimer();
@@ -686,7 +708,7 @@ size_t decode_smem_bytes(const DecodeLaunch& L, int* nw_out, int* spw_out, Stage
     if (spw < 1) spw = 1;
     size_t smem = static_cast<size_t>(NW * spw) * lay.stage_bytes;
     const size_t scratch = (NW * kMaxGqa * kHeadDim + 2 * NW * kMaxGqa) * sizeof(float);
-    const size_t combine = (2 * static_cast<size_t>(L.nsplit) * kMaxGqa + 2 * kMaxGqa) * sizeof(float);
+    const size_t combine = 0;  // the split combine works in registers
     if (smem < scratch) smem = scratch;
     if (smem < combine) smem = combine;
     smem += idx_bytes + 1024;

@@ -92,6 +92,7 @@ struct DecodeLaunch {
     const void* v_dense;
     int prefetch_distance;   // blocks per warp prefetched into L2 ahead of the ring
     int debug_stream_only;   // tools only: stream the ring without math
+    int debug_tail;          // tools only: 1 = skip the split combine, 2 = also skip the arrival spin (timing)
     const void* k_tail;      // [u][tail][d]
     const void* v_tail;
     // split geometry: unit u, split s covers blocks [nb*s/nsplit, nb*(s+1)/nsplit)

@@ -51,7 +51,12 @@ print(f"CTAs {len(t)}  start: min {t[:,0].min():.1f} max {t[:,0].max():.1f} us |
       f"med {np.median(t[:,1]):.1f} max {t[:,1].max():.1f} | loop end: min {t[:,2].min():.1f} med {np.median(t[:,2]):.1f} "
       f"max {t[:,2].max():.1f} | partial written: max {np.nanmax(t[:,3]):.1f} | combine done: max {np.nanmax(t[:,4]):.1f} us")
 print("loop-end percentiles (10/25/50/75/90/100):", np.percentile(t[:, 2], [10, 25, 50, 75, 90, 100]).round(1))
+nsp = len(t) // U
+for u in range(U):
+    tu = t[u * nsp:(u + 1) * nsp]
+    print(f"unit {u}: first data max {np.nanmax(tu[:, 1]):.1f} | loop end min {np.nanmin(tu[:, 2]):.1f} med {np.nanmedian(tu[:, 2]):.1f} "
+          f"max {np.nanmax(tu[:, 2]):.1f} | partial max {np.nanmax(tu[:, 3]):.1f} | done max {np.nanmax(tu[:, 4]):.1f}")
 last = ~np.isnan(t[:, 4])
 for row in t[last][:12]:
     print(f"combine CTA: loop end {row[2]:.1f} partial {row[3]:.1f} fence1 {row[7]:.1f} ticket {row[5]:.1f} "
-          f"m/l loaded {row[8]:.1f} weights {row[9]:.1f} O summed {row[10]:.1f} done {row[4]:.1f}")
+          f"O summed {row[10]:.1f} done {row[4]:.1f}")
