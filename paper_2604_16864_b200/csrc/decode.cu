@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[16];
     __shared__ int s_ticket;
+    __shared__ uint32_t s_q[kMaxGqa * kHeadDim / 2];  // the unit's query rows (16-bit pairs)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int split = blockIdx.x, u = blockIdx.y;
@@ -73,6 +74,16 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     const uint32_t base = (raw + idx_bytes + 1023u) & ~1023u;
     uint8_t* const base_ptr = smem_raw + (base - raw);
 
+    // The unit's queries: loaded first (they may live in pinned host memory --
+    // zero-copy host I/O, DecodePlan(host_io) -- so their latency overlaps the
+    // set-up and the first TMA issue), staged in shared memory below.
+    const uint32_t* qg = reinterpret_cast<const uint32_t*>(static_cast<const T*>(L.q) +
+                                                           static_cast<int64_t>(u) * L.q_rows * kHeadDim);
+    const int nqw = gqa * (kHeadDim / 2);
+    constexpr int kQW = kMaxGqa * (kHeadDim / 2) / (32 * NW);  // words per thread at most
+    uint32_t qw[kQW];
+#pragma unroll
+    for (int i = 0; i < kQW; ++i) qw[i] = threadIdx.x + i * 32 * NW < nqw ? qg[threadIdx.x + i * 32 * NW] : 0u;
     const int16_t* kidx = L.k_index + static_cast<int64_t>(u) * L.nb;
     const int16_t* vidx = L.v_index + static_cast<int64_t>(u) * L.nb;
     // dynamic block claiming needs the one-slot ring and the fused combine (which
@@ -192,6 +203,10 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     }
     if (dyn) nk = 1 << 30;  // until the unit's counter runs out
     __syncwarp();
+#pragma unroll
+    for (int i = 0; i < kQW; ++i)
+        if (threadIdx.x + i * 32 * NW < nqw) s_q[threadIdx.x + i * 32 * NW] = qw[i];
+    __syncthreads();
 
     // ------------------------------------------------------- consumers ----
     const int g = lane >> 2, t = lane & 3, half = t & 1;
@@ -205,13 +220,13 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
 
     {
         // Q^T fragments for GEMM1 (B operand, k = channel, n = query row g).
-        const T* q = static_cast<const T*>(L.q) + static_cast<int64_t>(u) * L.q_rows * kHeadDim;
+        const uint16_t* q = reinterpret_cast<const uint16_t*>(s_q);
         uint32_t qb[4][4];
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int x = 0; x < 4; ++x)
-                qb[j][x] = g < gqa ? ld_pair(q + g * kHeadDim + 32 * j + 8 * x + 2 * t) : 0u;
+                qb[j][x] = g < gqa ? s_q[(g * kHeadDim + 32 * j + 8 * x + 2 * t) / 2] : 0u;
 
         for (int k = 0; k < nk; ++k) {
             const int s = warp * spw + k % spw;

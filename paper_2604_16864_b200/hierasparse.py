@@ -457,22 +457,35 @@ class DecodePlan:
     hs_decode_ws), so replays share no state with other decode work."""
 
     def __init__(self, q: torch.Tensor, k: DeviceCompressedCache, v: DeviceCompressedCache,
-                 scale: float | None = None, splits: int = 0):
+                 scale: float | None = None, splits: int = 0, host_io: bool = False):
+        """host_io: the step reads the queries from pinned host memory (self.q_host)
+        and writes the output to pinned host memory (self.out_host) directly over
+        the host link (zero-copy), so one replay is a whole host-to-host decode
+        step: write q_host, replay, synchronise, read out_host."""
         _check_queries(q, k, "DecodePlan")
         self.q = q.contiguous().clone()
         self.k, self.v = k, v
         gqa = self.q.shape[1]
         self.out = torch.empty((k.n_units, gqa, k.head_dim), dtype=torch.float32, device=q.device)
+        self.host_io = host_io
+        if host_io:
+            self.q_host = self.q.cpu().pin_memory()
+            self.out_host = torch.empty(self.out.shape, dtype=torch.float32).pin_memory()
         lib = capi.load()
         nbytes = C.c_uint64()
         capi.check(lib.hs_decode_workspace_bytes(k.cref(), gqa, splits, C.byref(nbytes)))
         self.workspace = torch.zeros(int(nbytes.value), dtype=torch.uint8, device=q.device)
         scale = 1.0 / math.sqrt(k.head_dim) if scale is None else scale
 
+        # host_io: zero-copy -- the kernel reads the queries from the pinned (UVA
+        # mapped) q_host and the split combine writes O straight into out_host, so
+        # the step needs no copy-engine transfers (two small DMAs cost ~16 us).
+        qp = self.q_host.data_ptr() if host_io else self.q.data_ptr()
+        op = self.out_host.data_ptr() if host_io else self.out.data_ptr()
+
         def step():
-            capi.check(lib.hs_decode_ws(self.q.data_ptr(), k.cref(), v.cref(), None, None, 0, gqa, scale, splits,
-                                        self.out.data_ptr(), self.workspace.data_ptr(), self.workspace.numel(),
-                                        _stream()))
+            capi.check(lib.hs_decode_ws(qp, k.cref(), v.cref(), None, None, 0, gqa, scale, splits, op,
+                                        self.workspace.data_ptr(), self.workspace.numel(), _stream()))
         # Warm up on the capture stream so the TMA descriptors exist before
         # capture (no allocation may happen inside the graph).
         self.stream = torch.cuda.Stream()
@@ -489,9 +502,9 @@ class DecodePlan:
 
     def __call__(self, q: torch.Tensor | None = None) -> torch.Tensor:
         if q is not None:
-            self.q.copy_(q, non_blocking=True)
+            (self.q_host if self.host_io else self.q).copy_(q, non_blocking=not self.host_io)
         self.graph.replay()
-        return self.out
+        return self.out_host if self.host_io else self.out
 
 
 def decode_partial(q, k: DeviceCompressedCache, v: DeviceCompressedCache, block_begin: int, block_end: int,

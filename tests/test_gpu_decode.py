@@ -200,6 +200,24 @@ def test_decode_plans_own_their_workspaces(hs, port):
             assert (p.out - w).abs().max().item() < 1e-5
 
 
+def test_decode_plan_host_io(hs, port):
+    """DecodePlan(host_io=True): one graph replay copies the pinned host queries in,
+    decodes and copies the output to pinned host memory; fresh queries written to
+    q_host between replays are picked up, matching decode_attention."""
+    import torch
+    U, L = 4, 8192
+    kx, vx, kc, vc = build_caches(hs, port, U, L, 1.0, "bf16", seed=31)
+    q0 = to_torch(decode_queries(port, U, 4, "bf16", seed=31), "bf16")
+    q1 = to_torch(decode_queries(port, U, 4, "bf16", seed=32), "bf16")
+    plan = hs.DecodePlan(q0, kc, vc, host_io=True)
+    for q in (q0, q1, q0):
+        out = plan(q.cpu())
+        torch.cuda.synchronize()
+        want = hs.decode_attention(q, kc, vc).cpu()
+        assert out.device.type == "cpu" and out.is_pinned()
+        assert (out - want).abs().max().item() < 1e-5
+
+
 @pytest.mark.parametrize("tail", [1, 37, 200])
 def test_decode_tail_only_view(hs, port, tail):
     """CacheView{compressed = nullptr, dense_tail} (attention.hpp:22-31): decode over
