@@ -31,6 +31,9 @@ FULL_METRICS = [
     ("sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_on.avg.pct_of_peak_sustained_elapsed",
      "mma.sp bf16 ops % of peak"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem: tensor-core operand reads % of peak"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem: LSU wavefronts % of peak"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) pipe %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
 ]
 
