@@ -225,7 +225,7 @@ HS_API hs_status hs_decompress(const hs_device_cache* c, void* dst, uint64_t* st
  *           run-to-run deterministic partition of attention.hpp:380-381.  Results
  *           agree across split counts to float rounding (test_attention.cpp:315-326)
  *   out:    float [n_units][gqa][d]
-  * q and out may be pinned (UVA-mapped) host memory for block_size 64 / head_dim 128
+ * q and out may be pinned (UVA-mapped) host memory for block_size 64 / head_dim 128
  * caches: the kernel reads q and writes out over the host link (zero-copy).
  * gqa >= 1 (more than 8 rows run in chunks of 8). */
 HS_API hs_status hs_decode(const void* q, const hs_device_cache* k, const hs_device_cache* v,
