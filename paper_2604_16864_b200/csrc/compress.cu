@@ -207,6 +207,14 @@ struct PackArgs {
     const uint8_t* element_mask;  // mask_pack_kernel: explicit ElementMask u8 [u][rows][d]
     uint64_t mask_unit_stride;
     int B, d;                     // block size and head dim (generic-shape kernels)
+    // Static selection resolved in the pack kernel (no assign_slots launch): block b
+    // is dense iff protected (b < prefix or b >= nb - suffix) or !all_sparse; the
+    // CTA derives its slot and writes its own index-map entry, slot_block entry
+    // and flag (the same values assign_slots_kernel writes).
+    int static_sel, prefix, suffix, all_sparse;
+    int16_t* index_out;
+    int32_t* slot_block_out;
+    uint8_t* flags_out;
 };
 
 // One stored 2:4 group (kept pair word, 4-bit code) back to its four logical
@@ -291,7 +299,17 @@ __global__ void __launch_bounds__(kThreads, HS_COMPRESS_MINB) block_kernel(PackA
 
     bool dense = false;
     int slot = 0;
-    if (MODE != 0) {
+    if (MODE != 0 && a.static_sel) {
+        const bool prot = b < a.prefix || b >= a.nb - a.suffix;
+        dense = prot || !a.all_sparse;
+        slot = !a.all_sparse ? b : !prot ? b - a.prefix : b < a.prefix ? b : a.prefix + (b - (a.nb - a.suffix));
+        if (t == 0) {
+            const int64_t ub = static_cast<int64_t>(u) * a.nb;
+            a.index_out[ub + b] = static_cast<int16_t>(dense ? slot + 1 : -(slot + 1));
+            if (a.slot_block_out) a.slot_block_out[ub + (dense ? slot : a.dense_count + slot)] = b;
+            if (a.flags_out) a.flags_out[ub + b] = static_cast<uint8_t>(dense);
+        }
+    } else if (MODE != 0) {
         const int e = a.index_map[static_cast<int64_t>(u) * a.nb + b];
         dense = e > 0;
         slot = (e > 0 ? e : -e) - 1;
@@ -862,7 +880,17 @@ __global__ void __launch_bounds__(kThreads) gen_block_kernel(PackArgs a) {
     };
     bool dense = false;
     int slot = 0;
-    if (MODE != 0) {
+    if (MODE != 0 && a.static_sel) {
+        const bool prot = b < a.prefix || b >= a.nb - a.suffix;
+        dense = prot || !a.all_sparse;
+        slot = !a.all_sparse ? b : !prot ? b - a.prefix : b < a.prefix ? b : a.prefix + (b - (a.nb - a.suffix));
+        if (t == 0) {
+            const int64_t ub = static_cast<int64_t>(u) * a.nb;
+            a.index_out[ub + b] = static_cast<int16_t>(dense ? slot + 1 : -(slot + 1));
+            if (a.slot_block_out) a.slot_block_out[ub + (dense ? slot : a.dense_count + slot)] = b;
+            if (a.flags_out) a.flags_out[ub + b] = static_cast<uint8_t>(dense);
+        }
+    } else if (MODE != 0) {
         const int e = a.index_map[static_cast<int64_t>(u) * a.nb + b];
         dense = e > 0;
         slot = (e > 0 ? e : -e) - 1;
@@ -1023,7 +1051,7 @@ static cudaError_t launch_block_kernel(int axis, int mode, const PackArgs& a, in
 }
 
 cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
-    PackArgs a;
+    PackArgs a{};
     a.src = static_cast<const uint16_t*>(L.src);
     a.src_stride = L.src_unit_stride;
     a.nb = L.nb;
@@ -1067,6 +1095,17 @@ cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
             return cudaGetLastError();
         }
         return blocks(1);
+    }
+    a.static_sel = 0;
+    if (L.static_selection && a.B == kBlock && a.d == kHeadDim) {
+        a.static_sel = 1;
+        a.prefix = L.prefix;
+        a.suffix = L.suffix;
+        a.all_sparse = L.all_sparse;
+        a.index_out = L.index_map;
+        a.slot_block_out = L.slot_block;
+        a.flags_out = L.flags_out;
+        return blocks(L.losses ? 2 : 1);
     }
     if (L.static_selection) {
         assign_slots_kernel<<<L.n_units, 1024, 0, s>>>(nullptr, L.nb, L.prefix, L.suffix,

@@ -406,8 +406,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     __shared__ float s_delta[128], s_alpha[128], s_mrun[128], s_mused[2][128];
     __shared__ uint16_t s_bq[128];
     __shared__ int s_g2_issued;  // GEMM2 tiles issued (kG2First ordering)
-    __shared__ int s_bad;        // ping-pong: some output row of this CTA came out non-finite
     __shared__ typename std::conditional<PP, PPShared, PPNone>::type pps;  // ping-pong softmax state
+    __shared__ int s_bad;        // ping-pong: some output row of this CTA came out non-finite
 
     if constexpr (SAFE) {  // only the CTAs the fast pass flagged
         if (L.redo[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] == 0) return;
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     // Columns: hg stacked query heads x QT queries (column c = head h0 + c / QT,
     // query q0 + c % QT; QT a power of two, QT * hg = 128)
-    const int QT = L.qt, qmask = L.qt - 1;
+    const int QT = L.qt, qmask = L.qt - 1, qshift = __ffs(L.qt) - 1;
     const int n_tiles_q = (L.n_q + QT - 1) / QT;
     const int qt = n_tiles_q - 1 - static_cast<int>(blockIdx.x);  // heaviest causal tiles first
     const int h0 = blockIdx.y * L.hg, u = blockIdx.z;
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     const int rows_q = min(QT, L.n_q - q0);
     // output row of column c (valid iff (c & qmask) < rows_q)
     auto out_row = [&](int c) {
-        return L.out + (static_cast<int64_t>(u * L.gqa + h0 + c / QT) * L.n_q + q0 + (c & qmask)) * kHeadDim;
+        return L.out + (static_cast<int64_t>(u * L.gqa + h0 + (c >> qshift)) * L.n_q + q0 + (c & qmask)) * kHeadDim;
     };
 
     const uint32_t raw = smem_u32(smem_raw);
@@ -874,14 +874,22 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 const int key_pos = ti.dblk * kBlock + r;
                 const bool row_valid = (r < 64 || ti.ve1 != 0) && (ti.dblk < 0 || key_pos < n_kv);
                 c_first = row_valid ? ((L.causal && ti.dblk >= 0) ? key_pos - off - q0 : 0) : 1 << 30;
+#ifdef HS_XP_OLDMASK
+                fast = __all_sync(0xffffffffu, c_first <= c0);
+#else
                 fast = __all_sync(0xffffffffu, c_first <= (QT > 64 ? (c0 & qmask) : 0));
+#endif
             }
 #pragma unroll
             for (int k = 0; k < 64; k += 2) ffma2(x[k], x[k + 1], sl2, 0.f, 0.f);  // s*scale*log2e - m_used
             if (!fast) {
 #pragma unroll
                 for (int k = 0; k < 64; ++k)
+#ifdef HS_XP_OLDMASK
+                    if (c0 + k < c_first) x[k] = -INFINITY;
+#else
                     if (((c0 + k) & qmask) < c_first) x[k] = -INFINITY;
+#endif
             }
             bool slow = pending || *reinterpret_cast<volatile int*>(&s_ver[ch]) != bver;
             if (!slow) {
@@ -1136,7 +1144,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     const int c = c0 + k16 + k;
                     const float o = v[k] * s_alpha[c];
                     const bool cv = (c & qmask) < rows_q;
+#ifndef HS_XP_NOBAD
                     bad |= cv && !(fabsf(o) <= 3.4e38f);
+#endif
                     if (cv) out_row(c)[r] = ntiles > 0 ? (V16 ? ldexpf(o, v_exp) : o) : 0.f;
                 }
             }
