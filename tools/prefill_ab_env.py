@@ -1,12 +1,16 @@
 """A/B of prefill run-time switches (environment variables read per call) in one process.
 
-    python tools/prefill_ab_env.py L "S1,S2,..." "VAR=a|VAR=b|..." [reps]
+    python tools/prefill_ab_env.py L "S1,S2,..." "VAR=a;VAR2=c|VAR=b|..." [reps]
+
+AB_SLEEP=<s>: idle that long before every timed run (equal power state; with it the
+runs repeat to ~0.3%, without it the 1000 W cap moves them by up to 10%).
 
 Caches per S are built once; the variants alternate within each repetition so
 clock drift cancels.  configs[2] shape: 8 KV heads x GQA 4, causal, fp16.
 """
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -26,7 +30,7 @@ ref = torch.empty_like(out)
 
 
 def set_env(v):
-    for kv in v.split(","):
+    for kv in v.split(";"):
         if not kv:
             continue
         k, val = kv.split("=")
@@ -38,7 +42,7 @@ def set_env(v):
 
 def clear(vs):
     for v in vs:
-        for kv in v.split(","):
+        for kv in v.split(";"):
             if kv:
                 os.environ.pop(kv.split("=")[0], None)
 
@@ -64,6 +68,8 @@ for s in spars:
         for vv in variants:
             clear(variants)
             set_env(vv)
+            if os.environ.get("AB_SLEEP"):  # equal power / thermal state before every timed run
+                time.sleep(float(os.environ["AB_SLEEP"]))
             e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
             e0.record()
             hs.prefill_attention(q, kc, vc, causal=True, out=out)
