@@ -441,3 +441,36 @@ def test_absorb_tail_without_whole_block_is_a_noop(hs, port):
     kc = hs.prune_compress(kt[:, :L].contiguous(), hs.SparsityConfig(1.0, 1.0, 64), 1.0, 0)
     k2, rest = hs.absorb_tail(kc, kt[:, L:], hs.SparsityConfig(1.0, 1.0, 64), 1.0)
     assert k2 is kc and rest.shape[1] == 10
+
+
+@pytest.mark.parametrize("axis_name", ["key", "value"])
+def test_nan_losses_flag_exactly_quota_blocks(hs, port, axis_name):
+    """Blocks whose pruned values are NaN (an all-NaN token row, e.g. fp16 overflow)
+    get a NaN loss.  Selection orders NaN as the largest loss, so exactly
+    floor(S * prunable) blocks are sparse, the index map is a permutation of the
+    pool slots and decompress reads it back without a DataError (ADVICE: a NaN
+    rank once flagged extra blocks and packed past the sparse pool)."""
+    import torch
+    U, rows, s = 2, 2048, 0.5
+    x = gen_units(port, U, rows, 128, 5, 0, "f16")
+    # three NaN token rows inside one group of 4 tokens: NaN pruned values along both
+    # axes (key: whole channel groups; value: 3 NaN of a 4-token group)
+    x[0, 64 * 3 + 4:64 * 3 + 7, :] = np.nan    # block 3 of unit 0
+    x[1, 64 * 10:64 * 10 + 3, :] = np.nan      # block 10 of unit 1
+    xt = to_torch(x, "f16")
+    cfg = hs.SparsityConfig(s, s, 64)
+    axis = 0 if axis_name == "key" else 1
+    c = hs.prune_compress(xt, cfg, s, axis)
+    nb = rows // 64
+    quota = int(np.floor(s * nb))
+    im = c.index_map.cpu().numpy()
+    for u in range(U):
+        assert (im[u] < 0).sum() == quota and (im[u] > 0).sum() == nb - quota
+        assert sorted(-im[u][im[u] < 0] - 1) == list(range(quota))
+        assert sorted(im[u][im[u] > 0] - 1) == list(range(nb - quota))
+    losses = c.losses.cpu().numpy()
+    assert np.isnan(losses[0, 3]) and np.isnan(losses[1, 10])
+    assert im[0, 3] > 0 and im[1, 10] > 0  # NaN loss = largest: kept dense
+    out = hs.decompress(c)
+    torch.cuda.synchronize()
+    assert out.shape == xt.shape
