@@ -212,6 +212,7 @@ struct PackArgs {
     // CTA derives its slot and writes its own index-map entry, slot_block entry
     // and flag (the same values assign_slots_kernel writes).
     int static_sel, prefix, suffix, all_sparse;
+    int reverse;                  // block order last-to-first (L2 reuse after a classify pass)
     int16_t* index_out;
     int32_t* slot_block_out;
     uint8_t* flags_out;
@@ -253,7 +254,11 @@ __device__ double sequential_loss_in(const PackArgs& a, int u, int b) {
 
 template <typename T, int AXIS, int MODE, int SRC>
 __global__ void __launch_bounds__(kThreads, HS_COMPRESS_MINB) block_kernel(PackArgs a) {
-    const int b = blockIdx.x, u = blockIdx.y, t = threadIdx.x;
+    // reverse: walk the blocks last-to-first (the pack pass after a classify pass
+    // that read the source first-to-last: its last ~100 MB are still in L2)
+    const int b = a.reverse ? static_cast<int>(gridDim.x - 1 - blockIdx.x) : static_cast<int>(blockIdx.x);
+    const int u = a.reverse ? static_cast<int>(gridDim.y - 1 - blockIdx.y) : static_cast<int>(blockIdx.y);
+    const int t = threadIdx.x;
     // SRC 1: blocks past the input cache come from the dense source (a tail's
     // full blocks absorbed into the cache)
     const bool from_src = SRC == 0 || b >= a.in_nb;
@@ -646,71 +651,6 @@ __global__ void __launch_bounds__(256) rank_kernel(const double* losses, int nb,
     }
 }
 
-// The same selection by sorting: one CTA per unit bitonic-sorts the prunable
-// blocks' (orderable loss, index) pairs in shared memory and flags the first
-// quota positions.  The key maps the strict total order above onto unsigned
-// integers: -0.0 -> +0.0 (the reference's `<` treats them as equal), NaN above
-// +inf, ties by index.  O(n log^2 n) instead of rank_kernel's O(n^2) double
-// compares (2048 blocks: ~2 us instead of ~90 us); used while the pairs fit.
-constexpr int kSortMaxBlocks = 16384;  // 16384 x 12 B = 192 KB of shared memory
-__device__ __forceinline__ unsigned long long loss_key(double l) {
-    if (isnan(l)) return ~0ull;
-    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(l == 0.0 ? 0.0 : l));
-    return (b >> 63) ? ~b : (b | (1ull << 63));
-}
-__global__ void __launch_bounds__(1024) sort_select_kernel(const double* losses, int nb, int prefix, int suffix,
-                                                           int quota, int n2, uint8_t* flags) {
-    extern __shared__ __align__(16) unsigned long long s_key[];
-    uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_key + n2);
-    const int u = blockIdx.x, tid = threadIdx.x;
-    const double* L = losses + static_cast<int64_t>(u) * nb;
-    uint8_t* F = flags + static_cast<int64_t>(u) * nb;
-    const int lo = prefix, hi = nb - suffix, np = max(0, hi - lo);
-    for (int i = tid; i < n2; i += blockDim.x) {
-        s_key[i] = i < np ? loss_key(L[lo + i]) : ~0ull;
-        s_idx[i] = i < np ? static_cast<uint32_t>(lo + i) : 0xFFFFFFFFu;
-    }
-    for (int b = tid; b < nb; b += blockDim.x)
-        if (b < lo || b >= hi) F[b] = 1;  // protected blocks stay dense
-    __syncthreads();
-    for (int k = 2; k <= n2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = tid; i < n2; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const unsigned long long ki = s_key[i], kj = s_key[ixj];
-                    const uint32_t ii = s_idx[i], ij = s_idx[ixj];
-                    const bool gt = ki > kj || (ki == kj && ii > ij);
-                    if (gt == ((i & k) == 0)) {
-                        s_key[i] = kj;
-                        s_key[ixj] = ki;
-                        s_idx[i] = ij;
-                        s_idx[ixj] = ii;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-    for (int p = tid; p < np; p += blockDim.x) F[s_idx[p]] = p < quota ? 0 : 1;
-}
-static cudaError_t launch_rank(const double* losses, int n_units, int nb, int prefix, int suffix, int quota,
-                               uint8_t* flags, cudaStream_t s) {
-    const int np = nb - prefix - suffix;
-    if (np <= kSortMaxBlocks && getenv("HS_RANK_QUADRATIC") == nullptr) {
-        int n2 = 2;
-        while (n2 < np) n2 <<= 1;
-        const size_t smem = static_cast<size_t>(n2) * 12;
-        cudaError_t e = cudaFuncSetAttribute(sort_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        sort_select_kernel<<<n_units, 1024, smem, s>>>(losses, nb, prefix, suffix, quota, n2, flags);
-    } else {
-        rank_kernel<<<dim3((nb + 255) / 256, n_units), 256, 0, s>>>(losses, nb, prefix, suffix, quota, flags);
-    }
-    return cudaGetLastError();
-}
-
 // Slot assignment in block order (assemble_cache, compressed_cache.hpp:156-185):
 // index_map = +(dense rank + 1) or -(sparse rank + 1); slot_block inverts it.
 // flags_in == nullptr selects the static pattern (protected dense, prunable
@@ -718,12 +658,10 @@ static cudaError_t launch_rank(const double* losses, int n_units, int nb, int pr
 // A BlockMask whose dense count differs from the pool capacity (explicit masks
 // only) is a ConfigError recorded in the status word; slots past a pool are
 // then never written (block kernels skip them, slot_block stays in range).
-__global__ void __launch_bounds__(1024) assign_slots_kernel(const uint8_t* flags_in, int nb,
-                                                            int prefix, int suffix, int all_sparse,
-                                                            int dense_count, int16_t* index_map,
-                                                            int32_t* slot_block, uint8_t* flags_out,
-                                                            unsigned long long* status, int sparse_capacity) {
-    const int u = blockIdx.x, t = threadIdx.x;
+__device__ __forceinline__ void assign_slots_cta(int u, const uint8_t* flags_in, int nb, int prefix, int suffix, int all_sparse,
+                                                 int dense_count, int16_t* index_map, int32_t* slot_block,
+                                                 uint8_t* flags_out, unsigned long long* status, int sparse_capacity) {
+    const int t = threadIdx.x;
     const int per = (nb + 1023) / 1024;
     const int b0 = min(nb, t * per), b1 = min(nb, b0 + per);
     auto flag_of = [&](int b) -> int {
@@ -772,6 +710,166 @@ __global__ void __launch_bounds__(1024) assign_slots_kernel(const uint8_t* flags
         }
         if (flags_out) flags_out[static_cast<int64_t>(u) * nb + b] = static_cast<uint8_t>(f);
     }
+}
+__global__ void __launch_bounds__(1024) assign_slots_kernel(const uint8_t* flags_in, int nb, int prefix, int suffix, int all_sparse,
+                                                 int dense_count, int16_t* index_map, int32_t* slot_block,
+                                                 uint8_t* flags_out, unsigned long long* status, int sparse_capacity) {
+    assign_slots_cta(blockIdx.x, flags_in, nb, prefix, suffix, all_sparse, dense_count, index_map, slot_block,
+                     flags_out, status, sparse_capacity);
+}
+
+// The same selection by radix select (one 1024-thread CTA per unit): the
+// quota-th smallest orderable key T is found digit by digit (8 passes of an 8-bit
+// shared-memory histogram over the keys still matching the prefix), then a block
+// is sparse iff its key is below T, or equals T and it is among the first
+// `remaining` such blocks in index order (block-wide scans).  The key maps the
+// strict total order above onto unsigned integers: -0.0 -> +0.0 (the reference's
+// `<` treats them as equal), NaN above +inf.  Thread t keeps the keys of
+// prunable blocks t, t + 1024, ... in registers.  (A bitonic sort of the same pairs in one CTA
+// was issue-bound: 33 us per cache of 2048 blocks; radix select ~4 us.)
+constexpr int kSelectThreads = 1024, kSelectKpt = 16;
+constexpr int kSortMaxBlocks = kSelectThreads * kSelectKpt;  // 16384 blocks (1M tokens)
+__device__ __forceinline__ unsigned long long loss_key(double l) {
+    if (isnan(l)) return ~0ull;
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(l == 0.0 ? 0.0 : l));
+    return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+// Block-wide exclusive scan of v over 1024 threads; total in *total.
+__device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int t = s_warp[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        s_warp[lane] = t;  // inclusive warp totals
+    }
+    __syncthreads();
+    *total = s_warp[31];
+    const int r = x - v + (w ? s_warp[w - 1] : 0);
+    __syncthreads();  // s_warp is reused by the next scan
+    return r;
+}
+// Slots (assign_slots_cta) are assigned in the same CTA when index_map != nullptr.
+struct SlotOut {
+    int dense_count, sparse_capacity;
+    int16_t* index_map;
+    int32_t* slot_block;
+    uint8_t* flags_out;
+};
+__global__ void __launch_bounds__(kSelectThreads) radix_select_kernel(const double* losses, int nb, int prefix,
+                                                                      int suffix, int quota, uint8_t* flags,
+                                                                      SlotOut so) {
+    __shared__ int s_hist[256];
+    __shared__ int s_warp[32];
+    __shared__ int s_digit, s_remaining;
+    const int u = blockIdx.x, tid = threadIdx.x;
+    const double* L = losses + static_cast<int64_t>(u) * nb;
+    uint8_t* F = flags + static_cast<int64_t>(u) * nb;
+    const int lo = prefix, hi = nb - suffix, np = max(0, hi - lo);
+    for (int b = tid; b < nb; b += kSelectThreads)
+        if (b < lo || b >= hi) F[b] = 1;  // protected blocks stay dense
+    auto assign = [&]() {
+        if (so.index_map == nullptr) return;
+        __syncthreads();  // every flag of this unit written (CTA-scope ordering of the global stores)
+        assign_slots_cta(u, flags, nb, 0, 0, 0, so.dense_count, so.index_map, so.slot_block, so.flags_out, nullptr,
+                         so.sparse_capacity);
+    };
+    if (quota <= 0 || quota >= np) {  // nothing to rank: all prunable dense / all sparse
+        for (int i = tid; i < np; i += kSelectThreads) F[lo + i] = quota <= 0 ? 1 : 0;
+        assign();
+        return;
+    }
+    // key k of this thread is prunable block i = tid + k * 1024 (every warp holds keys)
+    const int nk = (np + kSelectThreads - 1) / kSelectThreads;
+    unsigned long long key[kSelectKpt];
+#pragma unroll
+    for (int k = 0; k < kSelectKpt; ++k) {
+        const int i = tid + k * kSelectThreads;
+        key[k] = k < nk && i < np ? loss_key(L[lo + i]) : 0ull;
+    }
+    unsigned long long pval = 0, pmask = 0;
+    int remaining = quota;  // selections still to make among keys matching the prefix
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        if (tid < 256) s_hist[tid] = 0;
+        __syncthreads();
+        // warp-aggregated increments: the leading digits of similar losses coincide,
+        // so per-key atomics on one bin would serialise
+#pragma unroll
+        for (int k = 0; k < kSelectKpt; ++k) {
+            if (k >= nk) break;
+            const int i = tid + k * kSelectThreads;
+            const bool in = i < np && (key[k] & pmask) == pval;
+            const int dg = in ? static_cast<int>((key[k] >> shift) & 0xFF) : 256;
+            const unsigned grp = __match_any_sync(0xffffffffu, dg);
+            if (in && (tid & 31) == __ffs(grp) - 1) atomicAdd(&s_hist[dg], __popc(grp));
+        }
+        __syncthreads();
+        if (tid < 32) {  // warp 0: the digit where the running count reaches `remaining`
+            int c[8], sum = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sum += (c[j] = s_hist[8 * tid + j]);
+            int incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= o) incl += y;
+            }
+            int before = incl - sum;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (before < remaining && remaining <= before + c[j]) {
+                    s_digit = 8 * tid + j;
+                    s_remaining = remaining - before;
+                }
+                before += c[j];
+            }
+        }
+        __syncthreads();
+        pval |= static_cast<unsigned long long>(s_digit) << shift;
+        pmask |= 0xFFull << shift;
+        remaining = s_remaining;
+        __syncthreads();  // s_digit / s_remaining read before the next pass writes them
+    }
+    // T = pval: every key below T is selected, and the first `remaining` keys equal
+    // to T in index order (ties to the lower block index): index order is (k, tid).
+    int base = 0;
+#pragma unroll
+    for (int k = 0; k < kSelectKpt; ++k) {
+        if (k >= nk) break;
+        const int i = tid + k * kSelectThreads;
+        const bool valid = i < np;
+        const bool eq = valid && key[k] == pval;
+        int total;
+        const int rank = base + block_exclusive_scan(eq ? 1 : 0, s_warp, &total);
+        base += total;
+        if (valid) F[lo + i] = (key[k] < pval || (eq && rank < remaining)) ? 0 : 1;
+    }
+    assign();
+}
+// so.index_map != nullptr: the slots are assigned too (*assigned = true) when the
+// radix-select kernel runs; the quadratic fallback leaves them to assign_slots_kernel.
+static cudaError_t launch_rank(const double* losses, int n_units, int nb, int prefix, int suffix, int quota,
+                               uint8_t* flags, cudaStream_t s, SlotOut so = SlotOut{}, bool* assigned = nullptr) {
+    if (assigned) *assigned = false;
+    const int np = nb - prefix - suffix;
+    if (np <= kSortMaxBlocks && getenv("HS_RANK_QUADRATIC") == nullptr) {
+        radix_select_kernel<<<n_units, kSelectThreads, 0, s>>>(losses, nb, prefix, suffix, quota, flags, so);
+        if (assigned) *assigned = so.index_map != nullptr;
+    } else {
+        rank_kernel<<<dim3((nb + 255) / 256, n_units), 256, 0, s>>>(losses, nb, prefix, suffix, quota, flags);
+    }
+    return cudaGetLastError();
 }
 
 // decompress (compressed_cache.hpp:271-298): pools -> logical [rows][d].
@@ -1116,11 +1214,17 @@ cudaError_t launch_prune_compress(const CompressLaunch& L, cudaStream_t s) {
     }
     // Loss-driven selection: classify -> rank -> assign -> pack.
     if ((err = blocks(0))) return err;
-    if ((err = launch_rank(L.losses, L.n_units, L.nb, L.prefix, L.suffix, L.quota, L.flags_tmp, s))) return err;
-    assign_slots_kernel<<<L.n_units, 1024, 0, s>>>(L.flags_tmp, L.nb, 0, 0, 0, L.dense_count,
-                                                   L.index_map, L.slot_block, L.flags_out, nullptr,
-                                                   L.sparse_count);
-    if ((err = cudaGetLastError())) return err;
+    bool assigned = false;
+    const SlotOut so{L.dense_count, L.sparse_count, L.index_map, L.slot_block, L.flags_out};
+    if ((err = launch_rank(L.losses, L.n_units, L.nb, L.prefix, L.suffix, L.quota, L.flags_tmp, s, so, &assigned)))
+        return err;
+    if (!assigned) {
+        assign_slots_kernel<<<L.n_units, 1024, 0, s>>>(L.flags_tmp, L.nb, 0, 0, 0, L.dense_count,
+                                                       L.index_map, L.slot_block, L.flags_out, nullptr,
+                                                       L.sparse_count);
+        if ((err = cudaGetLastError())) return err;
+    }
+    a.reverse = getenv("HS_COMPRESS_FORWARD") == nullptr;  // (tools: A/B of the pack order)
     return blocks(1);
 }
 

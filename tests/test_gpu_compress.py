@@ -474,3 +474,30 @@ def test_nan_losses_flag_exactly_quota_blocks(hs, port, axis_name):
     out = hs.decompress(c)
     torch.cuda.synchronize()
     assert out.shape == xt.shape
+
+
+@pytest.mark.parametrize("nb,prefix,suffix", [(2048, 0, 0), (3000, 5, 17), (16384, 1, 4), (40, 3, 2)])
+@pytest.mark.parametrize("s", [0.0, 0.1, 0.5, 0.9, 1.0])
+def test_select_blocks_radix_matches_stable_sort(hs, nb, prefix, suffix, s):
+    """hs_select_blocks (radix select) against select_blocks' stable ascending sort
+    (pruner.hpp:94-117): ties to the lower index (heavy ties drawn from a few values,
+    -0.0 == +0.0), NaN above +inf, protected prefix/suffix dense, exactly
+    floor(S * prunable) sparse."""
+    import torch
+    rng = np.random.default_rng(nb + int(100 * s))
+    U = 3
+    losses = rng.integers(0, 7, size=(U, nb)).astype(np.float64) * 0.25
+    losses[0, rng.integers(0, nb, 5)] = np.nan
+    losses[1, rng.integers(0, nb, 5)] = -0.0
+    losses[2, rng.integers(0, nb, 5)] = np.inf
+    sink, window = prefix * 64, suffix * 64
+    cfg = hs.SparsityConfig(s, s, 64, sink, window)
+    got = hs.select_blocks(torch.from_numpy(losses).cuda(), cfg, s).cpu().numpy()
+    np_ = nb - prefix - suffix
+    quota = int(np.floor(s * np_))
+    for u in range(U):
+        want = np.ones(nb, np.uint8)
+        lp = losses[u, prefix:nb - suffix]
+        order = np.lexsort((np.arange(np_), np.nan_to_num(lp, nan=0.0, posinf=np.inf), np.isnan(lp)))
+        want[prefix + order[:quota]] = 0
+        assert (got[u] == want).all(), (u, np.nonzero(got[u] != want)[0][:10])
