@@ -375,6 +375,41 @@ def leg_decode_grid(hs, dev, rank, world, scale, args, flush):
             "by_s_key_s_value": res}
 
 
+SMEM_BYTES_PER_CLK = 128  # per SM: one shared-memory port serves TMA writes, LSU and tensor-core operand reads
+
+
+def prefill_smem_bytes(kc, vc, L, G):
+    """Shared-memory bytes the prefill kernel moves for a causal n_q = n_kv = L pass over
+    every unit x G query heads: per 128-query x 128-key tile 108 KB
+    (Q operand reads 32, stabiliser MMA 8, row-sum MMA 36, P^T stores 32) plus per
+    64-key block K 32 KB dense / 18 KB 2:4 (TMA write, operand read, metadata) and
+    V 48 / 36 KB (TMA write, operand read, metadata, P^T operand read).  Tiles follow
+    the kernel's list: fully visible blocks paired by K kind, then diagonal blocks."""
+    ks = (kc.index_map < 0).cpu().numpy()
+    vs = (vc.index_map < 0).cpu().numpy()
+    U, nb = ks.shape
+    n_qt = (L + 127) // 128
+    total = 0
+    for u in range(U):
+        csk = np.concatenate([[0], np.cumsum(ks[u])])
+        csv = np.concatenate([[0], np.cumsum(vs[u])])
+        qt = np.arange(n_qt)
+        fv = np.minimum(nb, 2 * qt)                     # fully visible blocks
+        vis = np.minimum(nb, 2 * qt + 2)                # visible blocks (diagonal included)
+        ns = csk[fv]
+        nd = fv - ns
+        tiles = ns // 2 + nd // 2 + ns % 2 + nd % 2
+        d0 = np.minimum(fv, nb - 1)
+        d1 = np.minimum(fv + 1, nb - 1)
+        same = ks[u][d0] == ks[u][d1]
+        tiles = tiles + np.where(vis - fv == 2, np.where(same, 1, 2), vis - fv)
+        kspa, vspa = csk[vis], csv[vis]
+        blocks_k = (vis - kspa) * 32 + kspa * 18
+        blocks_v = (vis - vspa) * 48 + vspa * 36
+        total += int((tiles * 108 + blocks_k + blocks_v).sum()) * 1024
+    return total * G
+
+
 def leg_prefill(hs, D_, dev, rank, world, args):
     """configs[2]: Llama-3.1-8B prefill attention, causal, hierarchical mixed
     dense / 2:4 blocks at block sparsity S_K = S_V in {0, .25, .5, .75} (+1), fp16
@@ -409,9 +444,17 @@ def leg_prefill(hs, D_, dev, rank, world, args):
             ms = max_over_ranks(statistics.median(times), world)
             total = sum_over_ranks(flops, world)
             tflops = total / (ms * 1e-3) / 1e12
+            clk = cs.summary()
+            smem = sum_over_ranks(prefill_smem_bytes(kc, vc, Lp, G), world)
+            mhz = clk.get("sm_mhz") or 1965.0
+            smem_peak = SMEM_BYTES_PER_CLK * 148 * mhz * 1e6 * world  # bytes/s at the sampled clock
             entry = {"ms": round(ms, 3), "counted_tflops": round(tflops, 1), "frac": round(tflops / dense_peak, 4),
                      "frac_of_sustained": round(tflops / sustained_peak, 4) if sustained_peak else None,
-                     "counted_flops": int(total), "clocks": cs.summary()}
+                     "counted_flops": int(total), "clocks": clk,
+                     "smem_roofline": {"bytes": smem, "achieved_tbs": round(smem / (ms * 1e-3) / 1e12, 2),
+                                       "peak_tbs": round(smem_peak / 1e12, 2),
+                                       "frac": round(smem / (ms * 1e-3) / smem_peak, 4),
+                                       "model": "DESIGN.md 3.3: 128 B/clk/SM shared-memory port x 148 SMs x sampled SM clock"}}
             if rank == 0 and not args.skip_cpu and Lp <= 2 * args.prefill_ctx:
                 entry["parity"] = prefill_parity(hs, q, out, kc, vc, key, val, dt,
                                                  rows=64 if Lp > args.prefill_ctx else 256,
