@@ -238,9 +238,6 @@ __device__ __forceinline__ void exp2_fma2(float& x0, float& x1) {
 constexpr int kPolyPer8 = HS_PREFILL_POLY;  // default for the lockstep softmax
 static_assert(kPolyPer8 % 2 == 0, "polynomial exponentials run in packed pairs");
 
-#ifndef HS_PREFILL_EXP_FIRST
-#define HS_PREFILL_EXP_FIRST 0  // ping-pong: all exponentials before the P^T-buffer wait
-#endif
 #ifndef HS_PREFILL_EXP_F16X2
 #define HS_PREFILL_EXP_F16X2 0  // sm_100a splits f16x2 ex2 into two MUFU ops: no gain
 #endif
@@ -882,22 +879,14 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                 const int key_pos = ti.dblk * kBlock + r;
                 const bool row_valid = (r < 64 || ti.ve1 != 0) && (ti.dblk < 0 || key_pos < n_kv);
                 c_first = row_valid ? ((L.causal && ti.dblk >= 0) ? key_pos - off - q0 : 0) : 1 << 30;
-#ifdef HS_XP_OLDMASK
-                fast = __all_sync(0xffffffffu, c_first <= c0);
-#else
                 fast = __all_sync(0xffffffffu, c_first <= (QT > 64 ? (c0 & qmask) : 0));
-#endif
             }
 #pragma unroll
             for (int k = 0; k < 64; k += 2) ffma2(x[k], x[k + 1], sl2, 0.f, 0.f);  // s*scale*log2e - m_used
             if (!fast) {
 #pragma unroll
                 for (int k = 0; k < 64; ++k)
-#ifdef HS_XP_OLDMASK
-                    if (c0 + k < c_first) x[k] = -INFINITY;
-#else
                     if (((c0 + k) & qmask) < c_first) x[k] = -INFINITY;
-#endif
             }
             bool slow = pending || *reinterpret_cast<volatile int*>(&s_ver[ch]) != bver;
             if (!slow) {
@@ -966,35 +955,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_sempty[sb]);  // S^T[sb] consumed
-#if HS_PREFILL_EXP_FIRST
-            // Probabilities first (registers, packed 16-bit pairs), then the wait for
-            // this group's P^T buffer (GEMM2(t-2) + its l MMA done)
-            using PT0 = typename std::conditional<V16, __half, T>::type;  // P^T element type
-            uint32_t ph[32];
-#pragma unroll
-            for (int g8 = 0; g8 < 8; ++g8) {
-                float p[8];
-#pragma unroll
-                for (int k = 0; k < 8 - POLY; ++k) p[k] = fast_exp2(x[8 * g8 + k]);
-#pragma unroll
-                for (int k = 8 - POLY; k < 8; k += 2) {
-                    p[k] = x[8 * g8 + k];
-                    p[k + 1] = x[8 * g8 + k + 1];
-                    exp2_fma2(p[k], p[k + 1]);
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) ph[4 * g8 + k] = F16Traits<PT0>::pack(p[2 * k], p[2 * k + 1]);
-            }
-            if (t >= 2) mbar_wait_dbg(&bar_pempty[sb], ((t >> 1) - 1) & 1, dbgp, 22);  // P^T[sb] free (GEMM2(t-2) done)
-            if (tr0) trace(L, t, 3);
-            {
-                uint8_t* const pbuf = pbuf0 + sb * lay.p_bytes;
-#pragma unroll
-                for (int g8 = 0; g8 < 8; ++g8)
-                    *reinterpret_cast<uint4*>(pbuf + pt_base_h + ((static_cast<uint32_t>(g8) ^ r7) << 4)) =
-                        make_uint4(ph[4 * g8], ph[4 * g8 + 1], ph[4 * g8 + 2], ph[4 * g8 + 3]);
-            }
-#else
             if (t >= 2) mbar_wait_dbg(&bar_pempty[sb], ((t >> 1) - 1) & 1, dbgp, 22);  // P^T[sb] free (GEMM2(t-2) done)
             if (tr0) trace(L, t, 3);
             uint8_t* const pbuf = pbuf0 + sb * lay.p_bytes;
@@ -1030,7 +990,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     *reinterpret_cast<uint4*>(pbuf + 32768 + pto) = lo;
                 }
             }
-#endif
             if (tr0) trace(L, t, 12);
             bool need = false;
             if constexpr (!SAFE) {
@@ -1182,9 +1141,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
                     const int c = c0 + k16 + k;
                     const float o = v[k] * s_alpha[c];
                     const bool cv = (c & qmask) < rows_q;
-#ifndef HS_XP_NOBAD
                     bad |= cv && !(fabsf(o) <= 3.4e38f);
-#endif
                     if (cv) out_row(c)[r] = ntiles > 0 ? (V16 ? ldexpf(o, v_exp) : o) : 0.f;
                 }
             }
