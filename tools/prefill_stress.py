@@ -19,7 +19,9 @@ for i in range(n):
     s = float(rng.choice([0.0, 0.25, 0.5, 0.75, 1.0]))
     sink, window = int(rng.choice([0, 64, 100])), int(rng.choice([0, 128, 200]))
     causal = bool(rng.integers(0, 2))
-    U, gqa = int(rng.integers(1, 3)), int(rng.integers(1, 3))
+    U, gqa = int(rng.integers(1, 3)), int(rng.choice([1, 2, 4]))
+    hg = int(rng.choice([g for g in (1, 2, 4) if gqa % g == 0]))  # stacked-head layouts too
+    os.environ["HS_PREFILL_HG"] = str(hg)
     kc, vc, q = setup(hs, port, U, L, s, dtype, gqa, n_q, sink, window, seed=100 + i)
     scale = np.float32(1.0 / math.sqrt(128))
     t0 = time.time()
