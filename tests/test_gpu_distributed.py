@@ -71,6 +71,29 @@ def test_unit_shards_equal_rows_of_full_decode(hs, port):
         assert mx < 1e-5, (r, mx)
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_prefill_kv_head_shards_equal_rows_of_full_prefill(hs, port, world):
+    """configs[2] over N GPUs: rank r prefills the KV heads
+    heads_of_rank(8, N, r) with their GQA query heads -- compressed and attended on
+    their own -- and must reproduce the same heads of the single-GPU prefill (the
+    bench's prefill leg runs exactly this per rank; no collective)."""
+    from paper_2604_16864_b200 import distributed as D
+    U, L, gqa = 8, 1024, 4
+    kx = gen_units(port, U, L, 128, 13, 0, "f16")
+    vx = gen_units(port, U, L, 128, 13, 1, "f16")
+    q = np.stack([np.stack([port.round_to(port.random_gaussian(L, 128, port.head_seed(13, u, 2 + g)), "f16")
+                            for g in range(gqa)]) for u in range(U)])
+    cfg = hs.SparsityConfig(0.5, 0.5, 64, 64, 128)
+    kc, vc = hs.prune_cache(to_torch(kx, "f16"), to_torch(vx, "f16"), cfg)
+    full = hs.prefill_attention(to_torch(q, "f16"), kc, vc, causal=True).cpu().numpy()
+    for r in range(world):
+        sh = D.heads_of_rank(U, world, r)
+        ks, vs = hs.prune_cache(to_torch(kx[sh.begin:sh.end], "f16"), to_torch(vx[sh.begin:sh.end], "f16"), cfg)
+        got = hs.prefill_attention(to_torch(q[sh.begin:sh.end], "f16"), ks, vs, causal=True).cpu().numpy()
+        mx, _ = err_stats(got, full[sh.begin:sh.end])
+        assert mx < 1e-3, (r, mx)  # same arithmetic per head; the running max is per CTA
+
+
 @pytest.mark.parametrize("world,s,sink,window", [(2, 0.5, 64, 256), (4, 0.25, 100, 70), (8, 0.75, 0, 512)])
 def test_sharded_pruning_equals_whole_sequence(hs, port, world, s, sink, window):
     """prune_cache_sharded's device steps per simulated rank (block losses of the
