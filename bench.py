@@ -523,21 +523,21 @@ def leg_compress(hs, dev, rank, world, args, flush):
         nbytes = 2 * key.numel() * 2 + outp[0].nbytes() + outp[1].nbytes() + 2 * U * outp[0].logical_blocks * (8 + 1 + 4)
         res[f"prune_cache_s{s:g}"] = {"ms": round(ms, 4), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
                                       "frac_of_hbm": round(nbytes / (ms * 1e-3) / 1e9 / hbm, 4), "bytes": int(nbytes),
-                                      "selection": "static" if s == 1.0 else "loss-driven (classify, rank, pack)"}
+                                      "selection": "static" if s == 1.0 else "loss-driven (classify, radix select, pack)",
+                                      "call": "hierasparse.prune_cache (value cache on a side stream)"}
     kp, vp = hs.prune_cache(key, val, hs.SparsityConfig(0.5, 0.5, 64))
     dec = hs.SparsityConfig(1.0, 1.0, 64)
     k2, v2 = hs.recompress(kp, dec, 1.0), hs.recompress(vp, dec, 1.0)
     st = hs.StatusWord(dev)
 
-    def rc():
-        hs.recompress(kp, dec, 1.0, check=False, status=st)
-        hs.recompress(vp, dec, 1.0, check=False, status=st)
+    def rc():  # the decode-phase re-prune of both caches (value cache on a side stream)
+        hs.recompress_pair(kp, vp, dec, check=False, status=st)
     ms = max_over_ranks(min(time_steps(rc, args.steps, 3, flush)), world)
     st.check()
     nbytes = kp.nbytes() + vp.nbytes() + k2.nbytes() + v2.nbytes() + 2 * U * k2.logical_blocks * (8 + 1 + 4)
     res["recompress_s0.5_to_1"] = {"ms": round(ms, 4), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
                                    "frac_of_hbm": round(nbytes / (ms * 1e-3) / 1e9 / hbm, 4), "bytes": int(nbytes),
-                                   "call": "hierasparse.recompress x2 (hs_recompress, one pass, no host sync)"}
+                                   "call": "hierasparse.recompress_pair (hs_recompress per cache, one pass, no host sync)"}
     del key, val, kp, vp, k2, v2
     torch.cuda.empty_cache()
     return res

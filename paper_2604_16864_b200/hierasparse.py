@@ -196,8 +196,39 @@ def prune_cache(key: torch.Tensor, value: torch.Tensor, cfg: SparsityConfig, out
     if key.shape[-1] % 4:
         raise ConfigError("prune_cache: head dimension not divisible by m_group")
     ko, vo = out if out is not None else (None, None)
-    return (prune_compress(key, cfg, cfg.s_key, capi.AXIS_CHANNEL, ko),
-            prune_compress(value, cfg, cfg.s_value, capi.AXIS_SEQUENCE, vo))
+    if not (key.is_cuda and value.is_cuda):
+        return (prune_compress(key, cfg, cfg.s_key, capi.AXIS_CHANNEL, ko),
+                prune_compress(value, cfg, cfg.s_value, capi.AXIS_SEQUENCE, vo))
+    # The two caches are independent: the value cache runs on a side stream (forked
+    # from and joined back into the caller's stream), so one cache's selection
+    # kernels -- a CTA per unit -- overlap the other cache's block kernels.  Both
+    # outputs are allocated on the caller's stream before the fork.
+    if vo is None:
+        vo = _alloc_cache(value, cfg, cfg.s_value, capi.AXIS_SEQUENCE)
+    main = torch.cuda.current_stream(key.device)
+    side = _side_stream(key.device)
+    side.wait_stream(main)
+    kc = prune_compress(key, cfg, cfg.s_key, capi.AXIS_CHANNEL, ko)
+    with torch.cuda.stream(side):
+        vc = prune_compress(value, cfg, cfg.s_value, capi.AXIS_SEQUENCE, vo)
+    main.wait_stream(side)
+    return kc, vc
+
+
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(device) -> "torch.cuda.Stream":
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    if idx not in _SIDE_STREAMS:
+        _SIDE_STREAMS[idx] = torch.cuda.Stream(device=idx)
+    return _SIDE_STREAMS[idx]
+
+
+def _alloc_cache(x: torch.Tensor, cfg: SparsityConfig, sparsity: float, axis: int) -> DeviceCompressedCache:
+    U, rows, d = (x.shape if x.dim() == 3 else (1, *x.shape))
+    nb, dc, sc, _, _ = pool_counts(rows, cfg, sparsity)
+    return DeviceCompressedCache(x.dtype, axis, U, nb, dc, sc, x.device, d, cfg.block_size, cfg)
 
 
 def block_losses(x: torch.Tensor, cfg: SparsityConfig, axis: int) -> torch.Tensor:
@@ -318,10 +349,16 @@ def recompress(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: float, c
     reference's chain on the same pools.  A corrupt input cache raises
     decompress's DataError (check=False defers it to out.status.check(), so the
     call stays free of host synchronisation, e.g. inside a CUDA graph)."""
-    rows = c.logical_blocks * c.block_size
-    nb, dc, sc, _, _ = pool_counts(rows, cfg, sparsity)
-    out = DeviceCompressedCache(c.dtype, c.axis, c.n_units, nb, dc, sc, c.index_map.device, c.head_dim,
+    return _recompress_into(c, cfg, sparsity, _recompress_out(c, cfg, sparsity), check, status)
+
+
+def _recompress_out(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: float) -> DeviceCompressedCache:
+    nb, dc, sc, _, _ = pool_counts(c.logical_blocks * c.block_size, cfg, sparsity)
+    return DeviceCompressedCache(c.dtype, c.axis, c.n_units, nb, dc, sc, c.index_map.device, c.head_dim,
                                  cfg.block_size, cfg)
+
+
+def _recompress_into(c, cfg, sparsity, out, check, status):
     cc = cfg.c()
     st = _status(status, out.index_map.device)
     capi.check(capi.load().hs_recompress(c.cref(), C.byref(cc), sparsity, out.cref(), out.losses.data_ptr(),
@@ -381,10 +418,24 @@ def recompress_unfused(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: 
     return out
 
 
-def recompress_pair(k: DeviceCompressedCache, v: DeviceCompressedCache, cfg: SparsityConfig):
+def recompress_pair(k: DeviceCompressedCache, v: DeviceCompressedCache, cfg: SparsityConfig, check: bool = True,
+                    status: StatusWord | None = None):
     """prune_cache at the decode sparsity (cfg.s_key / cfg.s_value) of already
-    compressed caches (pipeline.hpp:228-240, "further pruned")."""
-    return recompress(k, cfg, cfg.s_key), recompress(v, cfg, cfg.s_value)
+    compressed caches (pipeline.hpp:228-240, "further pruned").  The
+    value cache runs on a side stream forked from and joined into the caller's
+    stream (outputs allocated on the caller's stream first), as in prune_cache."""
+    st = _status(status, k.index_map.device)
+    vo = _recompress_out(v, cfg, cfg.s_value)
+    main = torch.cuda.current_stream(k.index_map.device)
+    side = _side_stream(k.index_map.device)
+    side.wait_stream(main)
+    k2 = recompress(k, cfg, cfg.s_key, check=False, status=st)
+    with torch.cuda.stream(side):
+        v2 = _recompress_into(v, cfg, cfg.s_value, vo, False, st)
+    main.wait_stream(side)
+    if check:
+        st.check()
+    return k2, v2
 
 
 def _tails(k_tail, v_tail, U, d, dtype):

@@ -501,3 +501,23 @@ def test_select_blocks_radix_matches_stable_sort(hs, nb, prefix, suffix, s):
         order = np.lexsort((np.arange(np_), np.nan_to_num(lp, nan=0.0, posinf=np.inf), np.isnan(lp)))
         want[prefix + order[:quota]] = 0
         assert (got[u] == want).all(), (u, np.nonzero(got[u] != want)[0][:10])
+
+
+def test_pair_entry_points_match_single_cache_calls(hs, port):
+    """prune_cache / recompress_pair run the value cache on a side stream: results
+    equal the single-cache calls on the caller's stream, bit for bit."""
+    import torch
+    U, rows = 3, 4096
+    kx = to_torch(gen_units(port, U, rows, 128, 21, 0, "bf16"), "bf16")
+    vx = to_torch(gen_units(port, U, rows, 128, 21, 1, "bf16"), "bf16")
+    cfg = hs.SparsityConfig(0.5, 0.75, 64, 64, 128)
+    kc, vc = hs.prune_cache(kx, vx, cfg)
+    k1 = hs.prune_compress(kx, cfg, cfg.s_key, 0)
+    v1 = hs.prune_compress(vx, cfg, cfg.s_value, 1)
+    dec = hs.SparsityConfig(1.0, 1.0, 64, 64, 128)
+    k2, v2 = hs.recompress_pair(kc, vc, dec)
+    k3, v3 = hs.recompress(kc, dec, 1.0), hs.recompress(vc, dec, 1.0)
+    torch.cuda.synchronize()
+    for a, b in ((kc, k1), (vc, v1), (k2, k3), (v2, v3)):
+        for u in range(U):
+            assert_cache_equal(a, u, device_to_oracle(b, u))
