@@ -6,12 +6,14 @@
 // (assemble_cache, fused_magnitude_compress).  Pipeline per cache kind:
 //
 //   static selection (quota 0 or all prunable, known on the host):
-//     assign_slots  -> pack<with losses>                    (source read once)
+//     pack<with losses>, each CTA deriving its own slot     (source read once)
 //   loss-driven selection (0 < quota < prunable):
-//     classify (losses) -> rank (flags) -> assign_slots -> pack
+//     classify (losses) -> radix select + slot assignment (a CTA per unit) -> pack
+//   explicit BlockMask / ElementMask: assign_slots -> pack
 //
 // Layout: source [unit][rows][d] token-major 16-bit.  One CTA per 64x128 block
-// (16 KB): 16-byte vector loads, coalesced stores of the stored layouts.
+// (16 KB): one bulk copy into shared memory, coalesced stores of the stored
+// layouts.
 #include "common.cuh"
 #include "kernels.h"
 
