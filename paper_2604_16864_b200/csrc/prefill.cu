@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
         uint4* ob = reinterpret_cast<uint4*>(base_ptr + lay.off_bias);
         const uint32_t one = F16Traits<T>::pack(1.f, 1.f);
         const uint32_t one16 = F16Traits<__half>::pack(1.f, 1.f);  // the l MMA's B operand (fp16 P^T)
-        for (int i = tid; i < 4 * 128; i += 32 * kSoftWarps)
+        for (int i = tid; i < (V16 ? 4 : 3) * 128; i += 32 * kSoftWarps)  // (fp16 ones: V16 only)
             ob[i] = i < 128 ? make_uint4(one, one, one, one)
                             : i >= 384 ? make_uint4(one16, one16, one16, one16) : make_uint4(0u, 0u, 0u, 0u);
         if (tid < 128) {
@@ -1427,7 +1427,21 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s, int* n_kernel
     lay.v_e = 2 * lay.vblk;
     lay.v_stage = lay.v_e + 4096u;
     lay.tile_cap = static_cast<uint32_t>(prefill_tile_cap(L.nb, L.n_tail_blocks));
-    const uint32_t tiles_bytes = (lay.tile_cap * sizeof(TileInfo) + 1023u) & ~1023u;
+    const uint32_t tiles_bytes = (lay.tile_cap * sizeof(TileInfo) + 127u) & ~127u;
+    // the fp16 ones operand of the row-sum MMA exists only on the bf16 (v16) path
+    const uint32_t bias_bytes = L.v16 ? kBiasBytes : kBiasBytes - 2048u;
+    // static shared memory of the two kernel families (queried once): the plans use
+    // the real figure, not an estimate -- a few KB decide whether a dense-stage
+    // plan keeps two V stages at 128K
+    static int static_pp = -1, static_ls = -1;
+    if (static_pp < 0) {
+        cudaFuncAttributes fa{};
+        static_pp = cudaFuncGetAttributes(&fa, prefill_kernel<__half, false, false, true, 2>) == cudaSuccess
+                        ? static_cast<int>(fa.sharedSizeBytes) : 12288;
+        static_ls = cudaFuncGetAttributes(&fa, prefill_kernel<__half, false, false, false>) == cudaSuccess
+                        ? static_cast<int>(fa.sharedSizeBytes) : 8192;
+        (void)cudaGetLastError();
+    }
     lay.off_q = 0;
     lay.off_p = 32768;
     lay.p_bytes = hilo ? 65536u : 32768u;  // P^T (hi [+ lo]) per buffer
@@ -1443,7 +1457,7 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s, int* n_kernel
     const uint32_t plans_pp[][3] = {{2, 3, 3}, {2, 2, 3}, {2, 3, 2}, {2, 2, 2}, {2, 1, 3}, {2, 1, 2}, {2, 3, 1},
                                     {2, 2, 1}};
     auto choose = [&](uint32_t static_bytes, bool for_pp) {
-        const uint32_t budget = 227u * 1024u - static_bytes - 1024u /*align*/ - tiles_bytes - kBiasBytes;
+        const uint32_t budget = 227u * 1024u - static_bytes - 1024u /*align*/ - tiles_bytes - bias_bytes;
         const uint32_t(*list)[3] = for_pp ? plans_pp : plans;
         const int n = for_pp ? static_cast<int>(sizeof(plans_pp) / sizeof(plans_pp[0]))
                              : static_cast<int>(sizeof(plans) / sizeof(plans[0]));
@@ -1464,9 +1478,10 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s, int* n_kernel
     // 64 KB a buffer) and a plan with two buffers.  Measured at 64K: +11% on
     // fully 2:4 caches (softmax-bound), +1-2% with dense stages (ring-bound, hence
     // the two-V-stage plan preference above).
-    bool pp = !hilo && getenv("HS_PREFILL_NO_PP") == nullptr && choose(12288u, true) && lay.n_pbuf == 2;
-    if (getenv("HS_PREFILL_FORCE_PP")) pp = !hilo && choose(12288u, true) && lay.n_pbuf == 2;  // tools
-    if (!pp && !choose(8192u, false)) return cudaErrorInvalidConfiguration;
+    const uint32_t st_pp = static_cast<uint32_t>(static_pp) + 128u, st_ls = static_cast<uint32_t>(static_ls) + 128u;
+    bool pp = !hilo && getenv("HS_PREFILL_NO_PP") == nullptr && choose(st_pp, true) && lay.n_pbuf == 2;
+    if (getenv("HS_PREFILL_FORCE_PP")) pp = !hilo && choose(st_pp, true) && lay.n_pbuf == 2;  // tools
+    if (!pp && !choose(st_ls, false)) return cudaErrorInvalidConfiguration;
     if (const char* env = getenv("HS_PREFILL_PLAN")) {  // tools: "pbuf,nk,nv"
         unsigned a, b, c;
         if (sscanf(env, "%u,%u,%u", &a, &b, &c) == 3) {
@@ -1483,7 +1498,7 @@ cudaError_t launch_prefill(const PrefillLaunch& L, cudaStream_t s, int* n_kernel
     lay.off_v = lay.off_k + lay.nk * lay.k_stage;
     lay.off_tiles = lay.off_v + lay.nv * lay.v_stage;
     lay.off_bias = lay.off_tiles + tiles_bytes;
-    size_t smem = lay.off_bias + kBiasBytes + 1024;
+    size_t smem = lay.off_bias + bias_bytes + 1024;
     const size_t epi = lay.off_p + kSoftWG * 128 * (kCols + 1) * 4 + 1024;  // lockstep epilogue scratch
     if (!pp && smem < epi) smem = epi;
     {
