@@ -335,7 +335,10 @@ def leg_config5(hs, D_, dev, rank, world, scale, args, flush):
            "us_per_step": round(ms * 1e3, 2), "gbs": round(total / (ms * 1e-3) / 1e9, 1),
            "partial_us": round(ms_part * 1e3, 2),
            "partial_per_gpu_frac_of_hbm": round(nbytes / (t_part * 1e-3) / 1e9 / hbm, 4),
-           "gather_combine_us": round(ms_gc * 1e3, 2),
+           # added by the gather + combine inside the pipelined step (step - partial alone)
+           "gather_combine_us": round(max(0.0, ms - ms_part) * 1e3, 2),
+           # timed alone: an idle GPU waiting on the host-side enqueue of the two calls
+           "gather_combine_standalone_us": round(ms_gc * 1e3, 2),
            "gather_bytes_per_gpu": int(out["p"].numel() * 4), "bytes_per_step": int(total),
            "collective": "all_gather_into_tensor (NCCL)" if world > 1 else "none (1 GPU)"}
     if rank == 0 and not args.skip_cpu:
