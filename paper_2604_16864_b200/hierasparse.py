@@ -451,11 +451,14 @@ def _tails(k_tail, v_tail, U, d, dtype):
     return k_tail, v_tail, k_tail.shape[1]
 
 
-def _check_queries(q: torch.Tensor, k: DeviceCompressedCache, what: str) -> None:
+def _check_queries(q: torch.Tensor, k: DeviceCompressedCache, what: str, host_ok: bool = False) -> None:
     """The device kernels read q as [units, ..., head_dim] of the caches' 16-bit
-    dtype: reject anything else instead of reinterpreting its bits."""
-    if not isinstance(q, torch.Tensor) or not q.is_cuda:
-        raise ConfigError(f"{what}: queries must be a CUDA tensor")
+    dtype: reject anything else instead of reinterpreting its bits.  host_ok: a
+    contiguous pinned host tensor is accepted too (read over the host link)."""
+    pinned = host_ok and isinstance(q, torch.Tensor) and not q.is_cuda and q.is_pinned() and q.is_contiguous()
+    if not isinstance(q, torch.Tensor) or not (q.is_cuda or pinned):
+        raise ConfigError(f"{what}: queries must be a CUDA tensor" +
+                          (" or a contiguous pinned host tensor" if host_ok else ""))
     if q.dtype != k.dtype:
         raise ConfigError(f"{what}: query dtype {q.dtype} differs from the caches' {k.dtype}")
     if q.dim() < 2 or q.shape[0] != k.n_units or q.shape[-1] != k.head_dim:
@@ -484,9 +487,13 @@ def decode_attention(q: torch.Tensor, k: DeviceCompressedCache | None, v: Device
                      scale: float | None = None, splits: int = 0,
                      out: torch.Tensor | None = None) -> torch.Tensor:
     """decode_attention (attention.hpp:360-409) for every unit: q [units, gqa, d] -> fp32.
-    k = v = None attends to the dense tail alone (CacheView without a compressed cache)."""
+    k = v = None attends to the dense tail alone (CacheView without a compressed cache).
+    q and out may be contiguous pinned host tensors (zero-copy: the kernel reads q and
+    writes out over the host link; out is complete once the stream synchronises)."""
     k, v = _tail_only_view(k, v, k_tail, v_tail, q, "decode_attention")
-    _check_queries(q, k, "decode_attention")
+    _check_queries(q, k, "decode_attention", host_ok=True)
+    if out is not None and not out.is_cuda and not (out.is_pinned() and out.is_contiguous()):
+        raise ConfigError("decode_attention: out must be a CUDA tensor or a contiguous pinned host tensor")
     U = k.n_units
     if q.dim() != 3 or not q.is_contiguous():
         q = q.reshape(U, -1, k.head_dim).contiguous()
@@ -494,7 +501,7 @@ def decode_attention(q: torch.Tensor, k: DeviceCompressedCache | None, v: Device
     kt, vt, tail = _tails(k_tail, v_tail, U, k.head_dim, k.dtype)
     scale = 1.0 / math.sqrt(k.head_dim) if scale is None else scale
     if out is None:
-        out = torch.empty((U, gqa, k.head_dim), dtype=torch.float32, device=q.device)
+        out = torch.empty((U, gqa, k.head_dim), dtype=torch.float32, device=k.index_map.device)
     capi.check(_LIB().hs_decode(q.data_ptr(), k.cref(), v.cref(), _ptr(kt), _ptr(vt), tail, gqa,
                                 scale, splits, out.data_ptr(), _stream()))
     return out

@@ -218,6 +218,22 @@ def test_decode_plan_host_io(hs, port):
         assert (out - want).abs().max().item() < 1e-5
 
 
+def test_decode_pinned_host_queries_and_output(hs, port):
+    """decode_attention on a pinned host q with a pinned host out (zero-copy) equals
+    the device-resident call; a pageable host q is rejected."""
+    import torch
+    U, L = 3, 4096
+    kx, vx, kc, vc = build_caches(hs, port, U, L, 0.5, "bf16", seed=41)
+    q = to_torch(decode_queries(port, U, 12, "bf16", seed=41), "bf16")  # 12 rows: two row chunks
+    want = hs.decode_attention(q, kc, vc).cpu()
+    out = torch.empty(want.shape, dtype=torch.float32).pin_memory()
+    hs.decode_attention(q.cpu().pin_memory(), kc, vc, out=out)
+    torch.cuda.synchronize()
+    assert (out - want).abs().max().item() < 1e-5
+    with pytest.raises(hs.ConfigError):
+        hs.decode_attention(q.cpu(), kc, vc)
+
+
 @pytest.mark.parametrize("tail", [1, 37, 200])
 def test_decode_tail_only_view(hs, port, tail):
     """CacheView{compressed = nullptr, dense_tail} (attention.hpp:22-31): decode over
