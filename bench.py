@@ -181,6 +181,15 @@ class Flusher:
         torch.sum(self.buf, dim=0, out=self.sink)
 
 
+def hold_stream(steps: int):
+    """Hold the stream with a device-side sleep while the host enqueues the timed
+    steps, so a host hiccup (the clock sampler's nvidia-smi fork, GC) cannot leave the
+    GPU idle between a step's start event and its kernels: measured, such gaps put
+    60-140 us outliers into an otherwise 57 us decode step."""
+    import torch
+    torch.cuda._sleep(int(1.965e9 * min(0.05, 0.005 + 0.0005 * steps)))
+
+
 def time_steps(step, steps: int, warmup: int, flush=None) -> list:
     """Device time (ms) of `steps` calls of step() on the current stream, after
     `warmup` untimed calls; L2 flushed before each timed call when given."""
@@ -189,6 +198,7 @@ def time_steps(step, steps: int, warmup: int, flush=None) -> list:
         step()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    hold_stream(steps)
     for a, b in ev:
         if flush is not None:
             flush()
@@ -643,6 +653,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         t_wall = time.perf_counter()
+        hold_stream(args.steps)
         for i in range(args.steps):
             flush()
             starts[i].record()
