@@ -236,7 +236,9 @@ HS_API hs_status hs_decode(const void* q, const hs_device_cache* k, const hs_dev
  * a captured decode graph that owns its workspace shares no state with other
  * decode work, whatever stream handle it is replayed on.  The workspace must
  * hold hs_decode_workspace_bytes(k, gqa, splits) bytes and be zeroed before
- * its first use (the kernels re-arm their counters). */
+ * its first use (the kernels re-arm their counters and leave the combine's
+ * tagged mailbox empty).  It serves one (k geometry, gqa, splits): zero it
+ * again before using it for another. */
 HS_API hs_status hs_decode_workspace_bytes(const hs_device_cache* k, uint32_t gqa, uint32_t splits,
                                            uint64_t* bytes);
 HS_API hs_status hs_decode_ws(const void* q, const hs_device_cache* k, const hs_device_cache* v,

@@ -178,7 +178,7 @@ struct Workspace {
 std::mutex g_ws_mu;
 std::map<std::tuple<int, cudaStream_t, int>, Workspace> g_ws;
 
-enum WsKind { kWsCompress = 0, kWsDecode = 1, kWsMisc = 2, kWsPrefill = 3 };
+enum WsKind { kWsCompress = 0, kWsDecode = 1, kWsMisc = 2, kWsPrefill = 3, kWsMailbox = 4 };
 
 std::vector<void*> g_ws_retired;  // outgrown workspaces: never freed (a captured graph may still use them)
 
@@ -601,6 +601,13 @@ HS_API hs_status hs_status_word_decode(uint64_t word) {
 
 constexpr int kDynamicMaxBlocks = 256;  // blocks per split up to which decode claims blocks dynamically
 
+static size_t decode_plain_bytes(uint32_t n_units, int ns, uint32_t gqa) {
+    return ((static_cast<size_t>(n_units) * ns * gqa * (hs::kHeadDim + 2) * sizeof(float) + 255) / 256) * 256;
+}
+static size_t decode_mailbox_bytes(uint32_t n_units, int ns, uint32_t gqa) {
+    return static_cast<size_t>(n_units) * ns * gqa * hs::kHeadDim * 2 * sizeof(unsigned long long);
+}
+
 // Split count and workspace bytes of a decode launch (counters + split partials).
 static void decode_geometry(uint32_t n_units, uint32_t span, uint32_t gqa, uint32_t splits, int* ns_out,
                             size_t* cnt_bytes, size_t* part_bytes) {
@@ -608,7 +615,9 @@ static void decode_geometry(uint32_t n_units, uint32_t span, uint32_t gqa, uint3
     if (ns > static_cast<int>(span)) ns = static_cast<int>(span);  // attention.hpp:373-374 clamp
     if (ns < 1) ns = 1;
     *ns_out = ns;
-    *part_bytes = static_cast<size_t>(n_units) * ns * gqa * (hs::kHeadDim + 2) * sizeof(float);
+    // split partials [u][ns][gqa][d+2] f32, then the coop combine's tagged
+    // mailbox [u][ns][gqa][d] x 16 B (decode.cu)
+    *part_bytes = decode_plain_bytes(n_units, ns, gqa) + decode_mailbox_bytes(n_units, ns, gqa);
     *cnt_bytes = ((3 * static_cast<size_t>(n_units) * sizeof(int) + 255) / 256) * 256;
 }
 
@@ -748,19 +757,31 @@ static hs_status decode_common_rows(const void* q, const hs_device_cache* k, con
                     "decode_attention: %d blocks per CTA exceeds the index stage; use more splits",
                     L.max_blocks_per_cta);
     if ((st = fill_decode_maps(L, k, v))) return st;
+    // The combine mailbox must read as empty (zero) before every launch that uses
+    // it; its launches leave it so, but plain split partials must never land on
+    // it.  A caller's workspace serves one (k, gqa, splits) geometry:
+    // [counters][mailbox sized for the largest row chunk][plain partials].  The
+    // per-stream workspaces serve any geometry, so the mailbox gets its own.
     uint8_t* ws;
+    const uint32_t gmax = q_rows < 8 ? q_rows : 8;
     if (user_ws != nullptr) {
-        HS_CHECK_CONFIG(user_ws_bytes >= cnt_bytes + part_bytes,
+        int ns_max;
+        size_t cnt_max, part_max;
+        decode_geometry(L.n_units, static_cast<uint32_t>(span), gmax, splits, &ns_max, &cnt_max, &part_max);
+        HS_CHECK_CONFIG(user_ws_bytes >= cnt_max + part_max,
                         "decode_attention: workspace of %llu bytes is smaller than the %llu needed",
                         static_cast<unsigned long long>(user_ws_bytes),
-                        static_cast<unsigned long long>(cnt_bytes + part_bytes));
+                        static_cast<unsigned long long>(cnt_max + part_max));
         ws = static_cast<uint8_t*>(user_ws);
+        L.mailbox = reinterpret_cast<unsigned long long*>(ws + cnt_bytes);
+        L.partial = reinterpret_cast<float*>(ws + cnt_bytes + decode_mailbox_bytes(L.n_units, ns, gmax));
     } else {
-        ws = static_cast<uint8_t*>(workspace(s, cnt_bytes + part_bytes, kWsDecode, &st));
+        ws = static_cast<uint8_t*>(workspace(s, cnt_bytes + decode_plain_bytes(L.n_units, ns, gqa), kWsDecode, &st));
         if (st) return st;
+        L.mailbox = nullptr;  // allocated below when the launch combines cooperatively
+        L.partial = reinterpret_cast<float*>(ws + cnt_bytes);
     }
     L.counters = reinterpret_cast<int*>(ws);
-    L.partial = reinterpret_cast<float*>(ws + cnt_bytes);
     L.out = out;
     L.out_mode = out_mode;
     // The parallel combine spins on the unit's arrivals: only when the whole grid
@@ -768,6 +789,13 @@ static hs_status decode_common_rows(const void* q, const hs_device_cache* k, con
     // so residency is guaranteed, not assumed (decode.cu launch_t).
     L.coop_combine = static_cast<int64_t>(ns) * L.n_units <= static_cast<int64_t>(hs::decode_resident_ctas(L, sm_count()));
     if (const char* env = getenv("HS_DECODE_COOP")) L.coop_combine = L.coop_combine && atoi(env) != 0;
+    if (L.coop_combine && user_ws == nullptr) {
+        L.mailbox = static_cast<unsigned long long*>(
+            workspace(s, decode_mailbox_bytes(L.n_units, ns, gqa), kWsMailbox, &st));
+        if (st) return st;
+    }
+    if (const char* env = getenv("HS_DECODE_MAILBOX"))  // tools: A/B of the tagged-mailbox combine
+        if (atoi(env) == 0) L.mailbox = nullptr;
     L.blk_ctr = L.counters + 2 * L.n_units;
     // splits == 0 (auto): the unit's CTAs claim blocks dynamically (balanced across
     // SMs, summation order varies run to run).  An explicit split count keeps the

@@ -282,6 +282,19 @@ __device__ __forceinline__ void mma_16816<__half>(float (&d)[4], const uint32_t 
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// Single-copy-atomic 64-bit relaxed accesses at device scope (tagged mailboxes:
+// the payload carries its own validity, no separate flag / fence round trip).
+__device__ __forceinline__ void st_relaxed_gpu_v2(unsigned long long* p, unsigned long long a,
+                                                  unsigned long long b) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;\n\tst.relaxed.gpu.global.b64 [%0+8], %2;"
+                 ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_b64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

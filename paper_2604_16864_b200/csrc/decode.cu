@@ -473,7 +473,33 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     const int stride_p = gqa * (kHeadDim + 2);
     float* part = L.partial + (static_cast<int64_t>(u) * L.nsplit + split) * stride_p;
     constexpr float kLn2 = 0.6931471805599453f;
-    for (int idx = threadIdx.x; idx < gqa * (kHeadDim + 1); idx += nthr) {
+    // Tagged mailbox (coop combine): every (split, row, column) slot carries its
+    // own O, m and l in two single-copy-atomic 64-bit words whose non-zero tags
+    // mark them valid, so readers wait on the data itself -- no CTA barrier,
+    // release atomic and acquire poll between the stores and the combine's loads
+    // (each a device-scope round trip at the end of the step).
+    unsigned long long* const mbox = L.coop_combine && L.out != nullptr && L.debug_tail == 0 ? L.mailbox : nullptr;
+    if (mbox) {
+        unsigned long long* mb = mbox + (static_cast<int64_t>(u) * L.nsplit + split) * gqa * kHeadDim * 2;
+        for (int idx = threadIdx.x; idx < gqa * kHeadDim; idx += nthr) {
+            const int qq = idx / kHeadDim, c = idx % kHeadDim;
+            float M = -INFINITY;
+            for (int w = 0; w < NW; ++w) M = fmaxf(M, s_m[w * kMaxGqa + qq]);
+            float acc = 0.f, accl = 0.f;
+            for (int w = 0; w < NW; ++w) {
+                const float mw = s_m[w * kMaxGqa + qq];
+                const float wt = (mw == -INFINITY) ? 0.f : fast_exp2(mw - M);
+                acc += wt * s_o[(w * kMaxGqa + qq) * kHeadDim + c];
+                accl += wt * s_l[w * kMaxGqa + qq];
+            }
+            // ~bits(O) is never 0 (0xFFFFFFFF is no arithmetic result), l's tag is 1
+            st_relaxed_gpu_v2(mb + 2 * idx,
+                              static_cast<unsigned long long>(~__float_as_uint(acc)) |
+                                  (static_cast<unsigned long long>(__float_as_uint(M * kLn2)) << 32),
+                              static_cast<unsigned long long>(__float_as_uint(accl)) | (1ull << 32));
+        }
+    }
+    for (int idx = threadIdx.x; idx < (mbox ? 0 : gqa * (kHeadDim + 1)); idx += nthr) {
         const int qq = idx / (kHeadDim + 1), c = idx % (kHeadDim + 1);
         float M = -INFINITY;
         for (int w = 0; w < NW; ++w) M = fmaxf(M, s_m[w * kMaxGqa + qq]);
@@ -515,15 +541,42 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
             float M = -INFINITY, acc = 0.f, lsum = 0.f;
             for (int sp0 = r; valid && sp0 < L.nsplit; sp0 += 4 * G) {
                 float mv[4], lv[4], ov[4];
+                if (mbox) {
+                    // all slots' loads in flight together; re-poll only the late ones
+                    unsigned long long* pb[4];
+                    unsigned long long a[4], b[4];
 #pragma unroll
-                for (int x = 0; x < 4; ++x) {
-                    const int sp = sp0 + x * G;
-                    const float* ps = pq + static_cast<int64_t>(sp) * stride_p;
-                    // weak loads: ordered after the producers' release by the acquire
-                    // (and its L1 invalidation) plus the CTA barrier
-                    mv[x] = sp < L.nsplit ? ps[kHeadDim] : -INFINITY;
-                    lv[x] = sp < L.nsplit ? ps[kHeadDim + 1] : 0.f;
-                    ov[x] = sp < L.nsplit ? ps[c] : 0.f;
+                    for (int x = 0; x < 4; ++x) {
+                        const int sp = sp0 + x * G;
+                        pb[x] = mbox + ((static_cast<int64_t>(u) * L.nsplit + sp) * gqa * kHeadDim + idx) * 2;
+                        a[x] = sp < L.nsplit ? ld_relaxed_gpu_b64(pb[x]) : 0ull;
+                        b[x] = sp < L.nsplit ? ld_relaxed_gpu_b64(pb[x] + 1) : 0ull;
+                    }
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const bool live = sp0 + x * G < L.nsplit;
+                        while (live && (static_cast<uint32_t>(a[x]) == 0u || (b[x] >> 32) == 0u)) {
+                            __nanosleep(32);
+                            a[x] = ld_relaxed_gpu_b64(pb[x]);
+                            b[x] = ld_relaxed_gpu_b64(pb[x] + 1);
+                        }
+                        mv[x] = live ? __uint_as_float(static_cast<uint32_t>(a[x] >> 32)) : -INFINITY;
+                        ov[x] = live ? __uint_as_float(~static_cast<uint32_t>(a[x])) : 0.f;
+                        lv[x] = live ? __uint_as_float(static_cast<uint32_t>(b[x])) : 0.f;
+                        // this lane is the slot's only reader: leave it empty for the next launch
+                        if (live) *reinterpret_cast<ulonglong2*>(pb[x]) = make_ulonglong2(0ull, 0ull);
+                    }
+                } else {
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const int sp = sp0 + x * G;
+                        const float* ps = pq + static_cast<int64_t>(sp) * stride_p;
+                        // weak loads: ordered after the producers' release by the acquire
+                        // (and its L1 invalidation) plus the CTA barrier
+                        mv[x] = sp < L.nsplit ? ps[kHeadDim] : -INFINITY;
+                        lv[x] = sp < L.nsplit ? ps[kHeadDim + 1] : 0.f;
+                        ov[x] = sp < L.nsplit ? ps[c] : 0.f;
+                    }
                 }
                 const float Mc = fmaxf(fmaxf(M, fmaxf(mv[0], mv[1])), fmaxf(mv[2], mv[3]));
                 if (Mc == -INFINITY) continue;  // every split so far empty
@@ -564,6 +617,21 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
             }
         }
     };
+    if (mbox) {
+        // Every warp of the CTA finished claiming before the merge barrier; the
+        // unit's last CTA past this point re-arms the claim counter.
+        int* done = &L.counters[L.n_units + u];
+        if (threadIdx.x == nthr - 1 && atomicAdd(done, 1) == L.nsplit - 1) {
+            *done = 0;
+            if (dyn) *ctr = 0;
+        }
+        if (ct && threadIdx.x == 0) ct[5] = globaltimer();
+        const int n = gqa * kHeadDim;
+        combine_slice(static_cast<int>(static_cast<int64_t>(n) * split / L.nsplit),
+                      static_cast<int>(static_cast<int64_t>(n) * (split + 1) / L.nsplit));
+        if (ct && threadIdx.x == 0) ct[10] = ct[4] = globaltimer();
+        return;
+    }
     // Publication: the CTA barrier orders every thread's partial stores before
     // thread 0's release atomic on the unit's counter (no device-wide SC fence
     // in all 256 threads, ~0.5 us here); readers acquire the counter.

@@ -105,6 +105,9 @@ struct DecodeLaunch {
     float* out;              // fused combine target or nullptr (split partials only)
     int out_mode;            // 0: normalised [u][gqa][d]; 1: merged partial [u][gqa][d+2]
     int* counters;           // [2u] arrival / done counters for the fused combine
+    // coop combine mailbox: [u][nsplit][gqa][d] x {~bits(O) | bits(m) << 32, bits(l) | 1 << 32};
+    // zero = empty (each reader clears what it read, so launches leave it zeroed)
+    unsigned long long* mailbox;
     int coop_combine;        // every CTA resident: all CTAs of a unit merge in parallel
     int dynamic;             // warps claim the unit's blocks from blk_ctr (no static ranges)
     int* blk_ctr;            // [u] block claim counters (dynamic mode; reset by the combine)

@@ -200,6 +200,32 @@ def test_decode_plans_own_their_workspaces(hs, port):
             assert (p.out - w).abs().max().item() < 1e-5
 
 
+def test_decode_mailbox_after_other_modes(hs, port, monkeypatch):
+    """The cooperative combine's tagged mailbox must read empty before every launch:
+    plain split partials of a larger, non-cooperative decode on the same stream
+    (and a plan's row chunks of different widths in one workspace) never land on
+    it, so later cooperative decodes and plan replays stay exact."""
+    import torch
+    kx, vx, kcb, vcb = build_caches(hs, port, 8, 65536, 1.0, "bf16", seed=41)
+    qb = to_torch(decode_queries(port, 8, 8, "bf16", seed=41), "bf16")
+    U, L = 4, 8192
+    kx, vx, kc, vc = build_caches(hs, port, U, L, 0.5, "bf16", seed=42)
+    q = to_torch(decode_queries(port, U, 4, "bf16", seed=42), "bf16")
+    want = hs.decode_attention(q, kc, vc, splits=7).clone()
+    monkeypatch.setenv("HS_DECODE_COOP", "0")
+    hs.decode_attention(qb, kcb, vcb)  # plain partials over the whole decode workspace
+    monkeypatch.delenv("HS_DECODE_COOP")
+    for _ in range(3):
+        assert (hs.decode_attention(q, kc, vc) - want).abs().max().item() < 1e-5
+    q12 = to_torch(decode_queries(port, U, 12, "bf16", seed=43), "bf16")
+    want12 = hs.decode_attention(q12, kc, vc).clone()
+    plan = hs.DecodePlan(q12, kc, vc)
+    for _ in range(3):
+        plan()
+        torch.cuda.synchronize()
+        assert (plan.out - want12).abs().max().item() < 1e-5
+
+
 def test_decode_plan_host_io(hs, port):
     """DecodePlan(host_io=True): one graph replay copies the pinned host queries in,
     decodes and copies the output to pinned host memory; fresh queries written to
