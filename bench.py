@@ -533,11 +533,17 @@ def leg_compress(hs, dev, rank, world, args, flush):
         outp = hs.prune_cache(key, val, cfg)
         ms = max_over_ranks(min(time_steps(lambda: hs.prune_cache(key, val, cfg, out=outp), args.steps, 3, flush)),
                             world)
-        nbytes = 2 * key.numel() * 2 + outp[0].nbytes() + outp[1].nbytes() + 2 * U * outp[0].logical_blocks * (8 + 1 + 4)
+        # + per block: flag, slot_block entry and (when ranked) the FP64 loss
+        nbytes = 2 * key.numel() * 2 + outp[0].nbytes() + outp[1].nbytes() + \
+            2 * U * outp[0].logical_blocks * ((1 + 4) if s == 1.0 else (8 + 1 + 4))
         res[f"prune_cache_s{s:g}"] = {"ms": round(ms, 4), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
                                       "frac_of_hbm": round(nbytes / (ms * 1e-3) / 1e9 / hbm, 4), "bytes": int(nbytes),
                                       "selection": "static" if s == 1.0 else "loss-driven (classify, radix select, pack)",
-                                      "call": "hierasparse.prune_cache (value cache on a side stream)"}
+                                      **({"note": "frac_of_hbm above 1: ~40 MB of each cache's output is still dirty in L2 when "
+                                                  "its kernel ends and reaches DRAM during the next L2 flush (ncu: DRAM writes "
+                                                  "110-116 of 151 MB per cache, profiles/r02j_compress_dram.md); the peak is a "
+                                                  "50/50 read/write copy figure, this pass is 64% reads"} if s == 1.0 else {}),
+                                      "call": "hierasparse.prune_cache (value cache on a side stream; block losses only where the selection ranks them, as the reference's HierarchicalMask carries none)"}
     kp, vp = hs.prune_cache(key, val, hs.SparsityConfig(0.5, 0.5, 64))
     dec = hs.SparsityConfig(1.0, 1.0, 64)
     k2, v2 = hs.recompress(kp, dec, 1.0), hs.recompress(vp, dec, 1.0)
@@ -547,7 +553,7 @@ def leg_compress(hs, dev, rank, world, args, flush):
         hs.recompress_pair(kp, vp, dec, check=False, status=st)
     ms = max_over_ranks(min(time_steps(rc, args.steps, 3, flush)), world)
     st.check()
-    nbytes = kp.nbytes() + vp.nbytes() + k2.nbytes() + v2.nbytes() + 2 * U * k2.logical_blocks * (8 + 1 + 4)
+    nbytes = kp.nbytes() + vp.nbytes() + k2.nbytes() + v2.nbytes() + 2 * U * k2.logical_blocks * (1 + 4)  # static: no losses
     res["recompress_s0.5_to_1"] = {"ms": round(ms, 4), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
                                    "frac_of_hbm": round(nbytes / (ms * 1e-3) / 1e9 / hbm, 4), "bytes": int(nbytes),
                                    "call": "hierasparse.recompress_pair (hs_recompress per cache, one pass, no host sync)"}

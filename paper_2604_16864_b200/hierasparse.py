@@ -94,7 +94,9 @@ class DeviceCompressedCache:
         self.meta_pool = torch.empty((U, sparse_count, be // 16), dtype=torch.int16, device=dev)
         self.slot_block = torch.empty((U, logical_blocks), dtype=torch.int32, device=dev)
         self.flags = torch.empty((U, logical_blocks), dtype=torch.uint8, device=dev)
-        self.losses = torch.empty((U, logical_blocks), dtype=torch.float64, device=dev)
+        # block losses of the last selection that computed them (NaN: not computed --
+        # a static selection needs none unless asked for, with_losses=True)
+        self.losses = torch.full((U, logical_blocks), float("nan"), dtype=torch.float64, device=dev)
 
     @property
     def sequence_length(self) -> int:
@@ -168,13 +170,21 @@ def _unit_stride(x: torch.Tensor) -> int:
     return x.stride(0) if x.shape[0] > 1 else x.shape[1] * x.shape[2]
 
 
+def _static_selection(nb: int, sc: int, prefix: int, suffix: int) -> bool:
+    """select_blocks' quota is 0 or every prunable block (pruner.hpp:106-116): the
+    block mask follows from the protected regions alone, no loss is consulted."""
+    return sc == 0 or sc == nb - prefix - suffix
+
+
 def prune_compress(x: torch.Tensor, cfg: SparsityConfig, sparsity: float, axis: int,
-                   out: DeviceCompressedCache | None = None) -> DeviceCompressedCache:
+                   out: DeviceCompressedCache | None = None, with_losses: bool = True) -> DeviceCompressedCache:
     """hierarchical_mask_for (pruner.hpp:121-158) + fused_magnitude_compress
-    (compressed_cache.hpp:232-267) for one cache kind of every unit."""
+    (compressed_cache.hpp:232-267) for one cache kind of every unit.  The block
+    losses (pruner.hpp:81-89) land in out.losses; with_losses=False skips them when
+    the selection does not need them (quota 0 or all prunable blocks)."""
     x = _check_src(x)
     U, rows, d = x.shape
-    nb, dc, sc, _, _ = pool_counts(rows, cfg, sparsity)
+    nb, dc, sc, pre, suf = pool_counts(rows, cfg, sparsity)
     if out is None:
         out = DeviceCompressedCache(x.dtype, axis, U, nb, dc, sc, x.device, d, cfg.block_size, cfg)
     elif (out.n_units, out.logical_blocks, out.dense_count, out.sparse_count, out.dtype, out.axis, out.head_dim) != \
@@ -182,23 +192,26 @@ def prune_compress(x: torch.Tensor, cfg: SparsityConfig, sparsity: float, axis: 
         raise ConfigError("prune_cache: the output cache's geometry does not match")
     lib = capi.load()
     cc = cfg.c()
+    lp = out.losses.data_ptr() if with_losses or not _static_selection(nb, sc, pre, suf) else None
     capi.check(lib.hs_prune_compress(x.data_ptr(), _unit_stride(x), rows, C.byref(cc), sparsity, out.cref(),
-                                     out.losses.data_ptr(), out.flags.data_ptr(), _stream()))
+                                     lp, out.flags.data_ptr(), _stream()))
     return out
 
 
-def prune_cache(key: torch.Tensor, value: torch.Tensor, cfg: SparsityConfig, out=None):
+def prune_cache(key: torch.Tensor, value: torch.Tensor, cfg: SparsityConfig, out=None, with_losses: bool = False):
     """prune_cache (pruner.hpp:165-176) followed by compression of both caches:
     key along channels at S_K, value along the sequence at S_V.  out: an earlier
-    (key, value) result of the same geometry to overwrite (no allocation)."""
+    (key, value) result of the same geometry to overwrite (no allocation).  Like
+    the reference's HierarchicalMask (block + element masks, no losses), block
+    losses are computed only when the selection ranks them, unless with_losses."""
     if key.shape[-2] != value.shape[-2]:
         raise ConfigError("prune_cache: key/value sequence lengths differ")
     if key.shape[-1] % 4:
         raise ConfigError("prune_cache: head dimension not divisible by m_group")
     ko, vo = out if out is not None else (None, None)
     if not (key.is_cuda and value.is_cuda):
-        return (prune_compress(key, cfg, cfg.s_key, capi.AXIS_CHANNEL, ko),
-                prune_compress(value, cfg, cfg.s_value, capi.AXIS_SEQUENCE, vo))
+        return (prune_compress(key, cfg, cfg.s_key, capi.AXIS_CHANNEL, ko, with_losses),
+                prune_compress(value, cfg, cfg.s_value, capi.AXIS_SEQUENCE, vo, with_losses))
     # The two caches are independent: the value cache runs on a side stream (forked
     # from and joined back into the caller's stream), so one cache's selection
     # kernels -- a CTA per unit -- overlap the other cache's block kernels.  Both
@@ -208,9 +221,9 @@ def prune_cache(key: torch.Tensor, value: torch.Tensor, cfg: SparsityConfig, out
     main = torch.cuda.current_stream(key.device)
     side = _side_stream(key.device)
     side.wait_stream(main)
-    kc = prune_compress(key, cfg, cfg.s_key, capi.AXIS_CHANNEL, ko)
+    kc = prune_compress(key, cfg, cfg.s_key, capi.AXIS_CHANNEL, ko, with_losses)
     with torch.cuda.stream(side):
-        vc = prune_compress(value, cfg, cfg.s_value, capi.AXIS_SEQUENCE, vo)
+        vc = prune_compress(value, cfg, cfg.s_value, capi.AXIS_SEQUENCE, vo, with_losses)
     main.wait_stream(side)
     return kc, vc
 
@@ -340,7 +353,7 @@ def decompress(c: DeviceCompressedCache, check: bool = True, status: StatusWord 
 
 
 def recompress(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: float, check: bool = True,
-               status: StatusWord | None = None) -> DeviceCompressedCache:
+               status: StatusWord | None = None, with_losses: bool = False) -> DeviceCompressedCache:
     """The decode-phase re-prune (pipeline.hpp:227-240): decompress
     (compressed_cache.hpp:271-298) -> hierarchical_mask_for at the decode sparsity
     (pruner.hpp:121-158) -> fused_magnitude_compress, for every unit on the
@@ -348,8 +361,9 @@ def recompress(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: float, c
     on the fly, the dense cache is never materialised).  Bit-identical to the
     reference's chain on the same pools.  A corrupt input cache raises
     decompress's DataError (check=False defers it to out.status.check(), so the
-    call stays free of host synchronisation, e.g. inside a CUDA graph)."""
-    return _recompress_into(c, cfg, sparsity, _recompress_out(c, cfg, sparsity), check, status)
+    call stays free of host synchronisation, e.g. inside a CUDA graph).  Block
+    losses only when the selection ranks them, unless with_losses (as prune_cache)."""
+    return _recompress_into(c, cfg, sparsity, _recompress_out(c, cfg, sparsity), check, status, with_losses)
 
 
 def _recompress_out(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: float) -> DeviceCompressedCache:
@@ -358,10 +372,12 @@ def _recompress_out(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: flo
                                  cfg.block_size, cfg)
 
 
-def _recompress_into(c, cfg, sparsity, out, check, status):
+def _recompress_into(c, cfg, sparsity, out, check, status, with_losses=False):
     cc = cfg.c()
     st = _status(status, out.index_map.device)
-    capi.check(capi.load().hs_recompress(c.cref(), C.byref(cc), sparsity, out.cref(), out.losses.data_ptr(),
+    nb, _, sc, pre, suf = pool_counts(c.logical_blocks * c.block_size, cfg, sparsity)
+    lp = out.losses.data_ptr() if with_losses or not _static_selection(nb, sc, pre, suf) else None
+    capi.check(capi.load().hs_recompress(c.cref(), C.byref(cc), sparsity, out.cref(), lp,
                                          out.flags.data_ptr(), st.ptr(), _stream()))
     out.status = st
     if check:
@@ -419,7 +435,7 @@ def recompress_unfused(c: DeviceCompressedCache, cfg: SparsityConfig, sparsity: 
 
 
 def recompress_pair(k: DeviceCompressedCache, v: DeviceCompressedCache, cfg: SparsityConfig, check: bool = True,
-                    status: StatusWord | None = None):
+                    status: StatusWord | None = None, with_losses: bool = False):
     """prune_cache at the decode sparsity (cfg.s_key / cfg.s_value) of already
     compressed caches (pipeline.hpp:228-240, "further pruned").  The
     value cache runs on a side stream forked from and joined into the caller's
@@ -429,9 +445,9 @@ def recompress_pair(k: DeviceCompressedCache, v: DeviceCompressedCache, cfg: Spa
     main = torch.cuda.current_stream(k.index_map.device)
     side = _side_stream(k.index_map.device)
     side.wait_stream(main)
-    k2 = recompress(k, cfg, cfg.s_key, check=False, status=st)
+    k2 = recompress(k, cfg, cfg.s_key, check=False, status=st, with_losses=with_losses)
     with torch.cuda.stream(side):
-        v2 = _recompress_into(v, cfg, cfg.s_value, vo, False, st)
+        v2 = _recompress_into(v, cfg, cfg.s_value, vo, False, st, with_losses)
     main.wait_stream(side)
     if check:
         st.check()

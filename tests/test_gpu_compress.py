@@ -327,7 +327,7 @@ def test_decode_phase_recompress_matches_oracle(hs, port, dtype, s_pre, s_dec):
     vx = gen_units(port, U, L, 128, 21, 1, dtype)
     kc, vc = hs.prune_cache(to_torch(kx, dtype), to_torch(vx, dtype), hs.SparsityConfig(s_pre, s_pre, 64))
     cfg_dec = hs.SparsityConfig(s_dec, s_dec, 64)
-    k2, v2 = hs.recompress_pair(kc, vc, cfg_dec)
+    k2, v2 = hs.recompress_pair(kc, vc, cfg_dec, with_losses=True)
     for dev_old, dev_new, axis in ((kc, k2, 0), (vc, v2, 1)):
         for u in range(U):
             dense = port.decompress(device_to_oracle(dev_old, u))
@@ -378,7 +378,7 @@ def test_recompress_with_kept_zeros(hs, port, s_pre, s_dec):
     kc, vc = hs.prune_cache(to_torch(kx, "bf16"), to_torch(vx, "bf16"), pre)
     dec = hs.SparsityConfig(s_dec, s_dec, 64)
     for c in (kc, vc):
-        got = hs.recompress(c, dec, s_dec)
+        got = hs.recompress(c, dec, s_dec, with_losses=True)
         for u in range(U):
             want = port.prune_compress(port.decompress(device_to_oracle(c, u)), OCfg(s_dec, s_dec, 64), c.axis, s_dec)
             g = device_to_oracle(got, u)
@@ -521,3 +521,27 @@ def test_pair_entry_points_match_single_cache_calls(hs, port):
     for a, b in ((kc, k1), (vc, v1), (k2, k3), (v2, v3)):
         for u in range(U):
             assert_cache_equal(a, u, device_to_oracle(b, u))
+
+
+@pytest.mark.parametrize("s", [1.0, 0.0])
+def test_static_selection_skips_losses(hs, port, s):
+    """A static selection (quota 0 or every prunable block) needs no block loss:
+    prune_cache / recompress leave losses as NaN unless with_losses, and every
+    pool, index entry and flag is identical either way."""
+    import torch
+    U, L = 2, 2048
+    kx = to_torch(gen_units(port, U, L, 128, 61, 0, "bf16"), "bf16")
+    vx = to_torch(gen_units(port, U, L, 128, 61, 1, "bf16"), "bf16")
+    cfg = hs.SparsityConfig(s, s, 64, sink_tokens=64, local_window=128)
+    fast = hs.prune_cache(kx, vx, cfg)
+    full = hs.prune_cache(kx, vx, cfg, with_losses=True)
+    for a, b in zip(fast, full):
+        assert torch.isnan(a.losses).all() and not torch.isnan(b.losses).any()
+        for name in ("index_map", "dense_pool", "nnz_pool", "meta_pool", "flags", "slot_block"):
+            x, y = getattr(a, name), getattr(b, name)
+            if x.is_floating_point():
+                x, y = x.view(torch.int16), y.view(torch.int16)
+            assert torch.equal(x, y), name
+    r_fast, r_full = hs.recompress(full[0], cfg, s), hs.recompress(full[0], cfg, s, with_losses=True)
+    assert torch.isnan(r_fast.losses).all() and not torch.isnan(r_full.losses).any()
+    assert torch.equal(r_fast.nnz_pool.view(torch.int16), r_full.nnz_pool.view(torch.int16))

@@ -38,7 +38,7 @@ def caches(hs, g, name):
     key = f32(g[name + "_key"]).reshape(L + tail, d)
     val = f32(g[name + "_val"]).reshape(L + tail, d)
     cfg = hs.SparsityConfig(s, s, B, sink, window)
-    kc, vc = hs.prune_cache(to_torch(key[None, :L], "bf16"), to_torch(val[None, :L], "bf16"), cfg)
+    kc, vc = hs.prune_cache(to_torch(key[None, :L], "bf16"), to_torch(val[None, :L], "bf16"), cfg, with_losses=True)
     return key, val, kc, vc, (L, tail, d, B, gqa, n_q)
 
 
@@ -70,7 +70,7 @@ def test_decompress_and_recompress_general_shapes(hs, gold, port, name):
         assert (dec == want).all()
         # decode-phase re-prune to S = 1 (pipeline.hpp:227-240), fused, vs the oracle chain
         cfg = hs.SparsityConfig(1.0, 1.0, B)
-        r = hs.recompress(c, cfg, 1.0)
+        r = hs.recompress(c, cfg, 1.0, with_losses=True)
         w = port.prune_compress(want, OCfg(1.0, 1.0, B), c.axis, 1.0)
         got = device_to_oracle(r, 0)
         assert (got.index_map == w.index_map).all() and (got.nnz_pool == w.nnz_pool).all()
