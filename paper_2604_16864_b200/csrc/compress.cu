@@ -110,6 +110,37 @@ __device__ __forceinline__ void loss_add_pair(LossAcc& a, uint32_t lo, uint32_t 
              static_cast<double>(F16Traits<T>::to_float(static_cast<uint16_t>(hi)));
 }
 
+// Classify pass (losses only): the pruned pairs of two 2:4 groups at once in
+// 16-bit SIMD lanes (lane k = group k).  Each group is (glo.lo, glo.hi, ghi.lo,
+// ghi.hi); its pruned values are its two smallest magnitudes.  Positions do not
+// matter for the loss -- tied magnitudes are the same value -- so the keys carry
+// no index bits and one min/max network serves both groups (16 ALU ops for two
+// groups instead of ~50 for select2of4 twice).
+template <typename T>
+__device__ __forceinline__ void loss_add_groups2(LossAcc& a, uint32_t& mm, uint32_t g0lo, uint32_t g0hi,
+                                                 uint32_t g1lo, uint32_t g1hi) {
+    constexpr uint32_t kMag = 0x7FFF7FFFu;
+    const uint32_t P = __byte_perm(g0lo, g1lo, 0x5410u) & kMag, Q = __byte_perm(g0lo, g1lo, 0x7632u) & kMag;
+    const uint32_t R = __byte_perm(g0hi, g1hi, 0x5410u) & kMag, S = __byte_perm(g0hi, g1hi, 0x7632u) & kMag;
+    const uint32_t x = __vmaxu2(P, Q), y = __vminu2(P, Q), z = __vmaxu2(R, S), w = __vminu2(R, S);
+    const uint32_t s1 = __vminu2(y, w);                            // smallest (per lane)
+    const uint32_t s2 = __vminu2(__vmaxu2(y, w), __vminu2(x, z));  // second smallest
+    // smallest nonzero pruned magnitude, kept as (m - 1) per lane (0 wraps to 0xFFFF)
+    mm = __vminu2(mm, __vminu2(__vsub2(s1, 0x00010001u), __vsub2(s2, 0x00010001u)));
+#ifdef HS_XP_NO_LOSS
+    if (s1 != 0x12345u) return;  // timing experiment only
+#endif
+    a.sum += (static_cast<double>(F16Traits<T>::to_float(static_cast<uint16_t>(s1))) +
+              static_cast<double>(F16Traits<T>::to_float(static_cast<uint16_t>(s2)))) +
+             (static_cast<double>(F16Traits<T>::to_float(static_cast<uint16_t>(s1 >> 16))) +
+              static_cast<double>(F16Traits<T>::to_float(static_cast<uint16_t>(s2 >> 16))));
+}
+// Fold the packed (m - 1) minimum into LossAcc::min_mag (0xFFFF = none).
+__device__ __forceinline__ void loss_fold_min(LossAcc& a, uint32_t mm) {
+    const uint32_t m = min(mm & 0xFFFFu, mm >> 16) + 1u;  // 0x10000: no nonzero term
+    a.min_mag = min(a.min_mag, m);
+}
+
 // Reduce LossAcc across the CTA; thread 0 gets the total.  Returns true on
 // thread 0 when the parallel sum is provably the reference's sequential one:
 // every term is an integer multiple of u = 2^unit_exp(min nonzero magnitude),
@@ -330,6 +361,7 @@ __global__ void __launch_bounds__(kThreads, HS_COMPRESS_MINB) block_kernel(PackA
     if (SRC == 0) mbar_wait(&s_bar, 0);
     constexpr bool kLoss = MODE != 1;
     LossAcc acc;
+    uint32_t mm = 0xFFFFFFFFu;  // MODE 0: packed (min nonzero pruned magnitude - 1)
 
     if (SRC == 1 && in_e < 0 && (MODE == 0 || !dense)) {
         // A stored 2:4 block re-pruned (decode-phase re-prune): expanded, every
@@ -414,6 +446,10 @@ __global__ void __launch_bounds__(kThreads, HS_COMPRESS_MINB) block_kernel(PackA
                 *reinterpret_cast<uint4*>(dst + r * kHeadDim + c * 8) = v;
             }
             if (MODE == 1 && dense) continue;
+            if (MODE == 0) {
+                loss_add_groups2<T>(acc, mm, v.x, v.y, v.z, v.w);
+                continue;
+            }
             const Sel2of4 s0 = select2of4(v.x, v.y), s1 = select2of4(v.z, v.w);
             const uint32_t meta_byte = s0.code | (s1.code << 4);
             if (kLoss) {
@@ -486,7 +522,16 @@ __global__ void __launch_bounds__(kThreads, HS_COMPRESS_MINB) block_kernel(PackA
                 reinterpret_cast<uint4*>(dst)[q] = make_uint4(w[0], w[1], w[2], w[3]);
             }
         }
-        if (!(MODE == 1 && dense)) {
+        if (MODE == 0) {
+#pragma unroll
+            for (int gi = 0; gi < 8; gi += 2) {
+                const int r0 = 32 * h + 4 * gi;
+                auto word = [&](int r) {
+                    return tile[r * kHeadDim + c] | (static_cast<uint32_t>(tile[(r + 1) * kHeadDim + c]) << 16);
+                };
+                loss_add_groups2<T>(acc, mm, word(r0), word(r0 + 2), word(r0 + 4), word(r0 + 6));
+            }
+        } else if (!(MODE == 1 && dense)) {
             uint32_t vals[8];
             uint32_t meta = 0;
 #pragma unroll
@@ -512,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, HS_COMPRESS_MINB) block_kernel(PackA
 
     if (SRC == 1 && in_bad) record_status(a.status, static_cast<uint64_t>(u) * a.nb + b, kReasonCodesOrder);
     if (kLoss) {
+        if (MODE == 0) loss_fold_min(acc, mm);
         const bool exact = loss_reduce<T>(acc, s_sum, s_min, nullptr);
         if (t == 0) {
             double loss = acc.sum;
