@@ -55,8 +55,11 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     __shared__ uint32_t s_q[kMaxGqa * kHeadDim / 2];  // the unit's query rows (16-bit pairs)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int split = blockIdx.x, u = blockIdx.y;
-    long long* const ct = L.cta_times ? L.cta_times + 16 * (static_cast<int64_t>(u) * gridDim.x + split) : nullptr;
+    // interleave: a 1-D grid whose consecutive CTAs belong to different units, so
+    // every unit's splits spread over all GPCs instead of filling one or two
+    const int split = L.interleave ? static_cast<int>(blockIdx.x) / L.n_units : static_cast<int>(blockIdx.x);
+    const int u = L.interleave ? static_cast<int>(blockIdx.x) % L.n_units : static_cast<int>(blockIdx.y);
+    long long* const ct = L.cta_times ? L.cta_times + 16 * (static_cast<int64_t>(u) * L.nsplit + split) : nullptr;
     if (ct && threadIdx.x == 0) ct[0] = globaltimer();
     const int gqa = L.gqa;
     // Block range of this CTA (attention.hpp:380-381 partition of [begin, end)).
@@ -742,7 +745,7 @@ cudaError_t launch_t(const DecodeLaunch& L, int spw, StageLayout lay, size_t sme
     cudaError_t err = configure_t<T, NW, HILO>(smem);
     if (err) return err;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(L.nsplit, L.n_units);
+    cfg.gridDim = L.interleave ? dim3(L.nsplit * L.n_units) : dim3(L.nsplit, L.n_units);
     cfg.blockDim = dim3(32 * NW);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;

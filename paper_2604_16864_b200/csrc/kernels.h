@@ -110,6 +110,7 @@ struct DecodeLaunch {
     unsigned long long* mailbox;
     int coop_combine;        // every CTA resident: all CTAs of a unit merge in parallel
     int dynamic;             // warps claim the unit's blocks from blk_ctr (no static ranges)
+    int interleave;          // 1-D grid, CTA i = (unit i % n_units, split i / n_units)
     int* blk_ctr;            // [u] block claim counters (dynamic mode; reset by the combine)
     long long* cta_times;    // tools only: [grid][5] globaltimer at start / first data / loop end / partial written / combine done
     CUtensorMap tm_knnz, tm_kden, tm_vnnz, tm_vden;

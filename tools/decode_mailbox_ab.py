@@ -1,8 +1,9 @@
-"""A/B of the coop combine's hand-off (HS_DECODE_MAILBOX=0: counter release/acquire
-then plain partial loads; 1: tagged mailbox) on the bench headline: two DecodePlans
-captured under each setting, replayed alternately after an L2 flush with the stream
-held while the host enqueues (bench protocol).  Outputs must agree to fp32 rounding.
-    python tools/decode_mailbox_ab.py [reps]"""
+"""A/B of a decode run-time switch on the bench headline (default HS_DECODE_MAILBOX:
+0 = counter release/acquire then plain partial loads, 1 = tagged mailbox): two
+DecodePlans captured under each setting, replayed alternately after an L2 flush with
+the stream held while the host enqueues (bench protocol).  Outputs must agree to
+fp32 rounding.
+    python tools/decode_mailbox_ab.py [reps] [VAR]"""
 import os
 import statistics
 import sys
@@ -14,19 +15,20 @@ import bench
 from paper_2604_16864_b200 import hierasparse as hs
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+VAR = sys.argv[2] if len(sys.argv) > 2 else "HS_DECODE_MAILBOX"
 dev = torch.device("cuda", 0)
 scale = 1.0 / 128 ** 0.5
 kc, vc, q, step_bytes = bench.build_headline(hs, dev, 0, scale)
 flush = bench.Flusher(dev)
 plans = {}
 for var in ("0", "1"):
-    os.environ["HS_DECODE_MAILBOX"] = var
+    os.environ[VAR] = var
     plans[var] = hs.DecodePlan(q, kc, vc, scale=scale)
     for _ in range(5):
         plans[var]()
 torch.cuda.synchronize()
 d = (plans["0"].out - plans["1"].out).abs().max().item()
-print(f"max |mailbox - counters| = {d:.3e}")
+print(f"max |{VAR}=1 - {VAR}=0| = {d:.3e}")
 ref = hs.decode_attention(q, kc, vc, scale=scale, splits=18)  # static, deterministic
 
 
@@ -49,5 +51,5 @@ for rep in range(reps):
     for var in ("0", "1"):
         m, md = run(plans[var])
         err = (plans[var].out - ref).abs().max().item()
-        print(f"mailbox={var}: mean {m:.2f} median {md:.2f} us ({step_bytes / (md * 1e-6) / 1e9:.0f} GB/s) "
+        print(f"{VAR}={var}: mean {m:.2f} median {md:.2f} us ({step_bytes / (md * 1e-6) / 1e9:.0f} GB/s) "
               f"max |out - static| {err:.2e}", flush=True)
