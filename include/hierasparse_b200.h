@@ -142,7 +142,11 @@ HS_API hs_status hs_cache_bytes(const hs_device_cache* c, uint64_t* index_bytes,
  *        src_unit_stride elements.
  *   out: geometry fields + pointers filled by the caller (use hs_pool_counts).
  *   losses (double [n_units][nb]) and flags (u8 [n_units][nb], 1 = dense) are
- *   optional device outputs (BlockMask, masks.hpp:55-68).
+ *   optional device outputs (BlockMask, masks.hpp:55-68).  With losses == NULL
+ *   a static selection (quota 0 or every prunable block) computes no block loss
+ *   at all -- the mask follows from the protected regions -- which makes the
+ *   pass HBM-bound (~30% faster); a loss-driven selection ranks them in a
+ *   workspace either way.
  * Pool contents, index map, flags and losses are bit-identical to the reference
  * on the same (16-bit representable) inputs. */
 HS_API hs_status hs_prune_compress(const void* src, uint64_t src_unit_stride, uint64_t rows,
