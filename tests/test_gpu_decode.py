@@ -274,3 +274,23 @@ def test_decode_tail_only_view(hs, port, tail):
     want = np.stack([port.dense_attention(q[u], kx[u], vx[u], False, scale) for u in range(U)])
     mx, mr = err_stats(got, want)
     assert mx < MAX_ABS_TOL and mr < MEAN_REL_TOL, (mx, mr)
+
+
+@pytest.mark.parametrize("env", [{"HS_DECODE_INTERLEAVE": "0"}, {"HS_DECODE_MAILBOX": "0"},
+                                 {"HS_DECODE_COOP": "0"}, {"HS_DECODE_DYNAMIC": "0"}])
+def test_decode_launch_variants_agree(hs, port, monkeypatch, env):
+    """The legacy / fallback launch shapes kept behind switches -- the 2-D (split,
+    unit) grid, the counter hand-off instead of the tagged mailbox, the last-CTA
+    ticket combine, static split ranges -- give the default path's result."""
+    U, L = 8, 16384
+    kx, vx, kc, vc = build_caches(hs, port, U, L, 0.5, "bf16", seed=51)
+    q = to_torch(decode_queries(port, U, 4, "bf16", seed=51), "bf16")
+    want = hs.decode_attention(q, kc, vc).clone()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for _ in range(2):
+        got = hs.decode_attention(q, kc, vc)
+        assert (got - want).abs().max().item() < 1e-5
+    for k in env:
+        monkeypatch.delenv(k)
+    assert (hs.decode_attention(q, kc, vc) - want).abs().max().item() < 1e-5
