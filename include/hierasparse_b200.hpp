@@ -203,16 +203,27 @@ inline PoolCounts pool_counts(std::size_t rows, const SparsityConfig& cfg, doubl
 }
 
 // hierarchical_mask_for + fused_magnitude_compress for one cache kind of every
-// unit: src = device [n_units][rows][head_dim] 16-bit, token-major.
+// unit: src = device [n_units][rows][head_dim] 16-bit, token-major.  The block
+// losses land in out.losses() when the selection ranks them or with_losses;
+// a static selection (quota 0 or every prunable block) otherwise skips them
+// (the reference's HierarchicalMask carries none) and leaves NaN.
 inline DeviceCompressedCache compress_one(const void* src, DType dtype, uint32_t n_units, std::size_t rows,
                                           const SparsityConfig& cfg, double sparsity, GroupAxis axis,
-                                          cudaStream_t stream = nullptr, uint32_t head_dim = 128) {
+                                          cudaStream_t stream = nullptr, uint32_t head_dim = 128,
+                                          bool with_losses = false) {
     const PoolCounts p = pool_counts(rows, cfg, sparsity);
     DeviceCompressedCache out(dtype, axis, n_units, p.logical_blocks, p.dense_count, p.sparse_count, head_dim,
                               static_cast<uint32_t>(cfg.block_size));
     const hs_sparsity_config c = cfg.c();
-    check(hs_prune_compress(src, rows * head_dim, rows, &c, sparsity, &out.desc(), out.losses(), out.flags(),
-                            stream));
+    const bool static_sel =
+        p.sparse_count == 0 || p.sparse_count == p.logical_blocks - p.prefix_blocks - p.suffix_blocks;
+    double* losses = out.losses();
+    if (static_sel && !with_losses) {
+        check_cuda(cudaMemsetAsync(losses, 0xFF, sizeof(double) * n_units * p.logical_blocks, stream),
+                   "cudaMemsetAsync");  // all-ones doubles: NaN, "not computed"
+        losses = nullptr;
+    }
+    check(hs_prune_compress(src, rows * head_dim, rows, &c, sparsity, &out.desc(), losses, out.flags(), stream));
     return out;
 }
 
