@@ -60,7 +60,12 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     const int split = L.interleave ? static_cast<int>(blockIdx.x) / L.n_units : static_cast<int>(blockIdx.x);
     const int u = L.interleave ? static_cast<int>(blockIdx.x) % L.n_units : static_cast<int>(blockIdx.y);
     long long* const ct = L.cta_times ? L.cta_times + 16 * (static_cast<int64_t>(u) * L.nsplit + split) : nullptr;
-    if (ct && threadIdx.x == 0) ct[0] = globaltimer();
+    if (ct && threadIdx.x == 0) {
+        ct[0] = globaltimer();
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        ct[15] = smid;
+    }
     const int gqa = L.gqa;
     // Block range of this CTA (attention.hpp:380-381 partition of [begin, end)).
     const int span = L.block_end - L.block_begin;
@@ -559,7 +564,6 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
                     for (int x = 0; x < 4; ++x) {
                         const bool live = sp0 + x * G < L.nsplit;
                         while (live && (static_cast<uint32_t>(a[x]) == 0u || (b[x] >> 32) == 0u)) {
-                            __nanosleep(32);
                             a[x] = ld_relaxed_gpu_b64(pb[x]);
                             b[x] = ld_relaxed_gpu_b64(pb[x] + 1);
                         }
