@@ -534,6 +534,8 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
     // by a butterfly of shuffles -- a handful of dependent steps instead of one
     // thread walking every split (measured ~2 us of the configs[1] step).
     const float* P = L.partial + static_cast<int64_t>(u) * L.nsplit * stride_p;
+    // output staging past the merge scratch (free after the loop; up to gqa x d floats)
+    float* const s_stage = s_l + NW * kMaxGqa;
     auto combine_slice = [&](int lo, int hi) {
         constexpr float kLog2e = 1.4426950408889634f;
         const int ncols = hi - lo;
@@ -613,7 +615,10 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
             }
             if (!valid || r != 0) continue;
             if (L.out_mode == 0) {
-                L.out[(static_cast<int64_t>(u) * L.q_rows + qq) * kHeadDim + c] = acc / lsum;
+                // staged, then written by consecutive lanes: full 128-byte lines
+                // instead of a 16-byte piece per warp (out may be pinned host
+                // memory: one PCIe write per line, DecodePlan(host_io))
+                s_stage[idx - lo] = acc / lsum;
             } else {
                 float* po = L.out + (static_cast<int64_t>(u) * L.q_rows + qq) * (kHeadDim + 2);
                 po[c] = acc;
@@ -622,6 +627,12 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
                     po[kHeadDim + 1] = lsum;
                 }
             }
+        }
+        if (L.out_mode == 0) {
+            __syncthreads();
+            for (int idx = lo + static_cast<int>(threadIdx.x); idx < hi; idx += nthr)
+                L.out[(static_cast<int64_t>(u) * L.q_rows + idx / kHeadDim) * kHeadDim + idx % kHeadDim] =
+                    s_stage[idx - lo];
         }
     };
     if (mbox) {
@@ -634,8 +645,9 @@ __global__ void __launch_bounds__(32 * NW) decode_kernel(const __grid_constant__
         }
         if (ct && threadIdx.x == 0) ct[5] = globaltimer();
         const int n = gqa * kHeadDim;
-        combine_slice(static_cast<int>(static_cast<int64_t>(n) * split / L.nsplit),
-                      static_cast<int>(static_cast<int64_t>(n) * (split + 1) / L.nsplit));
+        // slices on 32-column (128-byte) boundaries: whole output lines per CTA
+        auto cut = [&](int sp) { return static_cast<int>(static_cast<int64_t>(n / 32) * sp / L.nsplit) * 32; };
+        combine_slice(cut(split), split == L.nsplit - 1 ? n : cut(split + 1));
         if (ct && threadIdx.x == 0) ct[10] = ct[4] = globaltimer();
         return;
     }
