@@ -18,9 +18,11 @@
 //          "RelayoutFragment"); bf16 P as a hi+lo pair
 //   GEMM2  mma.sp m16n8k32  V^T nnz [128 ch x 32] x P^T
 // Dense blocks take the dense m16n8k16 path.  Warps, then CTAs of a unit,
-// merge (m, l, O) with the reference combine: cooperatively (every CTA merges a
-// slice once the unit's partials are in) when the grid is resident, otherwise
-// in the unit's last CTA.
+// merge (m, l, O) with the reference combine: cooperatively when the grid is
+// resident (every CTA publishes its partial through a tagged mailbox -- slots
+// that carry their own validity -- and merges a 32-column slice once the
+// unit's partials are in), otherwise in the unit's last CTA.  The 1-D grid
+// interleaves units so each unit's splits span every GPC.
 #include <map>
 #include <mutex>
 #include <utility>
