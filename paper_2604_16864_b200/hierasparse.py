@@ -386,13 +386,14 @@ def _recompress_into(c, cfg, sparsity, out, check, status, with_losses=False):
 
 
 def absorb_tail(c: DeviceCompressedCache, tail: torch.Tensor, cfg: SparsityConfig, sparsity: float,
-                check: bool = True, status: StatusWord | None = None):
+                check: bool = True, status: StatusWord | None = None, with_losses: bool = False):
     """Dense-tail growth during decode: once the dense tail
     (CacheView::dense_tail, attention.hpp:19-31) holds whole blocks, re-prune the
     cache over its blocks followed by those tail blocks -- prune_cache + compress
     of [decompress(c); tail blocks] -- in one pass (hs_absorb_tail).  tail:
     [units, T, d] tokens after the cache.  Returns (cache, remaining tail of
-    T % block_size tokens); with no whole block the inputs come back unchanged."""
+    T % block_size tokens); with no whole block the inputs come back unchanged.
+    Block losses only when the selection ranks them, unless with_losses (as prune_cache)."""
     U, d, B = c.n_units, c.head_dim, c.block_size
     tail = tail.reshape(U, -1, d)
     full = (tail.shape[1] // B) * B
@@ -404,12 +405,13 @@ def absorb_tail(c: DeviceCompressedCache, tail: torch.Tensor, cfg: SparsityConfi
         tail = tail.contiguous()
     src = tail[:, :full]  # unit stride = the whole tail's; rows contiguous
     rows = c.logical_blocks * B + full
-    nb, dc, sc, _, _ = pool_counts(rows, cfg, sparsity)
+    nb, dc, sc, pre, suf = pool_counts(rows, cfg, sparsity)
     out = DeviceCompressedCache(c.dtype, c.axis, U, nb, dc, sc, c.index_map.device, d, cfg.block_size, cfg)
     cc = cfg.c()
     st = _status(status, out.index_map.device)
+    lp = out.losses.data_ptr() if with_losses or not _static_selection(nb, sc, pre, suf) else None
     capi.check(capi.load().hs_absorb_tail(c.cref(), src.data_ptr(), _unit_stride(src), full, C.byref(cc),
-                                          sparsity, out.cref(), out.losses.data_ptr(), out.flags.data_ptr(),
+                                          sparsity, out.cref(), lp, out.flags.data_ptr(),
                                           st.ptr(), _stream()))
     out.status = st
     if check:
@@ -418,10 +420,10 @@ def absorb_tail(c: DeviceCompressedCache, tail: torch.Tensor, cfg: SparsityConfi
 
 
 def absorb_tail_pair(k: DeviceCompressedCache, v: DeviceCompressedCache, k_tail: torch.Tensor,
-                     v_tail: torch.Tensor, cfg: SparsityConfig):
+                     v_tail: torch.Tensor, cfg: SparsityConfig, with_losses: bool = False):
     """absorb_tail for the key (S_K, channel groups) and value (S_V, sequence groups) caches."""
-    k2, kt = absorb_tail(k, k_tail, cfg, cfg.s_key)
-    v2, vt = absorb_tail(v, v_tail, cfg, cfg.s_value)
+    k2, kt = absorb_tail(k, k_tail, cfg, cfg.s_key, with_losses=with_losses)
+    v2, vt = absorb_tail(v, v_tail, cfg, cfg.s_value, with_losses=with_losses)
     return k2, v2, kt, vt
 
 

@@ -417,7 +417,7 @@ def test_absorb_tail_matches_oracle(hs, port, dtype, s_dec, tail_rows):
     kt, vt = to_torch(kx, dtype), to_torch(vx, dtype)
     kc, vc = hs.prune_cache(kt[:, :L].contiguous(), vt[:, :L].contiguous(), hs.SparsityConfig(0.5, 0.5, 64))
     cfg = hs.SparsityConfig(s_dec, s_dec, 64, sink_tokens=64)
-    k2, v2, krest, vrest = hs.absorb_tail_pair(kc, vc, kt[:, L:], vt[:, L:], cfg)
+    k2, v2, krest, vrest = hs.absorb_tail_pair(kc, vc, kt[:, L:], vt[:, L:], cfg, with_losses=True)
     full = (tail_rows // 64) * 64
     assert k2.logical_blocks == (L + full) // 64 and krest.shape[1] == tail_rows - full
     assert torch.equal(krest.view(torch.int16), kt[:, L + full:].view(torch.int16))
